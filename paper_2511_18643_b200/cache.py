@@ -1,0 +1,354 @@
+"""Cache runtime on the device: the batched Kitty KV store and the decode step.
+
+``KittyBatchCache`` is the product surface: B sequences x h_kv KV heads whose
+pages live in HBM (layout: include/kitty_b200.h, KittyCacheDesc).  One decode
+step is ``append`` (insert_token + maybe_pack, cache.py:107-178) followed by
+``attend`` (cache.py:217-252); both are single asynchronous launches on the
+current stream and can be captured in a CUDA graph.
+
+``KittyCacheState`` keeps the reference's single-sequence class name and
+methods (cache.py:83-252) on top of a batch of one, so tests written against
+``kittykv`` run unchanged (inputs are stored as bf16, like the paper's FP16
+system; pass bf16-representable values for bit-exact comparisons).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import PASSTHROUGH_BITS, KittyConfig
+from .errors import KittyError
+from .pages import _device, _stream, key_slot_bytes, serialize_slot, value_slot_bytes
+
+
+@dataclass(frozen=True)
+class AttentionOutput:
+    """cache.py:33-38."""
+
+    outputs: np.ndarray
+    probs: np.ndarray | None = None
+
+
+def component_counts(cfg: KittyConfig, length: int) -> dict:
+    """Occupancy of every component after ``length`` tokens (analysis.py:301-315)."""
+    sink = min(length, cfg.s)
+    past = max(0, length - cfg.s)
+    kp, kq = divmod(past, cfg.g)
+    local = min(cfg.r, past)
+    vp, vq = divmod(past - local, cfg.g)
+    return dict(sink=sink, key_pages=kp, key_qbuf=kq, local=local, value_pages=vp, value_qbuf=vq)
+
+
+def _check_device_config(cfg: KittyConfig):
+    if cfg.key_bits == PASSTHROUGH_BITS or cfg.value_bits == PASSTHROUGH_BITS:
+        raise KittyError("pass-through (16-bit) pages are not built on the device (key/value bits must be 2)")
+    if cfg.heuristic != "magnitude":
+        raise KittyError("the device pack path implements the magnitude heuristic only")
+
+
+class KittyBatchCache:
+    """B sequences of Kitty KV cache for one attention layer, resident in HBM."""
+
+    def __init__(self, cfg: KittyConfig, num_seqs: int, max_tokens: int, device=None):
+        _check_device_config(cfg)
+        self.lib = _lib.load_library()
+        _lib.check(self.lib.kitty_validate_config(ctypes.byref(cfg.to_c())), "config")
+        self.cfg = cfg
+        self.num_seqs = int(num_seqs)
+        self.device = torch.device(device) if device is not None else _device()
+        self.units = self.num_seqs * cfg.h_kv
+        self.key_slot = key_slot_bytes(cfg.d, cfg.g, cfg.d_boost)
+        self.value_slot = value_slot_bytes(cfg.d, cfg.g)
+        self.lengths = [0] * self.num_seqs  # host mirror of unit_len (no syncs needed)
+        self.key_pack_events = [0] * self.num_seqs
+        self.value_pack_events = [0] * self.num_seqs
+        self._alloc(max_tokens)
+        self._ws = None
+
+    # -- storage -------------------------------------------------------------
+
+    def _alloc(self, max_tokens: int):
+        cfg, dev, u = self.cfg, self.device, self.units
+        self.max_tokens = int(max_tokens)
+        self.max_pages = max(1, -(-max(0, self.max_tokens - cfg.s) // cfg.g))
+        bf = torch.bfloat16
+        self.unit_len = torch.zeros(u, dtype=torch.int32, device=dev)
+        self.k_sink = torch.zeros((u, cfg.s, cfg.d), dtype=bf, device=dev)
+        self.v_sink = torch.zeros((u, cfg.s, cfg.d), dtype=bf, device=dev)
+        self.k_qbuf = torch.zeros((u, cfg.g, cfg.d), dtype=bf, device=dev)
+        self.v_ring = torch.zeros((u, cfg.r + cfg.g, cfg.d), dtype=bf, device=dev)
+        self.key_pool = torch.zeros((u * self.max_pages, self.key_slot), dtype=torch.uint8, device=dev)
+        self.value_pool = torch.zeros((u * self.max_pages, self.value_slot), dtype=torch.uint8, device=dev)
+        ident = torch.arange(u * self.max_pages, dtype=torch.int32, device=dev).view(u, self.max_pages)
+        self.key_block_table = ident.clone()
+        self.value_block_table = ident.clone()
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._build_desc()
+
+    def _build_desc(self):
+        d = _lib.KittyCacheDesc()
+        d.cfg = self.cfg.to_c()
+        d.num_seqs = self.num_seqs
+        d.max_pages = self.max_pages
+        d.key_slot_bytes = self.key_slot
+        d.value_slot_bytes = self.value_slot
+        d.unit_len = self.unit_len.data_ptr()
+        d.k_sink = self.k_sink.data_ptr()
+        d.v_sink = self.v_sink.data_ptr()
+        d.k_qbuf = self.k_qbuf.data_ptr()
+        d.v_ring = self.v_ring.data_ptr()
+        d.key_pool = self.key_pool.data_ptr()
+        d.value_pool = self.value_pool.data_ptr()
+        d.key_block_table = self.key_block_table.data_ptr()
+        d.value_block_table = self.value_block_table.data_ptr()
+        d.status = self.status.data_ptr()
+        self.desc = d
+        self._desc_ref = ctypes.byref(d)
+
+    def grow(self, max_tokens: int):
+        """Re-allocate for longer sequences, keeping every page and row."""
+        old = dict(kp=self.key_pool, vp=self.value_pool, ln=self.unit_len, ks=self.k_sink,
+                   vs=self.v_sink, kq=self.k_qbuf, vr=self.v_ring, mp=self.max_pages,
+                   kbt=self.key_block_table, vbt=self.value_block_table, st=self.status)
+        self._alloc(max_tokens)
+        u = self.units
+        kv = self.key_pool.view(u, self.max_pages, -1)
+        vv = self.value_pool.view(u, self.max_pages, -1)
+        kv[:, : old["mp"]] = old["kp"][old["kbt"].reshape(-1).long()].view(u, old["mp"], -1)
+        vv[:, : old["mp"]] = old["vp"][old["vbt"].reshape(-1).long()].view(u, old["mp"], -1)
+        for name, key in (("unit_len", "ln"), ("k_sink", "ks"), ("v_sink", "vs"), ("k_qbuf", "kq"),
+                          ("v_ring", "vr"), ("status", "st")):
+            getattr(self, name).copy_(old[key])
+        self._ws = None
+
+    def workspace(self, max_tokens: int) -> torch.Tensor:
+        need = int(self.lib.kitty_attention_workspace_bytes(self._desc_ref, max_tokens))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(max(need, 16), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    # -- decode step -----------------------------------------------------------
+
+    def _count_events(self, b: int, n_after: int):
+        cfg = self.cfg
+        past = max(0, n_after - cfg.s)
+        if past and past % cfg.g == 0:
+            self.key_pack_events[b] += 1
+        vtot = max(0, past - cfg.r)
+        if vtot and vtot % cfg.g == 0:
+            self.value_pack_events[b] += 1
+
+    def append(self, k_new: torch.Tensor, v_new: torch.Tensor):
+        """Step 1 + step 3 for every sequence: k_new/v_new [B, h_kv, D] bf16."""
+        cfg = self.cfg
+        if max(self.lengths) + 1 > self.max_tokens:
+            self.grow(max(2 * self.max_tokens, max(self.lengths) + 1))
+        k_new = self._rows(k_new, (self.num_seqs, cfg.h_kv, cfg.d), "k_new")
+        v_new = self._rows(v_new, (self.num_seqs, cfg.h_kv, cfg.d), "v_new")
+        _lib.check(self.lib.kitty_append(self._desc_ref, k_new.data_ptr(), v_new.data_ptr(), _stream()), "append")
+        for b in range(self.num_seqs):
+            self.lengths[b] += 1
+            self._count_events(b, self.lengths[b])
+
+    def prefill(self, keys: torch.Tensor, values: torch.Tensor):
+        """cache.py:125-142 for an empty batch: keys/values [B, h_kv, P, D]."""
+        if any(self.lengths):
+            raise KittyError("prefill requires an empty state")
+        cfg = self.cfg
+        p = keys.shape[2]
+        if p > self.max_tokens:
+            self.grow(p)
+        keys = self._rows(keys, (self.num_seqs, cfg.h_kv, p, cfg.d), "keys")
+        values = self._rows(values, (self.num_seqs, cfg.h_kv, p, cfg.d), "values")
+        _lib.check(self.lib.kitty_prefill(self._desc_ref, keys.data_ptr(), values.data_ptr(), p, _stream()), "prefill")
+        for b in range(self.num_seqs):
+            for n in range(1, p + 1):
+                self._count_events(b, n)
+            self.lengths[b] = p
+
+    def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.bfloat16) -> torch.Tensor:
+        """Step 2 for every sequence: q [B, h_q, D] bf16 -> [B, h_q, D]."""
+        cfg = self.cfg
+        if min(self.lengths) == 0:
+            raise KittyError("attend on an empty cache")
+        q = self._rows(q, (self.num_seqs, cfg.h_q, cfg.d), "q")
+        if out is None:
+            out = torch.empty((self.num_seqs, cfg.h_q, cfg.d), dtype=out_dtype, device=self.device)
+        code = _lib.KITTY_F32 if out.dtype == torch.float32 else _lib.KITTY_BF16
+        max_tokens = max(self.lengths)
+        ws = self.workspace(max_tokens)
+        _lib.check(
+            self.lib.kitty_decode_attention(self._desc_ref, q.data_ptr(), out.data_ptr(), code, max_tokens,
+                                            ws.data_ptr(), ws.numel(), _stream()),
+            "attend",
+        )
+        return out
+
+    def check(self):
+        """Synchronise and raise for any data-dependent error a kernel reported."""
+        torch.cuda.current_stream().synchronize()
+        _lib.raise_status(int(self.status.item()) & 0xFFFFFFFF, "cache")
+
+    def _rows(self, t, shape, what):
+        if not isinstance(t, torch.Tensor):
+            t = torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32))
+        if tuple(t.shape) != tuple(shape):
+            raise KittyError(f"{what} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+        return t.to(device=self.device, dtype=torch.bfloat16).contiguous()
+
+    # -- readout ------------------------------------------------------------------
+
+    def flatten(self, b: int, h: int):
+        """flatten_keys / flatten_values (cache.py:210-215) -> float32 [n, D] each."""
+        n = self.lengths[b]
+        u = b * self.cfg.h_kv + h
+        ko = torch.empty((n, self.cfg.d), dtype=torch.float32, device=self.device)
+        vo = torch.empty((n, self.cfg.d), dtype=torch.float32, device=self.device)
+        _lib.check(self.lib.kitty_flatten(self._desc_ref, u, n, ko.data_ptr(), vo.data_ptr(), _stream()), "flatten")
+        return ko, vo
+
+    def page_counts(self, b: int) -> dict:
+        return component_counts(self.cfg, self.lengths[b])
+
+    def key_page_slots(self, b: int, h: int) -> torch.Tensor:
+        """Device slots (KTYP key bodies) of (b, h) in page order."""
+        c = self.page_counts(b)
+        u = b * self.cfg.h_kv + h
+        idx = self.key_block_table[u, : c["key_pages"]].long()
+        return self.key_pool[idx]
+
+    def value_page_slots(self, b: int, h: int) -> torch.Tensor:
+        c = self.page_counts(b)
+        u = b * self.cfg.h_kv + h
+        idx = self.value_block_table[u, : c["value_pages"]].long()
+        return self.value_pool[idx]
+
+    def export_pages(self, b: int, h: int):
+        """KTYP byte strings of all pages of (b, h): header + memcpy of each slot."""
+        cfg = self.cfg
+        ks = self.key_page_slots(b, h).cpu().numpy()
+        vs = self.value_page_slots(b, h).cpu().numpy()
+        return ([serialize_slot(s.tobytes(), "key", cfg.d, cfg.g, cfg.d_boost) for s in ks],
+                [serialize_slot(s.tobytes(), "value", cfg.d, cfg.g) for s in vs])
+
+    def hbm_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (
+            self.k_sink, self.v_sink, self.k_qbuf, self.v_ring, self.key_pool, self.value_pool))
+
+
+class KittyCacheState:
+    """The reference's per-sequence state (cache.py:83-252) on the device."""
+
+    def __init__(self, cfg: KittyConfig, max_tokens: int = 1024):
+        _check_device_config(cfg)
+        self.cfg = cfg
+        self._b = KittyBatchCache(cfg, 1, max_tokens)
+
+    @property
+    def total_tokens(self) -> int:
+        return self._b.lengths[0]
+
+    @property
+    def key_pack_events(self) -> int:
+        return self._b.key_pack_events[0]
+
+    @property
+    def value_pack_events(self) -> int:
+        return self._b.value_pack_events[0]
+
+    @property
+    def batch(self) -> KittyBatchCache:
+        return self._b
+
+    def _coerce_rows(self, new, what):
+        new = np.asarray(new.cpu() if isinstance(new, torch.Tensor) else new, dtype=np.float32)
+        if new.ndim == 1:
+            new = new[None, :]
+        if new.shape != (self.cfg.h_kv, self.cfg.d):
+            raise KittyError(f"{what} must have shape ({self.cfg.h_kv}, {self.cfg.d}), got {new.shape}")
+        return torch.from_numpy(new)[None]
+
+    def insert_token(self, k_new, v_new) -> None:
+        """cache.py:107-123 (pack fires inside, before any attend)."""
+        self._b.append(self._coerce_rows(k_new, "k_new"), self._coerce_rows(v_new, "v_new"))
+        self._b.check()
+
+    def prefill(self, keys, values) -> None:
+        """cache.py:125-142."""
+        if self.total_tokens != 0:
+            raise KittyError("prefill requires an empty state")
+        keys = np.asarray(keys, dtype=np.float32)
+        values = np.asarray(values, dtype=np.float32)
+        if keys.ndim == 2:
+            keys = keys[None]
+        if values.ndim == 2:
+            values = values[None]
+        if keys.shape != values.shape or keys.shape[0] != self.cfg.h_kv:
+            raise KittyError("prefill keys/values must be (h_kv, P, d) with equal shapes")
+        if keys.shape[1] == 0:
+            return
+        self._b.prefill(torch.from_numpy(keys)[None], torch.from_numpy(values)[None])
+        self._b.check()
+
+    def maybe_pack(self) -> int:
+        """cache.py:144-178: packing already ran inside insert; nothing is pending."""
+        return 0
+
+    def flatten_keys(self, kv_head: int = 0) -> np.ndarray:
+        return self._b.flatten(0, kv_head)[0].cpu().numpy()
+
+    def flatten_values(self, kv_head: int = 0) -> np.ndarray:
+        return self._b.flatten(0, kv_head)[1].cpu().numpy()
+
+    def attend(self, q, return_probs: bool = False) -> AttentionOutput:
+        """cache.py:217-252 on the device (fused dequant-attention)."""
+        if self.total_tokens == 0:
+            raise KittyError("attend on an empty cache")
+        if return_probs:
+            raise KittyError("return_probs is a debug output the fused kernel never materialises")
+        q = np.asarray(q.cpu() if isinstance(q, torch.Tensor) else q, dtype=np.float32)
+        if q.ndim == 1:
+            q = q[None, :]
+        if q.shape != (self.cfg.h_q, self.cfg.d):
+            raise KittyError(f"q must have shape ({self.cfg.h_q}, {self.cfg.d}), got {q.shape}")
+        out = self._b.attend(torch.from_numpy(q)[None], out_dtype=torch.float32)
+        return AttentionOutput(outputs=out[0].cpu().numpy())
+
+    def export_pages(self, kv_head: int = 0):
+        return self._b.export_pages(0, kv_head)
+
+
+def oracle_attend(keys, values, queries, kv_head_map=None) -> AttentionOutput:
+    """cache.py:261-301: dense float32 attention, run on the device."""
+    lib = _lib.load_library()
+    dev = _device()
+    keys = np.asarray(keys, dtype=np.float32)
+    values = np.asarray(values, dtype=np.float32)
+    queries = np.asarray(queries, dtype=np.float32)
+    if queries.ndim == 1:
+        queries = queries[None, :]
+    if keys.ndim == 2:
+        keys, values = keys[None], values[None]
+    if keys.shape != values.shape:
+        raise KittyError("keys and values must have matching shapes")
+    h_kv, length, d = keys.shape
+    if length == 0:
+        raise KittyError("attention over zero tokens")
+    n_q = queries.shape[0]
+    if kv_head_map is None:
+        kv_head_map = [i * h_kv // n_q for i in range(n_q)]
+    k = torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
+    v = torch.from_numpy(np.ascontiguousarray(values)).to(dev)
+    qs = torch.from_numpy(np.ascontiguousarray(queries)).to(dev)
+    kmap = torch.tensor(list(kv_head_map), dtype=torch.int32, device=dev)
+    out = torch.empty((n_q, d), dtype=torch.float32, device=dev)
+    ws = torch.empty(max(16, int(lib.kitty_dense_attention_workspace_bytes(n_q, length, d))), dtype=torch.uint8, device=dev)
+    _lib.check(lib.kitty_dense_attention(k.data_ptr(), v.data_ptr(), h_kv, length, d, qs.data_ptr(), n_q,
+                                         kmap.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream()),
+               "oracle_attend")
+    return AttentionOutput(outputs=out.cpu().numpy())

@@ -1,0 +1,263 @@
+// Decode attention over the heterogeneous Kitty store (K4/K5) and the dense
+// fp32 oracle_attend on device.
+//
+// This file holds the GENERIC split-KV path: any (s, r, g, d, group) the
+// reference config accepts.  Pages are dequantised on the fly per element
+// (Alg. 1 semantics, mul-then-add), logits are float32 / float32(sqrt(d))
+// (cache.py:241), softmax is max-subtracted (cache.py:255-258) per split and
+// merged across splits by log-sum-exp.  The specialised tensor-core kernel for
+// d = g = 128 lives in kitty_attention_fast.cu and is dispatched from
+// launch_decode_attention.
+#include "kitty_attention.cuh"
+#include "kitty_codec.cuh"
+
+namespace kitty {
+
+constexpr int kGenericChunk = 256;  // tokens per split of the generic path
+constexpr int kGenericThreads = 128;
+
+// Reads K/V elements of one unit in global token order (cache.py:12-15).
+struct CacheSource {
+    KittyCacheDesc c;
+    int u, n, kp, vp;
+    __device__ void init(const KittyCacheDesc& cd, int unit) {
+        c = cd;
+        u = unit;
+        n = cd.unit_len[unit];
+        const int past = n > cd.cfg.s ? n - cd.cfg.s : 0;
+        kp = past / cd.cfg.g;
+        vp = (past - min(cd.cfg.r, past)) / cd.cfg.g;
+    }
+    __device__ float key(int t, int ch) const {
+        const int d = c.cfg.d, S = c.cfg.s, G = c.cfg.g;
+        if (t < S) return bf16_to_f32(c.k_sink[((int64_t)u * S + t) * d + ch]);
+        const int pc = t - S;
+        if (pc < kp * G) {
+            const int p = pc / G, tl = pc % G, gb = G / 4;
+            const KeyLayout L{d, G, c.cfg.d_boost};
+            const uint8_t* slot = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes;
+            uint32_t code = (slot[L.dense_off() + ch * gb + tl / 4] >> (2 * (tl % 4))) & 3u;
+            const uint8_t r = slot[L.idx_off() + ch];
+            if (r != kSentinel) code |= ((slot[L.high_off() + r * gb + tl / 4] >> (2 * (tl % 4))) & 3u) << 2;
+            const float s = half_bits_to_f32(ld_u16(slot + L.scale_off() + 2 * ch));
+            const float z = half_bits_to_f32(ld_u16(slot + L.zero_off() + 2 * ch));
+            return __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
+        }
+        return bf16_to_f32(c.k_qbuf[((int64_t)u * G + pc % G) * d + ch]);
+    }
+    __device__ float val(int t, int ch) const {
+        const int d = c.cfg.d, S = c.cfg.s, G = c.cfg.g, W = c.cfg.r + c.cfg.g;
+        if (t < S) return bf16_to_f32(c.v_sink[((int64_t)u * S + t) * d + ch]);
+        const int pc = t - S;
+        if (pc < vp * G) {
+            const int p = pc / G, tl = pc % G;
+            const ValueLayout L{d, G};
+            const uint8_t* slot = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes;
+            const uint32_t code = (slot[L.codes_off() + tl * (d / 4) + ch / 4] >> (2 * (ch % 4))) & 3u;
+            const float s = half_bits_to_f32(ld_u16(slot + L.scale_off() + 2 * tl));
+            const float z = half_bits_to_f32(ld_u16(slot + L.zero_off() + 2 * tl));
+            return __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
+        }
+        return bf16_to_f32(c.v_ring[((int64_t)u * W + pc % W) * d + ch]);
+    }
+};
+
+struct DenseSource {
+    const float* k;
+    const float* v;
+    int d, n;
+    __device__ float key(int t, int ch) const { return k[(int64_t)t * d + ch]; }
+    __device__ float val(int t, int ch) const { return v[(int64_t)t * d + ch]; }
+};
+
+// One CTA = one (unit, split): tokens [split * chunk, min(n, (split + 1) * chunk)).
+// Writes the split's max m, sum l and unnormalised accumulator to the workspace.
+template <typename Src>
+__device__ void attend_split(const Src& src, int n, int d, int group, const float* qs,
+                             float sqrt_d, float* logit, float* ws_acc, float* ws_ml) {
+    const int split = blockIdx.x;
+    const int t0 = split * kGenericChunk;
+    const int t1 = min(n, t0 + kGenericChunk);
+    const int cnt = t1 - t0;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    if (cnt <= 0) {
+        for (int g = tid; g < group; g += nt) {
+            ws_ml[2 * g] = -INFINITY;
+            ws_ml[2 * g + 1] = 0.f;
+        }
+        for (int i = tid; i < group * d; i += nt) ws_acc[i] = 0.f;
+        return;
+    }
+    // logits (cache.py:241): float32 dot products / float32(sqrt(d))
+    for (int i = tid; i < cnt; i += nt) {
+        const int t = t0 + i;
+        for (int g0 = 0; g0 < group; g0 += 8) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const int gn = min(8, group - g0);
+            for (int ch = 0; ch < d; ++ch) {
+                const float kv = src.key(t, ch);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < gn) acc[j] = fmaf(qs[(g0 + j) * d + ch], kv, acc[j]);
+            }
+            for (int j = 0; j < gn; ++j) logit[(g0 + j) * kGenericChunk + i] = __fdiv_rn(acc[j], sqrt_d);
+        }
+    }
+    __syncthreads();
+    // max-subtracted exponentials (cache.py:255-258), one warp per query row
+    for (int g = warp; g < group; g += nw) {
+        float* row = logit + g * kGenericChunk;
+        float m = -INFINITY;
+        for (int i = lane; i < cnt; i += 32) m = fmaxf(m, row[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float l = 0.f;
+        for (int i = lane; i < cnt; i += 32) {
+            const float e = expf(row[i] - m);
+            row[i] = e;
+            l += e;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+        if (lane == 0) {
+            ws_ml[2 * g] = m;
+            ws_ml[2 * g + 1] = l;
+        }
+    }
+    __syncthreads();
+    // p^T @ V over the split (cache.py:245-248)
+    for (int i = tid; i < group * d; i += nt) {
+        const int g = i / d, ch = i % d;
+        const float* p = logit + g * kGenericChunk;
+        float acc = 0.f;
+        for (int j = 0; j < cnt; ++j) acc = fmaf(p[j], src.val(t0 + j, ch), acc);
+        ws_acc[i] = acc;
+    }
+}
+
+__global__ void attention_generic_kernel(KittyCacheDesc c, const uint16_t* q, int splits,
+                                         float* ws_acc, float* ws_ml) {
+    extern __shared__ __align__(16) float gsm[];
+    const int u = blockIdx.y;
+    const int d = c.cfg.d, group = c.cfg.h_q / c.cfg.h_kv;
+    const int b = u / c.cfg.h_kv, h = u % c.cfg.h_kv;
+    float* qs = gsm;                    // [group][d]
+    float* logit = gsm + group * d;     // [group][chunk]
+    const uint16_t* qg = q + ((int64_t)b * c.cfg.h_q + (int64_t)h * group) * d;
+    for (int i = threadIdx.x; i < group * d; i += blockDim.x) qs[i] = bf16_to_f32(qg[i]);
+    CacheSource src;
+    src.init(c, u);
+    __syncthreads();
+    const float sqrt_d = static_cast<float>(sqrt(static_cast<double>(d)));
+    const int64_t slot = (int64_t)u * splits + blockIdx.x;
+    attend_split(src, src.n, d, group, qs, sqrt_d, logit, ws_acc + slot * group * d,
+                 ws_ml + slot * group * 2);
+}
+
+__global__ void attention_dense_kernel(const float* keys, const float* values, int length, int d,
+                                       const float* queries, const int32_t* kv_map, int splits,
+                                       float* ws_acc, float* ws_ml) {
+    extern __shared__ __align__(16) float gsm[];
+    const int i = blockIdx.y;  // query index: one "unit" per query (group 1)
+    float* qs = gsm;
+    float* logit = gsm + d;
+    for (int ch = threadIdx.x; ch < d; ch += blockDim.x) qs[ch] = queries[(int64_t)i * d + ch];
+    const int h = kv_map[i];
+    DenseSource src{keys + (int64_t)h * length * d, values + (int64_t)h * length * d, d, length};
+    __syncthreads();
+    const float sqrt_d = static_cast<float>(sqrt(static_cast<double>(d)));
+    const int64_t slot = (int64_t)i * splits + blockIdx.x;
+    attend_split(src, length, d, 1, qs, sqrt_d, logit, ws_acc + slot * d, ws_ml + slot * 2);
+}
+
+// K5: log-sum-exp merge of the splits of every (unit, query row).
+// out row r of unit u goes to out_base(u) + r * d.
+__global__ void combine_kernel(const float* ws_acc, const float* ws_ml, int splits, int group,
+                               int d, int h_kv, int h_q, int dense, void* out, int out_dtype) {
+    const int u = blockIdx.x;
+    for (int i = threadIdx.x; i < group * d; i += blockDim.x) {
+        const int g = i / d, ch = i % d;
+        float m = -INFINITY;
+        for (int s = 0; s < splits; ++s) m = fmaxf(m, ws_ml[(((int64_t)u * splits + s) * group + g) * 2]);
+        float l = 0.f, acc = 0.f;
+        for (int s = 0; s < splits; ++s) {
+            const int64_t base = ((int64_t)u * splits + s) * group + g;
+            const float ms = ws_ml[base * 2];
+            if (ms == -INFINITY) continue;
+            const float w = expf(ms - m);
+            l += ws_ml[base * 2 + 1] * w;
+            acc += ws_acc[base * d + ch] * w;
+        }
+        const float o = acc / l;
+        int64_t row;
+        if (dense) {
+            row = u;
+        } else {
+            const int b = u / h_kv, h = u % h_kv;
+            row = (int64_t)b * h_q + (int64_t)h * group + g;
+        }
+        if (out_dtype == KITTY_F32)
+            static_cast<float*>(out)[row * d + ch] = o;
+        else
+            static_cast<uint16_t*>(out)[row * d + ch] = f32_to_bf16_bits(o);
+    }
+}
+
+static int generic_splits(int max_tokens) {
+    return max_tokens <= 0 ? 1 : (max_tokens + kGenericChunk - 1) / kGenericChunk;
+}
+
+size_t attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
+    const int units = c.num_seqs * c.cfg.h_kv;
+    const int group = c.cfg.h_q / c.cfg.h_kv;
+    size_t generic = (size_t)units * generic_splits(max_tokens) * group * (c.cfg.d + 2) * sizeof(float);
+    size_t fast = fast_attention_workspace_bytes(c, max_tokens);
+    return generic > fast ? generic : fast;
+}
+
+cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, void* out,
+                                    int out_dtype, int max_tokens, void* ws, size_t ws_bytes,
+                                    cudaStream_t st) {
+    const int units = c.num_seqs * c.cfg.h_kv;
+    if (units == 0) return cudaSuccess;
+    if (fast_attention_supported(c)) return launch_fast_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
+    const int group = c.cfg.h_q / c.cfg.h_kv;
+    const int d = c.cfg.d;
+    const int splits = generic_splits(max_tokens);
+    const size_t need = (size_t)units * splits * group * (d + 2) * sizeof(float);
+    if (ws_bytes < need) return cudaErrorInvalidValue;
+    float* ws_acc = static_cast<float*>(ws);
+    float* ws_ml = ws_acc + (size_t)units * splits * group * d;
+    const size_t sm = ((size_t)group * d + (size_t)group * kGenericChunk) * sizeof(float);
+    cudaFuncSetAttribute(attention_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attention_generic_kernel<<<dim3(splits, units), kGenericThreads, sm, st>>>(c, q, splits, ws_acc, ws_ml);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    combine_kernel<<<units, 128, 0, st>>>(ws_acc, ws_ml, splits, group, d, c.cfg.h_kv, c.cfg.h_q, 0, out, out_dtype);
+    return cudaGetLastError();
+}
+
+size_t dense_attention_workspace_bytes(int n_q, int length, int d) {
+    return (size_t)n_q * generic_splits(length) * (d + 2) * sizeof(float);
+}
+
+cudaError_t launch_dense_attention(const float* keys, const float* values, int h_kv, int length,
+                                   int d, const float* queries, int n_q, const int32_t* kv_map,
+                                   float* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+    (void)h_kv;
+    if (n_q == 0) return cudaSuccess;
+    const int splits = generic_splits(length);
+    if (ws_bytes < dense_attention_workspace_bytes(n_q, length, d)) return cudaErrorInvalidValue;
+    float* ws_acc = static_cast<float*>(ws);
+    float* ws_ml = ws_acc + (size_t)n_q * splits * d;
+    const size_t sm = ((size_t)d + kGenericChunk) * sizeof(float);
+    cudaFuncSetAttribute(attention_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attention_dense_kernel<<<dim3(splits, n_q), kGenericThreads, sm, st>>>(keys, values, length, d, queries, kv_map, splits, ws_acc, ws_ml);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    combine_kernel<<<n_q, 128, 0, st>>>(ws_acc, ws_ml, splits, 1, d, 1, 1, 1, out, KITTY_F32);
+    return cudaGetLastError();
+}
+
+}  // namespace kitty

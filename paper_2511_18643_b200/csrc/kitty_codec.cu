@@ -1,0 +1,622 @@
+// Page codec and cache-runtime kernels: quantize + pack (K1/K2), dequantize
+// (K6), append with the fused pack trigger (K3) and bulk prefill.
+//
+// Bit-exactness: channel scores are a sequential fp64
+// sum in token order (quant.py:72); the quantizer uses IEEE float32 division
+// and round-half-even (quant.py:112-114); dequantisation is multiply-then-add
+// with no FMA contraction (quant.py:120, pages.py:143); f16 metadata is RNE.
+#include "kitty_codec.cuh"
+
+namespace kitty {
+
+// ---------------------------------------------------------------------------
+// Block-level page packers.  `tile` holds the page rows in token order,
+// [g][d] (row = token), staged in shared memory by the caller.
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__device__ bool tile_all_finite(const T* tile, int n) {
+    int bad = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite(load_elem(tile, i));
+    return __syncthreads_or(bad) == 0;
+}
+
+// pack_key_page (pages.py:81-118) preceded, when `sel` is NULL, by
+// channel_scores + select_boost (cache.py:155-158).  Writes the KTYP body to
+// `slot_smem` (shared) and the f32 metadata to sc32/ze32 when non-NULL.
+template <typename T>
+__device__ void pack_key_tile(const T* tile, int g, int d, int d_boost, const int64_t* sel,
+                              uint8_t* slot_smem, PackScratch& sc, float* sc32, float* ze32) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const KeyLayout L{d, g, d_boost};
+    // boosted flags
+    if (sel) {
+        for (int c = tid; c < d; c += nt) sc.flag[c] = 0;
+        __syncthreads();
+        for (int j = tid; j < d_boost; j += nt) sc.flag[sel[j]] = 1;
+    } else {
+        // channel_scores (quant.py:64-72): sequential fp64 over tokens, / g
+        for (int c = tid; c < d; c += nt) {
+            double acc = 0.0;
+            for (int t = 0; t < g; ++t) acc += static_cast<double>(fabsf(load_elem(tile, (int64_t)t * d + c)));
+            sc.score[c] = acc / static_cast<double>(g);
+        }
+        __syncthreads();
+        // select_boost (quant.py:93): stable top-k on -score
+        for (int c = tid; c < d; c += nt) {
+            const double s = sc.score[c];
+            int rank = 0;
+            for (int j = 0; j < d; ++j) {
+                const double o = sc.score[j];
+                rank += (o > s) || (o == s && j < c);
+            }
+            sc.flag[c] = rank < d_boost;
+        }
+    }
+    __syncthreads();
+    // high_bits row of each boosted channel: ascending channel order (pages.py:103)
+    for (int c = tid; c < d; c += nt) {
+        int pos = 0;
+        for (int j = 0; j < c; ++j) pos += sc.flag[j];
+        sc.pos[c] = pos;
+    }
+    __syncthreads();
+    // per-channel quantization (quant.py:102-116) and 2-bit packing (pages.py:42-45)
+    const int gb = g / 4;
+    uint8_t* dense = slot_smem + L.dense_off();
+    uint8_t* high = slot_smem + L.high_off();
+    uint8_t* idx = slot_smem + L.idx_off();
+    uint8_t* s16 = slot_smem + L.scale_off();
+    uint8_t* z16 = slot_smem + L.zero_off();
+    for (int c = tid; c < d; c += nt) {
+        float mn = load_elem(tile, c), mx = mn;
+        for (int t = 1; t < g; ++t) {
+            const float v = load_elem(tile, (int64_t)t * d + c);
+            mn = fminf(mn, v);
+            mx = fmaxf(mx, v);
+        }
+        const bool boosted = sc.flag[c] != 0;
+        const LaneQuant q(mn, mx, boosted ? 15.f : 3.f);
+        const int row = sc.pos[c];
+        for (int b = 0; b < gb; ++b) {
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t code = q.code(load_elem(tile, (int64_t)(4 * b + j) * d + c));
+                lo |= (code & 3u) << (2 * j);
+                hi |= (code >> 2) << (2 * j);
+            }
+            dense[c * gb + b] = static_cast<uint8_t>(lo);
+            if (boosted) high[row * gb + b] = static_cast<uint8_t>(hi);
+        }
+        idx[c] = boosted ? static_cast<uint8_t>(row) : kSentinel;
+        // f16 metadata: stored unaligned-safe (2-byte aligned by construction)
+        st_u16(s16 + 2 * c, f32_to_half_bits(q.scale));
+        st_u16(z16 + 2 * c, f32_to_half_bits(mn));
+        if (sc32) sc32[c] = q.scale;
+        if (ze32) ze32[c] = mn;
+    }
+    __syncthreads();
+}
+
+// pack_value_page (pages.py:146-162): per-token (row) quantization at 2 bits,
+// packed along channels.  One warp per token row.
+template <typename T>
+__device__ void pack_value_tile(const T* tile, int g, int d, uint8_t* slot_smem, float* sc32,
+                                float* ze32) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const ValueLayout L{d, g};
+    uint8_t* codes = slot_smem + L.codes_off();
+    uint8_t* s16 = slot_smem + L.scale_off();
+    uint8_t* z16 = slot_smem + L.zero_off();
+    const int db = d / 4;
+    for (int t = warp; t < g; t += nw) {
+        const T* row = tile + (int64_t)t * d;
+        float mn = INFINITY, mx = -INFINITY;
+        for (int c = lane; c < d; c += 32) {
+            const float v = load_elem(row, c);
+            mn = fminf(mn, v);
+            mx = fmaxf(mx, v);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        const LaneQuant q(mn, mx, 3.f);
+        for (int b = lane; b < db; b += 32) {
+            uint32_t byte = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) byte |= q.code(load_elem(row, 4 * b + j)) << (2 * j);
+            codes[t * db + b] = static_cast<uint8_t>(byte);
+        }
+        if (lane == 0) {
+            st_u16(s16 + 2 * t, f32_to_half_bits(q.scale));
+            st_u16(z16 + 2 * t, f32_to_half_bits(mn));
+            if (sc32) sc32[t] = q.scale;
+            if (ze32) ze32[t] = mn;
+        }
+    }
+    __syncthreads();
+}
+
+__device__ void copy_slot_out(const uint8_t* slot_smem, uint8_t* gslot, int bytes) {
+    if ((bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(gslot) & 15) == 0) {
+        const uint4* s = reinterpret_cast<const uint4*>(slot_smem);
+        uint4* o = reinterpret_cast<uint4*>(gslot);
+        for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x) o[i] = s[i];
+    } else {
+        for (int i = threadIdx.x; i < bytes; i += blockDim.x) gslot[i] = slot_smem[i];
+    }
+}
+
+// Stage g rows [start, start + g) of a row ring of size `wrap` into smem.
+template <typename T>
+__device__ void stage_rows(T* tile, const T* base, int start, int wrap, int g, int d) {
+    if (sizeof(T) == 2 && (d % 8) == 0) {
+        const int vpr = d / 8;  // uint4 per row
+        for (int i = threadIdx.x; i < g * vpr; i += blockDim.x) {
+            const int r = i / vpr, v = i % vpr;
+            const uint4* src = reinterpret_cast<const uint4*>(base + (int64_t)((start + r) % wrap) * d);
+            reinterpret_cast<uint4*>(tile + (int64_t)r * d)[v] = src[v];
+        }
+    } else {
+        for (int i = threadIdx.x; i < g * d; i += blockDim.x) {
+            const int r = i / d, c = i % d;
+            tile[i] = base[(int64_t)((start + r) % wrap) * d + c];
+        }
+    }
+    __syncthreads();
+}
+
+// Shared-memory budget of one pack (tile + slot + scratch), in bytes.
+__host__ __device__ size_t pack_smem_bytes(int g, int d, int d_boost, int elem_bytes) {
+    size_t tile = (size_t)g * d * elem_bytes;
+    tile = (tile + 15) & ~size_t(15);
+    size_t slot = (size_t)KeyLayout{d, g, d_boost}.bytes();
+    const size_t vslot = (size_t)ValueLayout{d, g}.bytes();
+    if (vslot > slot) slot = vslot;
+    slot = (slot + 15) & ~size_t(15);
+    return tile + slot + PackScratch::bytes(d);
+}
+
+__device__ PackScratch carve_scratch(uint8_t* p, int d) {
+    PackScratch s;
+    s.score = reinterpret_cast<double*>(p);
+    s.pos = reinterpret_cast<int*>(p + 8 * (size_t)d);
+    s.flag = reinterpret_cast<uint8_t*>(p + 12 * (size_t)d);
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// Standalone codec kernels (one CTA per page)
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void pack_key_pages_kernel(const T* x, int g, int d, int d_boost, const int64_t* sel,
+                                      uint8_t* slots, int64_t stride, float* sc32, float* ze32,
+                                      uint32_t* status) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int p = blockIdx.x;
+    T* tile = reinterpret_cast<T*>(smem);
+    size_t off = ((size_t)g * d * sizeof(T) + 15) & ~size_t(15);
+    uint8_t* slot = smem + off;
+    off += ((size_t)max(KeyLayout{d, g, d_boost}.bytes(), ValueLayout{d, g}.bytes()) + 15) & ~size_t(15);
+    PackScratch sc = carve_scratch(smem + off, d);
+    stage_rows(tile, x + (int64_t)p * g * d, 0, g, g, d);
+    if (!tile_all_finite(tile, g * d)) {
+        if (threadIdx.x == 0) set_status(status, KITTY_STATUS_NONFINITE);
+        return;
+    }
+    pack_key_tile(tile, g, d, d_boost, sel ? sel + (int64_t)p * d_boost : nullptr, slot, sc,
+                  sc32 ? sc32 + (int64_t)p * d : nullptr, ze32 ? ze32 + (int64_t)p * d : nullptr);
+    copy_slot_out(slot, slots + p * stride, KeyLayout{d, g, d_boost}.bytes());
+}
+
+template <typename T>
+__global__ void pack_value_pages_kernel(const T* x, int g, int d, uint8_t* slots, int64_t stride,
+                                        float* sc32, float* ze32, uint32_t* status) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int p = blockIdx.x;
+    T* tile = reinterpret_cast<T*>(smem);
+    uint8_t* slot = smem + (((size_t)g * d * sizeof(T) + 15) & ~size_t(15));
+    stage_rows(tile, x + (int64_t)p * g * d, 0, g, g, d);
+    if (!tile_all_finite(tile, g * d)) {
+        if (threadIdx.x == 0) set_status(status, KITTY_STATUS_NONFINITE);
+        return;
+    }
+    pack_value_tile(tile, g, d, slot, sc32 ? sc32 + (int64_t)p * g : nullptr,
+                    ze32 ? ze32 + (int64_t)p * g : nullptr);
+    copy_slot_out(slot, slots + p * stride, ValueLayout{d, g}.bytes());
+}
+
+template <typename T>
+__global__ void channel_scores_kernel(const T* x, int g, int d, double* scores) {
+    const int p = blockIdx.x;
+    const T* tile = x + (int64_t)p * g * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        double acc = 0.0;
+        for (int t = 0; t < g; ++t) acc += static_cast<double>(fabsf(load_elem(tile, (int64_t)t * d + c)));
+        scores[(int64_t)p * d + c] = acc / static_cast<double>(g);
+    }
+}
+
+__global__ void select_boost_kernel(const double* scores, int d, int k, int64_t* out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t* flag = smem;
+    const double* s = scores + (int64_t)blockIdx.x * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        const double v = s[c];
+        int rank = 0;
+        for (int j = 0; j < d; ++j) rank += (s[j] > v) || (s[j] == v && j < c);
+        flag[c] = rank < k;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        if (!flag[c]) continue;
+        int pos = 0;
+        for (int j = 0; j < c; ++j) pos += flag[j];
+        out[(int64_t)blockIdx.x * k + pos] = c;
+    }
+}
+
+// dequantize_key_page (pages.py:121-143): validate the sentinel pattern, then
+// X = low | high[boost_idx] << 2, out = X * scale + zero (mul then add).
+__global__ void dequant_key_pages_kernel(const uint8_t* slots, int64_t stride, int g, int d,
+                                         int d_boost, const float* sc32, const float* ze32,
+                                         float* out, uint32_t* status) {
+    __shared__ int seen[256];
+    __shared__ int total;
+    const int p = blockIdx.x;
+    const KeyLayout L{d, g, d_boost};
+    const uint8_t* slot = slots + p * stride;
+    const uint8_t* idx = slot + L.idx_off();
+    for (int j = threadIdx.x; j < 256; j += blockDim.x) seen[j] = 0;
+    if (threadIdx.x == 0) total = 0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        const uint8_t b = idx[c];
+        if (b != kSentinel) {
+            atomicAdd(&seen[b], 1);
+            atomicAdd(&total, 1);
+        }
+    }
+    __syncthreads();
+    int bad = total != d_boost;
+    for (int j = threadIdx.x; j < 256; j += blockDim.x) bad |= (j < d_boost) ? (seen[j] != 1) : (seen[j] != 0);
+    if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0) set_status(status, KITTY_STATUS_PAGE_FORMAT);
+        return;
+    }
+    const int gb = g / 4;
+    const uint8_t* dense = slot + L.dense_off();
+    const uint8_t* high = slot + L.high_off();
+    const uint8_t* s16 = slot + L.scale_off();
+    const uint8_t* z16 = slot + L.zero_off();
+    float* o = out + (int64_t)p * d * g;
+    for (int i = threadIdx.x; i < d * gb; i += blockDim.x) {
+        const int c = i / gb, b = i % gb;
+        const float s = sc32 ? sc32[(int64_t)p * d + c] : half_bits_to_f32(ld_u16(s16 + 2 * c));
+        const float z = ze32 ? ze32[(int64_t)p * d + c] : half_bits_to_f32(ld_u16(z16 + 2 * c));
+        const uint32_t lo = dense[c * gb + b];
+        const uint8_t r = idx[c];
+        const uint32_t hi = (r != kSentinel) ? high[r * gb + b] : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t code = ((lo >> (2 * j)) & 3u) | (((hi >> (2 * j)) & 3u) << 2);
+            o[(int64_t)c * g + 4 * b + j] = __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
+        }
+    }
+}
+
+__global__ void dequant_value_pages_kernel(const uint8_t* slots, int64_t stride, int g, int d,
+                                           const float* sc32, const float* ze32, float* out) {
+    const int p = blockIdx.x;
+    const ValueLayout L{d, g};
+    const uint8_t* slot = slots + p * stride;
+    const uint8_t* s16 = slot + L.scale_off();
+    const uint8_t* z16 = slot + L.zero_off();
+    const int db = d / 4;
+    float* o = out + (int64_t)p * g * d;
+    for (int i = threadIdx.x; i < g * db; i += blockDim.x) {
+        const int t = i / db, b = i % db;
+        const float s = sc32 ? sc32[(int64_t)p * g + t] : half_bits_to_f32(ld_u16(s16 + 2 * t));
+        const float z = ze32 ? ze32[(int64_t)p * g + t] : half_bits_to_f32(ld_u16(z16 + 2 * t));
+        const uint32_t byte = slot[L.codes_off() + t * db + b];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            o[(int64_t)t * d + 4 * b + j] =
+                __fadd_rn(__fmul_rn(static_cast<float>((byte >> (2 * j)) & 3u), s), z);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Cache runtime: append (insert_token + maybe_pack) and prefill
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void copy_row_bf16(uint16_t* dst, const uint16_t* src, int d) {
+    if ((d % 8) == 0) {
+        for (int i = threadIdx.x; i < d / 8; i += blockDim.x)
+            reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else {
+        for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
+    }
+}
+
+// Pack key page `p` of unit `u` from `rows` (g consecutive rows of a ring of
+// size `wrap` starting at `start`) into its block-table slot.
+__device__ void pack_key_into_cache(const KittyCacheDesc& c, int u, int p, const uint16_t* base,
+                                    int start, int wrap, uint8_t* smem) {
+    const KittyConfigC& k = c.cfg;
+    if (p >= c.max_pages) {
+        if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+        return;
+    }
+    uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
+    size_t off = ((size_t)k.g * k.d * 2 + 15) & ~size_t(15);
+    uint8_t* slot = smem + off;
+    off += ((size_t)max(KeyLayout{k.d, k.g, k.d_boost}.bytes(), ValueLayout{k.d, k.g}.bytes()) + 15) & ~size_t(15);
+    PackScratch sc = carve_scratch(smem + off, k.d);
+    stage_rows(tile, base, start, wrap, k.g, k.d);
+    if (!tile_all_finite(tile, k.g * k.d)) {
+        if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_NONFINITE);
+    }
+    pack_key_tile(tile, k.g, k.d, k.d_boost, nullptr, slot, sc, nullptr, nullptr);
+    const int32_t s = c.key_block_table[(int64_t)u * c.max_pages + p];
+    copy_slot_out(slot, c.key_pool + (int64_t)s * c.key_slot_bytes, KeyLayout{k.d, k.g, k.d_boost}.bytes());
+}
+
+__device__ void pack_value_into_cache(const KittyCacheDesc& c, int u, int p, const uint16_t* base,
+                                      int start, int wrap, uint8_t* smem) {
+    const KittyConfigC& k = c.cfg;
+    if (p >= c.max_pages) {
+        if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+        return;
+    }
+    uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
+    uint8_t* slot = smem + (((size_t)k.g * k.d * 2 + 15) & ~size_t(15));
+    stage_rows(tile, base, start, wrap, k.g, k.d);
+    if (!tile_all_finite(tile, k.g * k.d)) {
+        if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_NONFINITE);
+    }
+    pack_value_tile(tile, k.g, k.d, slot, nullptr, nullptr);
+    const int32_t s = c.value_block_table[(int64_t)u * c.max_pages + p];
+    copy_slot_out(slot, c.value_pool + (int64_t)s * c.value_slot_bytes, ValueLayout{k.d, k.g}.bytes());
+}
+
+// insert_token (cache.py:107-123) for one unit per CTA, then the pack trigger
+// of maybe_pack (cache.py:144-178) on this unit's own counts.
+__global__ void append_kernel(KittyCacheDesc c, const uint16_t* k_new, const uint16_t* v_new) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const KittyConfigC& k = c.cfg;
+    const int u = blockIdx.x;
+    const int d = k.d, S = k.s, G = k.g, W = k.r + k.g;
+    const int t = c.unit_len[u];
+    const uint16_t* kr = k_new + (int64_t)u * d;
+    const uint16_t* vr = v_new + (int64_t)u * d;
+    uint16_t* kq = c.k_qbuf + (int64_t)u * G * d;
+    uint16_t* vring = c.v_ring + (int64_t)u * W * d;
+    if (t < S) {
+        copy_row_bf16(c.k_sink + ((int64_t)u * S + t) * d, kr, d);
+        copy_row_bf16(c.v_sink + ((int64_t)u * S + t) * d, vr, d);
+    } else {
+        const int pc = t - S;  // position past the sink
+        copy_row_bf16(kq + (int64_t)(pc % G) * d, kr, d);
+        copy_row_bf16(vring + (int64_t)(pc % W) * d, vr, d);
+    }
+    __syncthreads();
+    const int n = t + 1;
+    const int past = n > S ? n - S : 0;
+    if (past > 0 && past % G == 0) pack_key_into_cache(c, u, past / G - 1, kq, 0, G, smem);
+    const int vtot = past > k.r ? past - k.r : 0;  // tokens that left the local window
+    if (vtot > 0 && vtot % G == 0) {
+        const int p = vtot / G - 1;
+        __syncthreads();
+        pack_value_into_cache(c, u, p, vring, (p * G) % W, W, smem);
+    }
+    if (threadIdx.x == 0) c.unit_len[u] = n;
+}
+
+// Prefill, fp rows: every prompt token whose final home (after the fold of
+// `P` appends) is a sink / q-buffer / ring row is copied there.
+__global__ void prefill_rows_kernel(KittyCacheDesc c, const uint16_t* keys, const uint16_t* values,
+                                    int P) {
+    const KittyConfigC& k = c.cfg;
+    const int u = blockIdx.y;
+    const int d = k.d, S = k.s, G = k.g, W = k.r + k.g;
+    const int past = P > S ? P - S : 0;
+    const int kp = past / G;
+    const int local = min(k.r, past);
+    const int vp = (past - local) / G;
+    for (int t = blockIdx.x; t < P; t += gridDim.x) {
+        const uint16_t* kr = keys + ((int64_t)u * P + t) * d;
+        const uint16_t* vr = values + ((int64_t)u * P + t) * d;
+        if (t < S) {
+            copy_row_bf16(c.k_sink + ((int64_t)u * S + t) * d, kr, d);
+            copy_row_bf16(c.v_sink + ((int64_t)u * S + t) * d, vr, d);
+        } else {
+            const int pc = t - S;
+            if (pc >= kp * G) copy_row_bf16(c.k_qbuf + ((int64_t)u * G + pc % G) * d, kr, d);
+            if (pc >= vp * G) copy_row_bf16(c.v_ring + ((int64_t)u * W + pc % W) * d, vr, d);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) c.unit_len[u] = P;
+}
+
+// Prefill, pages: blockIdx.x < kp packs key page blockIdx.x, else value page
+// blockIdx.x - kp; a page depends only on its own g tokens.
+__global__ void prefill_pack_kernel(KittyCacheDesc c, const uint16_t* keys, const uint16_t* values,
+                                    int P, int kp, int vp) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const KittyConfigC& k = c.cfg;
+    const int u = blockIdx.y;
+    const int y = blockIdx.x;
+    if (y < kp) {
+        pack_key_into_cache(c, u, y, keys + ((int64_t)u * P + k.s) * k.d, y * k.g, 1 << 30, smem);
+    } else if (y < kp + vp) {
+        const int p = y - kp;
+        pack_value_into_cache(c, u, p, values + ((int64_t)u * P + k.s) * k.d, p * k.g, 1 << 30, smem);
+    }
+}
+
+// flatten_keys / flatten_values (cache.py:210-215) of one unit.
+__global__ void flatten_kernel(KittyCacheDesc c, int u, int n, float* keys_out, float* values_out) {
+    const KittyConfigC& k = c.cfg;
+    const int d = k.d, S = k.s, G = k.g, W = k.r + k.g;
+    const int past = n > S ? n - S : 0;
+    const int kp = past / G;
+    const int local = min(k.r, past);
+    const int vp = (past - local) / G;
+    const KeyLayout KL{d, G, k.d_boost};
+    const ValueLayout VL{d, G};
+    const int gb = G / 4, db = d / 4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)n * d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int t = static_cast<int>(i / d), ch = static_cast<int>(i % d);
+        float kv, vv;
+        if (t < S) {
+            kv = bf16_to_f32(c.k_sink[((int64_t)u * S + t) * d + ch]);
+            vv = bf16_to_f32(c.v_sink[((int64_t)u * S + t) * d + ch]);
+        } else {
+            const int pc = t - S;
+            if (pc < kp * G) {
+                const int p = pc / G, tl = pc % G;
+                const uint8_t* slot = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes;
+                uint32_t code = (slot[KL.dense_off() + ch * gb + tl / 4] >> (2 * (tl % 4))) & 3u;
+                const uint8_t r = slot[KL.idx_off() + ch];
+                if (r != kSentinel) code |= ((slot[KL.high_off() + r * gb + tl / 4] >> (2 * (tl % 4))) & 3u) << 2;
+                const float s = half_bits_to_f32(ld_u16(slot + KL.scale_off() + 2 * ch));
+                const float z = half_bits_to_f32(ld_u16(slot + KL.zero_off() + 2 * ch));
+                kv = __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
+            } else {
+                kv = bf16_to_f32(c.k_qbuf[((int64_t)u * G + pc % G) * d + ch]);
+            }
+            if (pc < vp * G) {
+                const int p = pc / G, tl = pc % G;
+                const uint8_t* slot = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes;
+                const uint32_t code = (slot[VL.codes_off() + tl * db + ch / 4] >> (2 * (ch % 4))) & 3u;
+                const float s = half_bits_to_f32(ld_u16(slot + VL.scale_off() + 2 * tl));
+                const float z = half_bits_to_f32(ld_u16(slot + VL.zero_off() + 2 * tl));
+                vv = __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
+            } else {
+                vv = bf16_to_f32(c.v_ring[((int64_t)u * W + pc % W) * d + ch]);
+            }
+        }
+        keys_out[i] = kv;
+        values_out[i] = vv;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+
+cudaError_t launch_pack_key_pages(const void* x, int dtype, int P, int g, int d, int d_boost,
+                                  const int64_t* sel, uint8_t* slots, int64_t stride, float* sc32,
+                                  float* ze32, uint32_t* status, cudaStream_t st) {
+    if (P == 0) return cudaSuccess;
+    const size_t sm = pack_smem_bytes(g, d, d_boost, dtype == KITTY_F32 ? 4 : 2);
+    if (dtype == KITTY_F32) {
+        auto kfn = pack_key_pages_kernel<float>;
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kfn<<<P, 128, sm, st>>>(static_cast<const float*>(x), g, d, d_boost, sel, slots, stride,
+                                sc32, ze32, status);
+    } else {
+        auto kfn = pack_key_pages_kernel<uint16_t>;
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kfn<<<P, 128, sm, st>>>(static_cast<const uint16_t*>(x), g, d, d_boost, sel, slots,
+                                stride, sc32, ze32, status);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_value_pages(const void* x, int dtype, int P, int g, int d, uint8_t* slots,
+                                    int64_t stride, float* sc32, float* ze32, uint32_t* status,
+                                    cudaStream_t st) {
+    if (P == 0) return cudaSuccess;
+    const size_t sm = pack_smem_bytes(g, d, 0, dtype == KITTY_F32 ? 4 : 2);
+    if (dtype == KITTY_F32) {
+        auto kfn = pack_value_pages_kernel<float>;
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kfn<<<P, 128, sm, st>>>(static_cast<const float*>(x), g, d, slots, stride, sc32, ze32, status);
+    } else {
+        auto kfn = pack_value_pages_kernel<uint16_t>;
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kfn<<<P, 128, sm, st>>>(static_cast<const uint16_t*>(x), g, d, slots, stride, sc32, ze32, status);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_channel_scores(const void* x, int dtype, int P, int g, int d, double* scores,
+                                  cudaStream_t st) {
+    if (P == 0) return cudaSuccess;
+    if (dtype == KITTY_F32)
+        channel_scores_kernel<float><<<P, 128, 0, st>>>(static_cast<const float*>(x), g, d, scores);
+    else
+        channel_scores_kernel<uint16_t><<<P, 128, 0, st>>>(static_cast<const uint16_t*>(x), g, d, scores);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_select_boost(const double* scores, int P, int d, int k, int64_t* out,
+                                cudaStream_t st) {
+    if (P == 0 || k == 0) return cudaSuccess;
+    select_boost_kernel<<<P, 128, d, st>>>(scores, d, k, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequant_key_pages(const uint8_t* slots, int64_t stride, int P, int g, int d,
+                                     int d_boost, const float* sc32, const float* ze32, float* out,
+                                     uint32_t* status, cudaStream_t st) {
+    if (P == 0) return cudaSuccess;
+    dequant_key_pages_kernel<<<P, 256, 0, st>>>(slots, stride, g, d, d_boost, sc32,
+                                                                ze32, out, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequant_value_pages(const uint8_t* slots, int64_t stride, int P, int g, int d,
+                                       const float* sc32, const float* ze32, float* out,
+                                       cudaStream_t st) {
+    if (P == 0) return cudaSuccess;
+    dequant_value_pages_kernel<<<P, 256, 0, st>>>(slots, stride, g, d, sc32, ze32, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_append(const KittyCacheDesc& c, const uint16_t* k_new, const uint16_t* v_new,
+                          cudaStream_t st) {
+    const int units = c.num_seqs * c.cfg.h_kv;
+    if (units == 0) return cudaSuccess;
+    const size_t sm = pack_smem_bytes(c.cfg.g, c.cfg.d, c.cfg.d_boost, 2);
+    cudaFuncSetAttribute(append_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    append_kernel<<<units, 128, sm, st>>>(c, k_new, v_new);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prefill(const KittyCacheDesc& c, const uint16_t* keys, const uint16_t* values,
+                           int P, cudaStream_t st) {
+    const int units = c.num_seqs * c.cfg.h_kv;
+    if (units == 0) return cudaSuccess;
+    const int S = c.cfg.s, G = c.cfg.g;
+    const int past = P > S ? P - S : 0;
+    const int kp = past / G;
+    const int vp = (past - min(c.cfg.r, past)) / G;
+    const int gx = P > 0 ? min(P, 1024) : 1;
+    prefill_rows_kernel<<<dim3(gx, units), 128, 0, st>>>(c, keys, values, P);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || kp + vp == 0) return e;
+    const size_t sm = pack_smem_bytes(G, c.cfg.d, c.cfg.d_boost, 2);
+    cudaFuncSetAttribute(prefill_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    prefill_pack_kernel<<<dim3(kp + vp, units), 128, sm, st>>>(c, keys, values, P, kp, vp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flatten(const KittyCacheDesc& c, int u, int n, float* ko, float* vo,
+                           cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const int64_t total = (int64_t)n * c.cfg.d;
+    const int64_t want = (total + 255) / 256;
+    const int blocks = static_cast<int>(want < 4096 ? want : 4096);
+    flatten_kernel<<<blocks, 256, 0, st>>>(c, u, n, ko, vo);
+    return cudaGetLastError();
+}
+
+}  // namespace kitty

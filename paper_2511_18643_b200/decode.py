@@ -1,0 +1,106 @@
+"""Multi-layer decode step over Kitty caches, with CUDA-graph replay.
+
+A model's decode step runs, for every attention layer, ``append`` (insert the
+new K/V rows, pack full q-buffers) then ``attend`` (fused dequant-attention)
+-- the reference's loop body (cli.py:310-315, cache.py:107-252) for a batch
+of sequences.  ``DecodeStep`` owns fixed input/output buffers so the whole
+step (2 launches per layer + the split combine) is captured once into a CUDA
+graph and replayed; the device reads sequence lengths from HBM, so the same
+graph serves every step.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .cache import KittyBatchCache
+from .config import KittyConfig
+from .pages import _stream
+
+
+class DecodeStep:
+    def __init__(self, cfg: KittyConfig, num_layers: int, num_seqs: int, max_tokens: int, device=None):
+        self.cfg = cfg
+        self.num_layers = num_layers
+        self.num_seqs = num_seqs
+        self.max_tokens = max_tokens
+        self.layers = [KittyBatchCache(cfg, num_seqs, max_tokens, device) for _ in range(num_layers)]
+        dev = self.layers[0].device
+        self.device = dev
+        bf = torch.bfloat16
+        self.k_in = torch.zeros((num_layers, num_seqs, cfg.h_kv, cfg.d), dtype=bf, device=dev)
+        self.v_in = torch.zeros((num_layers, num_seqs, cfg.h_kv, cfg.d), dtype=bf, device=dev)
+        self.q_in = torch.zeros((num_layers, num_seqs, cfg.h_q, cfg.d), dtype=bf, device=dev)
+        self.out = torch.zeros((num_layers, num_seqs, cfg.h_q, cfg.d), dtype=bf, device=dev)
+        # one workspace shared by the layers (they run back to back on one stream)
+        self.ws = self.layers[0].workspace(max_tokens)
+        self.graph = None
+        self.lib = _lib.load_library()
+
+    # bytes moved per step by the inputs / outputs (for the e2e host copies)
+    def input_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.k_in, self.v_in, self.q_in))
+
+    def output_bytes(self) -> int:
+        return self.out.numel() * self.out.element_size()
+
+    def launches_per_step(self) -> int:
+        return self.num_layers * (1 + self.attention_launches())
+
+    def attention_launches(self) -> int:
+        from .cache import KittyBatchCache  # noqa: F401
+
+        return 1 if self.fast_path() else 2
+
+    def fast_path(self) -> bool:
+        c = self.cfg
+        return c.d == 128 and c.g == 128 and c.group_size in (1, 2, 4, 8)
+
+    def _launch(self):
+        lib, st = self.lib, _stream()
+        for l, cache in enumerate(self.layers):
+            _lib.check(lib.kitty_append(cache._desc_ref, self.k_in[l].data_ptr(), self.v_in[l].data_ptr(), st), "append")
+            _lib.check(lib.kitty_decode_attention(cache._desc_ref, self.q_in[l].data_ptr(), self.out[l].data_ptr(),
+                                                  _lib.KITTY_BF16, self.max_tokens, self.ws.data_ptr(),
+                                                  self.ws.numel(), st), "attend")
+
+    def _advance(self):
+        for cache in self.layers:
+            for b in range(self.num_seqs):
+                cache.lengths[b] += 1
+                cache._count_events(b, cache.lengths[b])
+
+    def step(self):
+        """One eager decode step over all layers."""
+        if max(self.layers[0].lengths) + 1 > self.max_tokens:
+            raise ValueError("decode step past the allocated context")
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch()
+        self._advance()
+
+    def capture(self):
+        """Capture one step into a CUDA graph (does not advance the state)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            # the capture records launches only; lengths are read on device at replay
+            with torch.cuda.graph(g, stream=s):
+                self._launch()
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+        return g
+
+    def attention_only(self, layer: int):
+        cache = self.layers[layer]
+        _lib.check(self.lib.kitty_decode_attention(cache._desc_ref, self.q_in[layer].data_ptr(), self.out[layer].data_ptr(),
+                                                   _lib.KITTY_BF16, self.max_tokens, self.ws.data_ptr(), self.ws.numel(),
+                                                   _stream()), "attend")
+
+    def append_only(self, layer: int):
+        cache = self.layers[layer]
+        _lib.check(self.lib.kitty_append(cache._desc_ref, self.k_in[layer].data_ptr(), self.v_in[layer].data_ptr(),
+                                         _stream()), "append")
