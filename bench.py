@@ -223,10 +223,10 @@ def run_kitty(args):
     achieved = bytes_per_launch / (attn_avg_ms * 1e-3) / 1e9
 
     # -- e2e: host (pinned) inputs -> device, step, outputs -> host, per step
-    h_k = ks[warmup:].cpu().pin_memory()
-    h_v = vs[warmup:].cpu().pin_memory()
-    h_q = qs[warmup:].cpu().pin_memory()
-    h_out = torch.empty(step.out.shape, dtype=step.out.dtype).pin_memory()
+    host_k = ks[warmup:].cpu().pin_memory()
+    host_v = vs[warmup:].cpu().pin_memory()
+    host_q = qs[warmup:].cpu().pin_memory()
+    host_out = torch.empty(step.out.shape, dtype=step.out.dtype).pin_memory()
     e_steps = min(steps, 5)
     torch.cuda.synchronize()
     if world > 1:
@@ -235,11 +235,11 @@ def run_kitty(args):
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record()
     for i in range(e_steps):
-        step.k_in.copy_(h_k[i], non_blocking=True)
-        step.v_in.copy_(h_v[i], non_blocking=True)
-        step.q_in.copy_(h_q[i], non_blocking=True)
+        step.k_in.copy_(host_k[i], non_blocking=True)
+        step.v_in.copy_(host_v[i], non_blocking=True)
+        step.q_in.copy_(host_q[i], non_blocking=True)
         step.step()
-        h_out.copy_(step.out, non_blocking=True)
+        host_out.copy_(step.out, non_blocking=True)
     e3.record()
     torch.cuda.synchronize()
     e_ms = e2.elapsed_time(e3)

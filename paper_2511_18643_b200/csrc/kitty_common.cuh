@@ -24,8 +24,15 @@ __device__ __forceinline__ float load_elem(const uint16_t* p, int64_t i) {
 __device__ __forceinline__ float half_bits_to_f32(uint16_t h) {
     return __half2float(__ushort_as_half(h));
 }
-__device__ __forceinline__ uint16_t f32_to_half_bits(float f) {
-    return __half_as_ushort(__float2half_rn(f));
+// f32 -> f16 (RNE) bit pattern.  Written with an explicit cvt: going through
+// __half_as_ushort and then splitting the result into bytes let nvcc 12.9 fuse
+// the byte extraction into a numeric F2I.U8.F16 conversion (wrong bytes).
+__device__ __forceinline__ uint32_t f32_to_half_bits(float f) {
+    unsigned short h;
+    asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f));
+    uint32_t r;
+    asm("cvt.u32.u16 %0, %1;" : "=r"(r) : "h"(h));
+    return r;
 }
 __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(f));
@@ -75,9 +82,9 @@ struct LaneQuant {
 __device__ __forceinline__ uint16_t ld_u16(const uint8_t* p) {
     return static_cast<uint16_t>(p[0] | (p[1] << 8));
 }
-__device__ __forceinline__ void st_u16(uint8_t* p, uint16_t v) {
-    p[0] = static_cast<uint8_t>(v & 0xff);
-    p[1] = static_cast<uint8_t>(v >> 8);
+__device__ __forceinline__ void st_u16(uint8_t* p, uint32_t v) {
+    p[0] = static_cast<uint8_t>(v & 0xffu);
+    p[1] = static_cast<uint8_t>((v >> 8) & 0xffu);
 }
 
 __device__ __forceinline__ void set_status(uint32_t* status, uint32_t bits) {
