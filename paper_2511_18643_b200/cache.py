@@ -129,7 +129,8 @@ class KittyBatchCache:
     def workspace(self, max_tokens: int) -> torch.Tensor:
         need = int(self.lib.kitty_attention_workspace_bytes(self._desc_ref, max_tokens))
         if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(max(need, 16), dtype=torch.uint8, device=self.device)
+            # zeroed: the fused kernel keeps self-resetting work counters at its head
+            self._ws = torch.zeros(max(need, 16), dtype=torch.uint8, device=self.device)
         return self._ws
 
     # -- decode step -----------------------------------------------------------

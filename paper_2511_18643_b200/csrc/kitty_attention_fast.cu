@@ -1,14 +1,810 @@
-// Tensor-core fused dequant-attention for d = g = 128 (placeholder: the
-// generic path serves every shape until this kernel lands).
+// Fused dequant-attention decode kernel for d = g = 128 (K4 + K5 in one launch).
+//
+// Semantics: KittyCacheState.attend (cache.py:217-252) -- per (sequence, KV
+// head) unit, logits q.k / sqrt(d) over sink | key pages | key q-buffer, fp32
+// max-subtracted softmax, probabilities times values over sink | value pages |
+// value q-buffer | local -- with pages dequantised inside the loop (Alg. 1,
+// PAPER.md:425-446) instead of from cached f32 rows.
+//
+// Design:
+//  * persistent CTAs (2 per SM x 4 warps); every warp pulls work items from
+//    an atomic queue: FP items (the unit's full-precision tokens, CUDA cores)
+//    first, then chunks of `ppc` quantized K/V page pairs (tensor cores);
+//  * each warp streams page pairs through a private 2-stage shared-memory ring
+//    with cp.async.bulk (1-D TMA) + mbarrier, so the next pair is in flight
+//    while the current one is computed;
+//  * 2-bit codes become fp16 MMA operands with one PRMT (pair two channels)
+//    plus one LOP3 per 2 codes: (x & mask) | 0x6400 = 1024 + w*c, w in {16, 64};
+//    the 1024 offset and w are removed per row after the MMA;
+//  * per-channel key scale is folded into q (B = q*alpha*s, fp16), per-token
+//    value scale into p (B = p*s); zero points and the offset sums come out of
+//    one auxiliary MMA tile (row 0 = ones, row 8 = zeros) whose B columns 4-7
+//    carry the unscaled q / p (GQA group <= 4 leaves them free);
+//  * mma.sync.m16n8k16 f16 x f16 -> f32, swap-AB: M = 16 tokens (QK) or 16
+//    channels (PV), N = the GQA group, K = 16 channels (QK) or tokens (PV);
+//  * warp-shuffle online softmax in the log2 domain; partials (m, l, acc) per
+//    item go to the workspace and the last item of a unit merges them (LSE)
+//    and writes the bf16/f32 output -- no separate combine launch.
 #include "kitty_attention.cuh"
+#include "kitty_codec.cuh"
 
 namespace kitty {
+namespace fastattn {
 
-bool fast_attention_supported(const KittyCacheDesc&) { return false; }
-size_t fast_attention_workspace_bytes(const KittyCacheDesc&, int) { return 0; }
-cudaError_t launch_fast_attention(const KittyCacheDesc&, const uint16_t*, void*, int, int, void*,
-                                  size_t, cudaStream_t) {
-    return cudaErrorNotSupported;
+constexpr int D = 128;
+constexpr int G = 128;
+constexpr int kWarps = 4;         // warps per CTA
+constexpr int kCtasPerSm = 2;
+constexpr int kKeySlotMax = 5760;  // d_boost = 32
+constexpr int kStageBytes = kKeySlotMax + 4608;
+constexpr int kPtStride = 136;     // f16 per row of the transposed-P buffer
+constexpr int kFpChunk = 32;       // fp tokens per online-softmax step
+constexpr float kAlpha = 0.12751743074f;  // log2(e) / sqrt(128)
+constexpr uint32_t kMagic = 0x64006400u;  // f16x2 (1024, 1024)
+constexpr uint32_t kOnes = 0x3C003C00u;   // f16x2 (1, 1)
+
+struct __align__(128) WarpSmem {
+    uint8_t stage[2][kStageBytes];  // K page | V page (KTYP bodies)
+    uint32_t pt[8][kPtStride / 2];  // P^T as f16x2: rows 0-3 p*s, rows 4-7 p
+    uint16_t qa4[4][D];             // 4 * q * alpha (f16) for boosted-row gathers
+    float qf[4][D];                 // q * alpha (f32) for the fp routine
+    float ps[4][kFpChunk];          // fp routine probabilities
+    uint8_t inv[32];                // boosted channel of high_bits row j
+    unsigned long long mbar[2];
+};
+
+struct Params {
+    KittyCacheDesc c;
+    const uint16_t* q;
+    void* out;
+    int out_dtype;
+    int ppc;    // page pairs per quantized item
+    int cmax;   // quantized items per unit (grid bound)
+    int units;
+    int* ctr;   // [0] next item, [1] finished warps, [2 + u] arrivals of unit u
+    float* part;
+};
+
+// ---- small PTX helpers --------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+__device__ __forceinline__ float ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t lds32(const void* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
+// Two 32-bit words = 16 tokens (K: one channel row) or 16 channels (V: one
+// token row) each; byte b of both -> the fp16x2 A operands of 4 tokens x 2
+// rows.  Values are 1024 + 16 c (rows gid) and 1024 + 64 c (rows gid + 8).
+//   e_lo / e_hi: codes 0 / 1 of the byte, o_lo / o_hi: codes 2 / 3.
+// (a & b) | c in ONE LOP3: with two immediates ptxas splits it into two, so
+// the masks / magic are kept in registers (Consts, made opaque once per warp).
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+struct Consts {
+    uint32_t m_lo, m_hi, magic;
+    __device__ __forceinline__ Consts() {
+        m_lo = 0x00300030u;
+        m_hi = 0x00C000C0u;
+        magic = kMagic;
+        asm volatile("" : "+r"(m_lo), "+r"(m_hi), "+r"(magic));
+    }
+};
+
+template <int B>
+__device__ __forceinline__ void conv_byte(const Consts& k, uint32_t w0, uint32_t w1, uint32_t& e_lo,
+                                          uint32_t& e_hi, uint32_t& o_lo, uint32_t& o_hi) {
+    constexpr uint32_t sel = B | (B << 4) | ((4 + B) << 8) | ((4 + B) << 12);
+    const uint32_t x = prmt(w0, w1, sel);
+    const uint32_t y = x * 16u;
+    e_lo = and_or(y, k.m_lo, k.magic);
+    e_hi = and_or(y, k.m_hi, k.magic);
+    o_lo = and_or(x, k.m_lo, k.magic);
+    o_hi = and_or(x, k.m_hi, k.magic);
+}
+
+// acc[8][4] += A(2-bit codes of rows r0..r3, word gid) x B for one k-step.
+// rows = (w0, w1) pair P0 and (w2, w3) pair P1.
+__device__ __forceinline__ void mma_codes(const Consts& k, float (&acc)[8][4], uint32_t w0, uint32_t w1,
+                                          uint32_t w2, uint32_t w3, uint32_t b0, uint32_t b1) {
+    uint32_t e0, e1, o0, o1, E0, E1, O0, O1;
+    conv_byte<0>(k, w0, w1, e0, e1, o0, o1);
+    conv_byte<0>(k, w2, w3, E0, E1, O0, O1);
+    mma16816(acc[0], e0, e1, E0, E1, b0, b1);
+    mma16816(acc[1], o0, o1, O0, O1, b0, b1);
+    conv_byte<1>(k, w0, w1, e0, e1, o0, o1);
+    conv_byte<1>(k, w2, w3, E0, E1, O0, O1);
+    mma16816(acc[2], e0, e1, E0, E1, b0, b1);
+    mma16816(acc[3], o0, o1, O0, O1, b0, b1);
+    conv_byte<2>(k, w0, w1, e0, e1, o0, o1);
+    conv_byte<2>(k, w2, w3, E0, E1, O0, O1);
+    mma16816(acc[4], e0, e1, E0, E1, b0, b1);
+    mma16816(acc[5], o0, o1, O0, O1, b0, b1);
+    conv_byte<3>(k, w0, w1, e0, e1, o0, o1);
+    conv_byte<3>(k, w2, w3, E0, E1, O0, O1);
+    mma16816(acc[6], e0, e1, E0, E1, b0, b1);
+    mma16816(acc[7], o0, o1, O0, O1, b0, b1);
+}
+
+struct UnitGeom {
+    int n, kp, vp, nfp;
+};
+
+__device__ __forceinline__ UnitGeom unit_geom(const KittyCacheDesc& c, int u) {
+    UnitGeom g;
+    g.n = c.unit_len[u];
+    const int S = c.cfg.s;
+    const int past = g.n > S ? g.n - S : 0;
+    g.kp = past / G;
+    g.vp = (past - min(c.cfg.r, past)) / G;
+    g.nfp = g.n > S ? S + (past - g.vp * G) : g.n;  // sink + value fp tokens
+    return g;
+}
+
+// ---- the kernel ------------------------------------------------------------------
+
+template <int GROUP, int NKH>
+__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel(Params P) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+    const KittyCacheDesc& c = P.c;
+    const int S = c.cfg.s, W = c.cfg.r + c.cfg.g;
+    const int d_boost = c.cfg.d_boost;
+    const int kslot = static_cast<int>(c.key_slot_bytes);
+    const int vslot = static_cast<int>(c.value_slot_bytes);
+    const int scale_off = D * G / 4 + d_boost * G / 4 + D;  // KTYP key scales
+    const int zero_off = scale_off + 2 * D;
+    const int total_items = P.units * (1 + P.cmax);
+    const int hkv = c.cfg.h_kv;
+
+    if (lane == 0) {
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    sm.inv[lane] = 0;
+    __syncwarp();
+    const Consts kc;
+
+    uint32_t issued = 0, consumed = 0;
+
+    auto pull = [&]() -> int {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(P.ctr, 1);
+        __syncwarp();
+        return __shfl_sync(0xffffffffu, i, 0);
+    };
+    // item -> (kind, unit, first page, end page); kind 0 = end, 1 = fp, 2 = pages, 3 = empty
+    auto decode = [&](int it, int& kind, int& u, int& p0, int& p1) {
+        if (it >= total_items) {
+            kind = 0;
+            return;
+        }
+        if (it < P.units) {
+            kind = 1;
+            u = it;
+            p0 = p1 = 0;
+            return;
+        }
+        const int i2 = it - P.units;
+        const int ch = i2 / P.units;
+        u = i2 - ch * P.units;
+        const UnitGeom gm = unit_geom(c, u);
+        p0 = ch * P.ppc;
+        p1 = min(gm.vp, p0 + P.ppc);
+        kind = (p0 < p1 && gm.n > 0) ? 2 : 3;
+    };
+    auto next_item = [&](int& kind, int& u, int& p0, int& p1) {
+        for (;;) {
+            decode(pull(), kind, u, p0, p1);
+            if (kind == 1 && c.unit_len[u] == 0) continue;
+            if (kind != 3) return;
+        }
+    };
+    auto issue = [&](int u, int p) {
+        const int s = issued & 1;
+        if (lane == 0) {
+            const uint8_t* ks = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * kslot;
+            const uint8_t* vs = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * vslot;
+            mbar_expect_tx(&sm.mbar[s], kslot + vslot);
+            bulk_g2s(sm.stage[s], ks, kslot, &sm.mbar[s]);
+            bulk_g2s(sm.stage[s] + kslot, vs, vslot, &sm.mbar[s]);
+        }
+        __syncwarp();
+        ++issued;
+    };
+
+    // per-unit query state
+    int cur_unit = -1;
+    uint32_t qa[8][2];  // B fragments of q*alpha (f16x2) for this lane's column
+    auto load_unit = [&](int u) {
+        if (u == cur_unit) return;
+        cur_unit = u;
+        const int b = u / hkv, h = u - b * hkv;
+        const uint16_t* qg = P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP) * D;
+        for (int g = 0; g < 4; ++g) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int d = 4 * lane + i;
+                const float v = g < GROUP ? bf16_to_f32(qg[g * D + d]) * kAlpha : 0.f;
+                sm.qf[g][d] = v;
+                sm.qa4[g][d] = static_cast<uint16_t>(f32_to_half_bits(4.f * v));
+            }
+        }
+        __syncwarp();
+        const int col = gid & 3;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int d = 16 * ks + 2 * tig + 8 * hh;
+                qa[ks][hh] = pack_f16x2(sm.qf[col][d], sm.qf[col][d + 1]);
+            }
+        }
+    };
+
+    // merge the partials of unit u (called by the warp that completed it)
+    auto finish_unit = [&](int u) {
+        __threadfence();
+        int old = 0;
+        if (lane == 0) old = atomicAdd(&P.ctr[2 + u], 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        const UnitGeom gm = unit_geom(c, u);
+        const int nparts = 1 + (gm.vp + P.ppc - 1) / P.ppc;
+        if (old != nparts - 1) return;
+        __threadfence();
+        const int b = u / hkv, h = u - b * hkv;
+        const float* pb = P.part + (int64_t)u * (1 + P.cmax) * GROUP * (D + 2);
+        for (int g = 0; g < GROUP; ++g) {
+            float M = -INFINITY;
+            for (int i = 0; i < nparts; ++i) M = fmaxf(M, __ldcg(pb + (int64_t)i * GROUP * (D + 2) + GROUP * D + 2 * g));
+            float L = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+            for (int i = 0; i < nparts; ++i) {
+                const float* pi = pb + (int64_t)i * GROUP * (D + 2);
+                const float mi = __ldcg(pi + GROUP * D + 2 * g);
+                const float wgt = mi == -INFINITY ? 0.f : ex2(mi - M);
+                L += wgt * __ldcg(pi + GROUP * D + 2 * g + 1);
+                const float4 a = __ldcg(reinterpret_cast<const float4*>(pi + g * D) + lane);
+                o0 += wgt * a.x;
+                o1 += wgt * a.y;
+                o2 += wgt * a.z;
+                o3 += wgt * a.w;
+            }
+            const float inv = 1.f / L;
+            const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
+            if (P.out_dtype == KITTY_F32) {
+                reinterpret_cast<float4*>(static_cast<float*>(P.out) + row * D)[lane] =
+                    make_float4(o0 * inv, o1 * inv, o2 * inv, o3 * inv);
+            } else {
+                uint2 v;
+                v.x = f32_to_bf16_bits(o0 * inv) | (f32_to_bf16_bits(o1 * inv) << 16);
+                v.y = f32_to_bf16_bits(o2 * inv) | (f32_to_bf16_bits(o3 * inv) << 16);
+                reinterpret_cast<uint2*>(static_cast<uint16_t*>(P.out) + row * D)[lane] = v;
+            }
+        }
+        if (lane == 0) P.ctr[2 + u] = 0;  // reset for the next launch
+    };
+
+    // ---- full-precision tokens of a unit (sink, value q-buffer + local; keys
+    // of those tokens from the sink, a key page or the key q-buffer) --------
+    auto process_fp = [&](int u) {
+        load_unit(u);
+        const UnitGeom gm = unit_geom(c, u);
+        const int s_len = min(gm.n, S);
+        const int T = gm.nfp;
+        float m[4], l[4], acc[4][4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            m[g] = -INFINITY;
+            l[g] = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[g][i] = 0.f;
+        }
+        const uint16_t* ksink = c.k_sink + (int64_t)u * S * D;
+        const uint16_t* vsink = c.v_sink + (int64_t)u * S * D;
+        const uint16_t* kq = c.k_qbuf + (int64_t)u * G * D;
+        const uint16_t* vr = c.v_ring + (int64_t)u * W * D;
+        const int vbase = S + gm.vp * G;  // first value-fp token past the sink
+#pragma unroll 1
+        for (int c0 = 0; c0 < T; c0 += kFpChunk) {
+            const int j = c0 + lane;
+            const bool valid = j < T;
+            float lg[4] = {0.f, 0.f, 0.f, 0.f};
+            if (valid) {
+                const int t = j < s_len ? j : vbase + (j - s_len);
+                const uint16_t* krow = nullptr;
+                const uint8_t* kpg = nullptr;
+                int tl = 0;
+                if (t < S) {
+                    krow = ksink + (int64_t)t * D;
+                } else {
+                    const int pc = t - S;
+                    if (pc < gm.kp * G) {
+                        kpg = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + pc / G] * kslot;
+                        tl = pc % G;
+                    } else {
+                        krow = kq + (int64_t)(pc % G) * D;
+                    }
+                }
+                if (krow) {
+#pragma unroll 4
+                    for (int v8 = 0; v8 < D / 8; ++v8) {
+                        const uint4 w = reinterpret_cast<const uint4*>(krow)[v8];
+                        const float k8[8] = {__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u),
+                                             __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u),
+                                             __uint_as_float(w.z << 16), __uint_as_float(w.z & 0xffff0000u),
+                                             __uint_as_float(w.w << 16), __uint_as_float(w.w & 0xffff0000u)};
+#pragma unroll
+                        for (int g = 0; g < GROUP; ++g) {
+                            const float4 qa_ = *reinterpret_cast<const float4*>(&sm.qf[g][8 * v8]);
+                            const float4 qb_ = *reinterpret_cast<const float4*>(&sm.qf[g][8 * v8 + 4]);
+                            lg[g] = fmaf(qa_.x, k8[0], lg[g]);
+                            lg[g] = fmaf(qa_.y, k8[1], lg[g]);
+                            lg[g] = fmaf(qa_.z, k8[2], lg[g]);
+                            lg[g] = fmaf(qa_.w, k8[3], lg[g]);
+                            lg[g] = fmaf(qb_.x, k8[4], lg[g]);
+                            lg[g] = fmaf(qb_.y, k8[5], lg[g]);
+                            lg[g] = fmaf(qb_.z, k8[6], lg[g]);
+                            lg[g] = fmaf(qb_.w, k8[7], lg[g]);
+                        }
+                    }
+                } else {
+                    // key page token: Alg. 1 per element from the page in global memory
+                    const int sh = 2 * (tl & 3), byte = tl >> 2;
+#pragma unroll 2
+                    for (int d = 0; d < D; ++d) {
+                        uint32_t code = (kpg[d * (G / 4) + byte] >> sh) & 3u;
+                        const uint32_t r = kpg[D * G / 4 + d_boost * G / 4 + d];
+                        if (r != kSentinel) code |= ((kpg[D * G / 4 + r * (G / 4) + byte] >> sh) & 3u) << 2;
+                        const float s = half_bits_to_f32(ld_u16(kpg + scale_off + 2 * d));
+                        const float z = half_bits_to_f32(ld_u16(kpg + zero_off + 2 * d));
+                        const float kv = fmaf(static_cast<float>(code), s, z);
+#pragma unroll
+                        for (int g = 0; g < GROUP; ++g) lg[g] = fmaf(sm.qf[g][d], kv, lg[g]);
+                    }
+                }
+            }
+            // online softmax over this chunk (log2 domain)
+#pragma unroll
+            for (int g = 0; g < GROUP; ++g) {
+                float x = valid ? lg[g] : -INFINITY;
+                float mc = x;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+                const float mn = fmaxf(m[g], mc);
+                const float corr = ex2(m[g] - mn);
+                const float p = valid ? ex2(x - mn) : 0.f;
+                float ps = p;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+                l[g] = l[g] * corr + ps;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[g][i] *= corr;
+                sm.ps[g][lane] = p;
+                m[g] = mn;
+            }
+            __syncwarp();
+            const int cnt = min(kFpChunk, T - c0);
+#pragma unroll 2
+            for (int jj = 0; jj < cnt; ++jj) {
+                const int jt = c0 + jj;
+                const int t = jt < s_len ? jt : vbase + (jt - s_len);
+                const uint16_t* vrow = t < S ? vsink + (int64_t)t * D : vr + (int64_t)((t - S) % W) * D;
+                const uint2 w = reinterpret_cast<const uint2*>(vrow)[lane];
+                const float v0 = __uint_as_float(w.x << 16), v1 = __uint_as_float(w.x & 0xffff0000u);
+                const float v2 = __uint_as_float(w.y << 16), v3 = __uint_as_float(w.y & 0xffff0000u);
+#pragma unroll
+                for (int g = 0; g < GROUP; ++g) {
+                    const float pg = sm.ps[g][jj];
+                    acc[g][0] = fmaf(pg, v0, acc[g][0]);
+                    acc[g][1] = fmaf(pg, v1, acc[g][1]);
+                    acc[g][2] = fmaf(pg, v2, acc[g][2]);
+                    acc[g][3] = fmaf(pg, v3, acc[g][3]);
+                }
+            }
+            __syncwarp();
+        }
+        float* base = P.part + ((int64_t)u * (1 + P.cmax)) * GROUP * (D + 2);
+#pragma unroll
+        for (int g = 0; g < GROUP; ++g) {
+            reinterpret_cast<float4*>(base + g * D)[lane] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+            if (lane == 0) {
+                base[GROUP * D + 2 * g] = m[g];
+                base[GROUP * D + 2 * g + 1] = l[g];
+            }
+        }
+    };
+
+    // ---- one quantized K/V page pair in stage s ----------------------------------
+    float om[2], ol[2], oacc[8][4];
+    auto page_pair = [&](int s) {
+        const uint8_t* kp = sm.stage[s];
+        const uint8_t* vp = sm.stage[s] + kslot;
+        const uint32_t* kw = reinterpret_cast<const uint32_t*>(kp);
+        const uint32_t* vw = reinterpret_cast<const uint32_t*>(vp);
+        const bool main_col = gid < 4;
+        const bool row0 = gid == 0;
+
+        // boosted rows -> channels (inverse of boost_idx)
+        if (NKH > 0) {
+            const uint32_t bw = lds32(kp + D * G / 4 + d_boost * G / 4 + 4 * lane);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t bi = (bw >> (8 * i)) & 0xffu;
+                if (bi < 32u) sm.inv[bi] = static_cast<uint8_t>(4 * lane + i);
+            }
+            __syncwarp();
+        }
+
+        // ---- QK^T: logits of 128 tokens x (group | aux) columns
+        float acc[8][4];
+        float aux[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int c0 = 16 * ks + 2 * tig;
+            uint32_t s0 = lds32(kp + scale_off + 2 * c0);
+            uint32_t s1 = lds32(kp + scale_off + 2 * (c0 + 8));
+            s0 = main_col ? s0 : kOnes;
+            s1 = main_col ? s1 : kOnes;
+            const uint32_t b0 = hmul2(qa[ks][0], s0);
+            const uint32_t b1 = hmul2(qa[ks][1], s1);
+            const uint32_t w0 = kw[8 * c0 + gid], w1 = kw[8 * (c0 + 1) + gid];
+            const uint32_t w2 = kw[8 * (c0 + 8) + gid], w3 = kw[8 * (c0 + 9) + gid];
+            mma_codes(kc, acc, w0, w1, w2, w3, b0, b1);
+            const uint32_t z0 = lds32(kp + zero_off + 2 * c0);
+            const uint32_t z1 = lds32(kp + zero_off + 2 * (c0 + 8));
+            mma16816(aux, row0 ? kOnes : 0u, row0 ? z0 : 0u, row0 ? kOnes : 0u, row0 ? z1 : 0u, b0, b1);
+        }
+#pragma unroll
+        for (int hk = 0; hk < NKH; ++hk) {
+            const int j0 = 16 * hk + 2 * tig;
+            const int jj[4] = {j0, j0 + 1, j0 + 8, j0 + 9};
+            uint32_t hv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int ch = sm.inv[jj[i]];
+                const float q4 = half_bits_to_f32(sm.qa4[gid & 3][ch]);
+                const float sc = half_bits_to_f32(ld_u16(kp + scale_off + 2 * ch));
+                hv[i] = (main_col && jj[i] < d_boost) ? __float_as_uint(q4 * sc) : 0u;
+            }
+            const uint32_t b0 = pack_f16x2(__uint_as_float(hv[0]), __uint_as_float(hv[1]));
+            const uint32_t b1 = pack_f16x2(__uint_as_float(hv[2]), __uint_as_float(hv[3]));
+            const uint32_t* hw = reinterpret_cast<const uint32_t*>(kp + D * G / 4);
+            mma_codes(kc, acc, hw[8 * j0 + gid], hw[8 * (j0 + 1) + gid], hw[8 * (j0 + 8) + gid], hw[8 * (j0 + 9) + gid],
+                      b0, b1);
+            mma16816(aux, row0 ? kOnes : 0u, 0u, row0 ? kOnes : 0u, 0u, b0, b1);
+        }
+        // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha)
+        float sumB[2], cst[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            sumB[j] = __shfl_sync(0xffffffffu, aux[j], tig & 1);
+            cst[j] = __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
+        }
+        float b16[2], b64[2], mnew[2], corr[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            b16[j] = cst[j] - 64.f * sumB[j];
+            b64[j] = cst[j] - 16.f * sumB[j];
+            float x16 = acc[0][j], x64 = acc[0][2 + j];
+#pragma unroll
+            for (int m = 1; m < 8; ++m) {
+                x16 = fmaxf(x16, acc[m][j]);
+                x64 = fmaxf(x64, acc[m][2 + j]);
+            }
+            float pm = fmaxf(fmaf(x16, 1.f / 16.f, b16[j]), fmaf(x64, 1.f / 64.f, b64[j]));
+            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 4));
+            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 8));
+            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 16));
+            mnew[j] = fmaxf(om[j], pm);
+            corr[j] = ex2(om[j] - mnew[j]);
+            b16[j] -= mnew[j];
+            b64[j] -= mnew[j];
+        }
+        // P^T -> shared (rows 0-3: p * s_token, rows 4-7: p), tokens 16 gid + 2m (+1)
+        const uint8_t* vscale = vp + G * D / 4;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int tok = 16 * gid + 2 * m;
+            const uint32_t sv = lds32(vscale + 2 * tok);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const float p0 = ex2(fmaf(acc[m][j], 1.f / 16.f, b16[j]));
+                const float p1 = ex2(fmaf(acc[m][2 + j], 1.f / 64.f, b64[j]));
+                const uint32_t pu = pack_f16x2(p0, p1);
+                if (tig < 2) {
+                    const int g = 2 * tig + j;
+                    sm.pt[g][tok / 2] = hmul2(pu, sv);
+                    sm.pt[4 + g][tok / 2] = pu;
+                }
+            }
+        }
+        __syncwarp();
+
+        // ---- P V: 128 channels x (group | aux) columns over the page's tokens
+        float pacc[8][4];
+        float vaux[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int m = 0; m < 8; ++m) pacc[m][0] = pacc[m][1] = pacc[m][2] = pacc[m][3] = 0.f;
+        const uint8_t* vzero = vscale + 2 * G;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int t0 = 16 * ks + 2 * tig;
+            const uint32_t b0 = sm.pt[gid][t0 / 2];
+            const uint32_t b1 = sm.pt[gid][t0 / 2 + 4];
+            const uint32_t w0 = vw[8 * t0 + gid], w1 = vw[8 * (t0 + 1) + gid];
+            const uint32_t w2 = vw[8 * (t0 + 8) + gid], w3 = vw[8 * (t0 + 9) + gid];
+            mma_codes(kc, pacc, w0, w1, w2, w3, b0, b1);
+            const uint32_t z0 = lds32(vzero + 2 * t0);
+            const uint32_t z1 = lds32(vzero + 2 * (t0 + 8));
+            mma16816(vaux, row0 ? kOnes : 0u, row0 ? z0 : 0u, row0 ? kOnes : 0u, row0 ? z1 : 0u, b0, b1);
+        }
+        // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float sBv = __shfl_sync(0xffffffffu, vaux[j], tig & 1);
+            const float lp = __shfl_sync(0xffffffffu, vaux[j], 2 + (tig & 1));
+            const float zz = __shfl_sync(0xffffffffu, vaux[2 + j], 2 + (tig & 1));
+            ol[j] = ol[j] * corr[j] + lp;
+            const float c16 = zz - 64.f * sBv;
+            const float c64 = zz - 16.f * sBv;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                oacc[m][j] = fmaf(pacc[m][j], 1.f / 16.f, fmaf(oacc[m][j], corr[j], c16));
+                oacc[m][2 + j] = fmaf(pacc[m][2 + j], 1.f / 64.f, fmaf(oacc[m][2 + j], corr[j], c64));
+            }
+            om[j] = mnew[j];
+        }
+        __syncwarp();
+    };
+
+    // ---- work loop: one page pair (or one fp item) per iteration, single call
+    // sites so the hot body is emitted once --------------------------------------
+    int kind, u, p0, p1;
+    next_item(kind, u, p0, p1);
+    int nkind = 0, nu = 0, np0 = 0, np1 = 0;
+    if (kind != 0) next_item(nkind, nu, np0, np1);
+    bool first_issued = false;
+    int p = p0;
+#pragma unroll 1
+    while (kind != 0) {
+        bool item_done;
+        if (kind == 1) {
+            if (nkind == 2 && !first_issued) {
+                issue(nu, np0);
+                first_issued = true;
+            }
+            process_fp(u);
+            item_done = true;
+        } else {
+            if (p == p0) {
+                if (!first_issued) issue(u, p0);
+                first_issued = false;
+                load_unit(u);
+                om[0] = om[1] = -INFINITY;
+                ol[0] = ol[1] = 0.f;
+#pragma unroll
+                for (int m = 0; m < 8; ++m) oacc[m][0] = oacc[m][1] = oacc[m][2] = oacc[m][3] = 0.f;
+            }
+            // keep one page pair in flight behind the one being computed
+            const bool more = p + 1 < p1;
+            const int iu = more ? u : nu;
+            const int ip = more ? p + 1 : np0;
+            if (more || nkind == 2) {
+                issue(iu, ip);
+                if (!more) first_issued = true;
+            }
+            const int s = consumed & 1;
+            mbar_wait(&sm.mbar[s], (consumed >> 1) & 1);
+            page_pair(s);
+            ++consumed;
+            ++p;
+            item_done = p == p1;
+            if (item_done) {
+                // partial of this chunk: slot 1 + chunk
+                const int slot = 1 + p0 / P.ppc;
+                float* base = P.part + ((int64_t)u * (1 + P.cmax) + slot) * GROUP * (D + 2);
+                if (tig < 2) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int g = 2 * tig + j;
+                        if (g < GROUP) {
+#pragma unroll
+                            for (int m = 0; m < 8; ++m)
+                                *reinterpret_cast<float2*>(base + g * D + 16 * gid + 2 * m) =
+                                    make_float2(oacc[m][j], oacc[m][2 + j]);
+                            if (gid == 0) {
+                                base[GROUP * D + 2 * g] = om[j];
+                                base[GROUP * D + 2 * g + 1] = ol[j];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (item_done) {
+            finish_unit(u);
+            kind = nkind;
+            u = nu;
+            p0 = np0;
+            p1 = np1;
+            p = p0;
+            if (kind != 0) next_item(nkind, nu, np0, np1);
+        }
+    }
+    // the last warp out resets the work queue for the next launch
+    __syncwarp();
+    if (lane == 0) {
+        const int done = atomicAdd(&P.ctr[1], 1);
+        if (done == static_cast<int>(gridDim.x) * kWarps - 1) {
+            P.ctr[0] = 0;
+            P.ctr[1] = 0;
+        }
+    }
+}
+
+}  // namespace fastattn
+
+// ---- host side ---------------------------------------------------------------------
+
+using namespace fastattn;
+
+static int num_sms() {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+bool fast_attention_supported(const KittyCacheDesc& c) {
+    const int group = c.cfg.h_q / c.cfg.h_kv;
+    return c.cfg.d == D && c.cfg.g == G && c.cfg.key_bits == 2 && c.cfg.value_bits == 2 &&
+           (group == 1 || group == 2 || group == 4) && c.cfg.d_boost <= 32 &&
+           c.key_slot_bytes <= kKeySlotMax && c.value_slot_bytes == 4608;
+}
+
+struct FastPlan {
+    int ppc, cmax, units, group;
+    size_t ctr_bytes, part_bytes;
+};
+
+static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
+    FastPlan p;
+    p.units = c.num_seqs * c.cfg.h_kv;
+    p.group = c.cfg.h_q / c.cfg.h_kv;
+    const int past = max_tokens > c.cfg.s ? max_tokens - c.cfg.s : 0;
+    const int maxp = past / G + 1;
+    const long long pages = (long long)p.units * maxp;
+    const long long warps = (long long)num_sms() * kCtasPerSm * kWarps;
+    int ppc = static_cast<int>(pages / (2 * warps));
+    ppc = ppc < 1 ? 1 : (ppc > 8 ? 8 : ppc);
+    p.ppc = ppc;
+    p.cmax = (maxp + ppc - 1) / ppc;
+    p.ctr_bytes = (((size_t)(2 + p.units) * sizeof(int)) + 255) & ~size_t(255);
+    p.part_bytes = (size_t)p.units * (1 + p.cmax) * p.group * (D + 2) * sizeof(float);
+    return p;
+}
+
+size_t fast_attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
+    if (!fast_attention_supported(c)) return 0;
+    const FastPlan p = plan(c, max_tokens);
+    return p.ctr_bytes + p.part_bytes;
+}
+
+template <int GROUP, int NKH>
+static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
+    auto kfn = fast_attention_kernel<GROUP, NKH>;
+    const size_t sm = sizeof(WarpSmem) * kWarps;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, kWarps * 32, sm, st>>>(prm);
+    return cudaGetLastError();
+}
+
+template <int GROUP>
+static cudaError_t launch_g(const Params& prm, int nkh, int grid, cudaStream_t st) {
+    if (nkh == 0) return launch_t<GROUP, 0>(prm, grid, st);
+    if (nkh == 1) return launch_t<GROUP, 1>(prm, grid, st);
+    return launch_t<GROUP, 2>(prm, grid, st);
+}
+
+cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, void* out, int out_dtype,
+                                  int max_tokens, void* ws, size_t ws_bytes, cudaStream_t st) {
+    const FastPlan p = plan(c, max_tokens);
+    if (ws_bytes < p.ctr_bytes + p.part_bytes) return cudaErrorInvalidValue;
+    Params prm;
+    prm.c = c;
+    prm.q = q;
+    prm.out = out;
+    prm.out_dtype = out_dtype;
+    prm.ppc = p.ppc;
+    prm.cmax = p.cmax;
+    prm.units = p.units;
+    prm.ctr = static_cast<int*>(ws);
+    prm.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ctr_bytes);
+    const long long items = (long long)p.units * (1 + p.cmax);
+    long long ctas = (items + kWarps - 1) / kWarps;
+    const long long cap = (long long)num_sms() * kCtasPerSm;
+    const int grid = static_cast<int>(ctas < cap ? ctas : cap);
+    const int nkh = (c.cfg.d_boost + 15) / 16;
+    switch (p.group) {
+        case 1: return launch_g<1>(prm, nkh, grid, st);
+        case 2: return launch_g<2>(prm, nkh, grid, st);
+        default: return launch_g<4>(prm, nkh, grid, st);
+    }
 }
 
 }  // namespace kitty
