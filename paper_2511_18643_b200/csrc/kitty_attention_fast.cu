@@ -60,6 +60,7 @@ struct Params {
     int out_dtype;
     int ppc;    // page pairs per quantized item
     int cmax;   // quantized items per unit (grid bound)
+    int fmax;   // fp-token chunk items per unit (grid bound)
     int units;
     int* ctr;   // [0] next item, [1] finished warps, [2 + u] arrivals of unit u
     float* part;
@@ -221,7 +222,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     const int vslot = static_cast<int>(c.value_slot_bytes);
     const int scale_off = D * G / 4 + d_boost * G / 4 + D;  // KTYP key scales
     const int zero_off = scale_off + 2 * D;
-    const int total_items = P.units * (1 + P.cmax);
     const int hkv = c.cfg.h_kv;
 
     if (lane == 0) {
@@ -241,30 +241,41 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         __syncwarp();
         return __shfl_sync(0xffffffffu, i, 0);
     };
-    // item -> (kind, unit, first page, end page); kind 0 = end, 1 = fp, 2 = pages, 3 = empty
+    // item -> (kind, unit, a, b); kind 0 = end, 1 = fp chunk a, 2 = pages [a, b), 3 = empty.
+    // fp chunks and page chunks are interleaved so the latency-bound fp work
+    // of some warps overlaps the tensor-core work of the others.
+    const int nf = P.units * P.fmax, nq = P.units * P.cmax;
+    const int n2 = 2 * min(nf, nq);
     auto decode = [&](int it, int& kind, int& u, int& p0, int& p1) {
-        if (it >= total_items) {
+        if (it >= nf + nq) {
             kind = 0;
             return;
         }
-        if (it < P.units) {
-            kind = 1;
-            u = it;
-            p0 = p1 = 0;
-            return;
+        bool fp;
+        int idx;
+        if (it < n2) {
+            fp = (it & 1) == 0;
+            idx = it >> 1;
+        } else {
+            fp = nf > nq;
+            idx = it - n2 + min(nf, nq);
         }
-        const int i2 = it - P.units;
-        const int ch = i2 / P.units;
-        u = i2 - ch * P.units;
+        const int ch = idx / P.units;
+        u = idx - ch * P.units;
         const UnitGeom gm = unit_geom(c, u);
-        p0 = ch * P.ppc;
-        p1 = min(gm.vp, p0 + P.ppc);
-        kind = (p0 < p1 && gm.n > 0) ? 2 : 3;
+        if (fp) {
+            p0 = ch;
+            p1 = 0;
+            kind = (gm.n > 0 && ch * kFpChunk < gm.nfp) ? 1 : 3;
+        } else {
+            p0 = ch * P.ppc;
+            p1 = min(gm.vp, p0 + P.ppc);
+            kind = (p0 < p1 && gm.n > 0) ? 2 : 3;
+        }
     };
     auto next_item = [&](int& kind, int& u, int& p0, int& p1) {
         for (;;) {
             decode(pull(), kind, u, p0, p1);
-            if (kind == 1 && c.unit_len[u] == 0) continue;
             if (kind != 3) return;
         }
     };
@@ -317,17 +328,21 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         if (lane == 0) old = atomicAdd(&P.ctr[2 + u], 1);
         old = __shfl_sync(0xffffffffu, old, 0);
         const UnitGeom gm = unit_geom(c, u);
-        const int nparts = 1 + (gm.vp + P.ppc - 1) / P.ppc;
-        if (old != nparts - 1) return;
+        const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
+        const int nqc = (gm.vp + P.ppc - 1) / P.ppc;
+        if (old != nfc + nqc - 1) return;
         __threadfence();
         const int b = u / hkv, h = u - b * hkv;
-        const float* pb = P.part + (int64_t)u * (1 + P.cmax) * GROUP * (D + 2);
+        const float* pb = P.part + (int64_t)u * (P.fmax + P.cmax) * GROUP * (D + 2);
+        auto slot_of = [&](int i) { return i < nfc ? i : P.fmax + (i - nfc); };
+        const int nparts = nfc + nqc;
         for (int g = 0; g < GROUP; ++g) {
             float M = -INFINITY;
-            for (int i = 0; i < nparts; ++i) M = fmaxf(M, __ldcg(pb + (int64_t)i * GROUP * (D + 2) + GROUP * D + 2 * g));
+            for (int i = 0; i < nparts; ++i)
+                M = fmaxf(M, __ldcg(pb + (int64_t)slot_of(i) * GROUP * (D + 2) + GROUP * D + 2 * g));
             float L = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
             for (int i = 0; i < nparts; ++i) {
-                const float* pi = pb + (int64_t)i * GROUP * (D + 2);
+                const float* pi = pb + (int64_t)slot_of(i) * GROUP * (D + 2);
                 const float mi = __ldcg(pi + GROUP * D + 2 * g);
                 const float wgt = mi == -INFINITY ? 0.f : ex2(mi - M);
                 L += wgt * __ldcg(pi + GROUP * D + 2 * g + 1);
@@ -352,126 +367,134 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         if (lane == 0) P.ctr[2 + u] = 0;  // reset for the next launch
     };
 
-    // ---- full-precision tokens of a unit (sink, value q-buffer + local; keys
-    // of those tokens from the sink, a key page or the key q-buffer) --------
-    auto process_fp = [&](int u) {
+    // ---- one chunk of <= 32 full-precision tokens of a unit: the sink and the
+    // value q-buffer + local (cache.py:196-208); keys of those tokens come from
+    // the key sink, a key page (Alg. 1 from a shared-memory copy of the page)
+    // or the key q-buffer.  Lane = token for QK, lane = 4 channels for PV. ----
+    auto process_fp = [&](int u, int fc) {
         load_unit(u);
         const UnitGeom gm = unit_geom(c, u);
         const int s_len = min(gm.n, S);
-        const int T = gm.nfp;
-        float m[4], l[4], acc[4][4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            m[g] = -INFINITY;
-            l[g] = 0.f;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[g][i] = 0.f;
-        }
-        const uint16_t* ksink = c.k_sink + (int64_t)u * S * D;
-        const uint16_t* vsink = c.v_sink + (int64_t)u * S * D;
-        const uint16_t* kq = c.k_qbuf + (int64_t)u * G * D;
-        const uint16_t* vr = c.v_ring + (int64_t)u * W * D;
+        const int c0 = fc * kFpChunk;
+        const int cnt = min(kFpChunk, gm.nfp - c0);
         const int vbase = S + gm.vp * G;  // first value-fp token past the sink
-#pragma unroll 1
-        for (int c0 = 0; c0 < T; c0 += kFpChunk) {
-            const int j = c0 + lane;
-            const bool valid = j < T;
-            float lg[4] = {0.f, 0.f, 0.f, 0.f};
-            if (valid) {
-                const int t = j < s_len ? j : vbase + (j - s_len);
-                const uint16_t* krow = nullptr;
-                const uint8_t* kpg = nullptr;
-                int tl = 0;
-                if (t < S) {
-                    krow = ksink + (int64_t)t * D;
-                } else {
-                    const int pc = t - S;
-                    if (pc < gm.kp * G) {
-                        kpg = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + pc / G] * kslot;
-                        tl = pc % G;
-                    } else {
-                        krow = kq + (int64_t)(pc % G) * D;
-                    }
-                }
-                if (krow) {
-#pragma unroll 4
-                    for (int v8 = 0; v8 < D / 8; ++v8) {
-                        const uint4 w = reinterpret_cast<const uint4*>(krow)[v8];
-                        const float k8[8] = {__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u),
-                                             __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u),
-                                             __uint_as_float(w.z << 16), __uint_as_float(w.z & 0xffff0000u),
-                                             __uint_as_float(w.w << 16), __uint_as_float(w.w & 0xffff0000u)};
+        auto token_of = [&](int j) { return j < s_len ? j : vbase + (j - s_len); };
+        const bool valid = lane < cnt;
+        const int t = token_of(c0 + (valid ? lane : 0));
+        const int pc = t - S;
+        const bool in_page = t >= S && pc < gm.kp * G;
+        float lg[4] = {0.f, 0.f, 0.f, 0.f};
+        if (!in_page) {
+            const uint16_t* krow = t < S ? c.k_sink + ((int64_t)u * S + t) * D
+                                         : c.k_qbuf + ((int64_t)u * G + pc % G) * D;
+            uint4 w[16];
 #pragma unroll
-                        for (int g = 0; g < GROUP; ++g) {
-                            const float4 qa_ = *reinterpret_cast<const float4*>(&sm.qf[g][8 * v8]);
-                            const float4 qb_ = *reinterpret_cast<const float4*>(&sm.qf[g][8 * v8 + 4]);
-                            lg[g] = fmaf(qa_.x, k8[0], lg[g]);
-                            lg[g] = fmaf(qa_.y, k8[1], lg[g]);
-                            lg[g] = fmaf(qa_.z, k8[2], lg[g]);
-                            lg[g] = fmaf(qa_.w, k8[3], lg[g]);
-                            lg[g] = fmaf(qb_.x, k8[4], lg[g]);
-                            lg[g] = fmaf(qb_.y, k8[5], lg[g]);
-                            lg[g] = fmaf(qb_.z, k8[6], lg[g]);
-                            lg[g] = fmaf(qb_.w, k8[7], lg[g]);
-                        }
-                    }
-                } else {
-                    // key page token: Alg. 1 per element from the page in global memory
-                    const int sh = 2 * (tl & 3), byte = tl >> 2;
-#pragma unroll 2
-                    for (int d = 0; d < D; ++d) {
-                        uint32_t code = (kpg[d * (G / 4) + byte] >> sh) & 3u;
-                        const uint32_t r = kpg[D * G / 4 + d_boost * G / 4 + d];
-                        if (r != kSentinel) code |= ((kpg[D * G / 4 + r * (G / 4) + byte] >> sh) & 3u) << 2;
-                        const float s = half_bits_to_f32(ld_u16(kpg + scale_off + 2 * d));
-                        const float z = half_bits_to_f32(ld_u16(kpg + zero_off + 2 * d));
-                        const float kv = fmaf(static_cast<float>(code), s, z);
+            for (int i = 0; i < 16; ++i) w[i] = reinterpret_cast<const uint4*>(krow)[i];
 #pragma unroll
-                        for (int g = 0; g < GROUP; ++g) lg[g] = fmaf(sm.qf[g][d], kv, lg[g]);
-                    }
-                }
-            }
-            // online softmax over this chunk (log2 domain)
-#pragma unroll
-            for (int g = 0; g < GROUP; ++g) {
-                float x = valid ? lg[g] : -INFINITY;
-                float mc = x;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
-                const float mn = fmaxf(m[g], mc);
-                const float corr = ex2(m[g] - mn);
-                const float p = valid ? ex2(x - mn) : 0.f;
-                float ps = p;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-                l[g] = l[g] * corr + ps;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) acc[g][i] *= corr;
-                sm.ps[g][lane] = p;
-                m[g] = mn;
-            }
-            __syncwarp();
-            const int cnt = min(kFpChunk, T - c0);
-#pragma unroll 2
-            for (int jj = 0; jj < cnt; ++jj) {
-                const int jt = c0 + jj;
-                const int t = jt < s_len ? jt : vbase + (jt - s_len);
-                const uint16_t* vrow = t < S ? vsink + (int64_t)t * D : vr + (int64_t)((t - S) % W) * D;
-                const uint2 w = reinterpret_cast<const uint2*>(vrow)[lane];
-                const float v0 = __uint_as_float(w.x << 16), v1 = __uint_as_float(w.x & 0xffff0000u);
-                const float v2 = __uint_as_float(w.y << 16), v3 = __uint_as_float(w.y & 0xffff0000u);
+            for (int i = 0; i < 16; ++i) {
+                const float k8[8] = {__uint_as_float(w[i].x << 16), __uint_as_float(w[i].x & 0xffff0000u),
+                                     __uint_as_float(w[i].y << 16), __uint_as_float(w[i].y & 0xffff0000u),
+                                     __uint_as_float(w[i].z << 16), __uint_as_float(w[i].z & 0xffff0000u),
+                                     __uint_as_float(w[i].w << 16), __uint_as_float(w[i].w & 0xffff0000u)};
 #pragma unroll
                 for (int g = 0; g < GROUP; ++g) {
-                    const float pg = sm.ps[g][jj];
+                    const float4 qa_ = *reinterpret_cast<const float4*>(&sm.qf[g][8 * i]);
+                    const float4 qb_ = *reinterpret_cast<const float4*>(&sm.qf[g][8 * i + 4]);
+                    lg[g] = fmaf(qa_.x, k8[0], lg[g]);
+                    lg[g] = fmaf(qa_.y, k8[1], lg[g]);
+                    lg[g] = fmaf(qa_.z, k8[2], lg[g]);
+                    lg[g] = fmaf(qa_.w, k8[3], lg[g]);
+                    lg[g] = fmaf(qb_.x, k8[4], lg[g]);
+                    lg[g] = fmaf(qb_.y, k8[5], lg[g]);
+                    lg[g] = fmaf(qb_.z, k8[6], lg[g]);
+                    lg[g] = fmaf(qb_.w, k8[7], lg[g]);
+                }
+            }
+        }
+        // keys that sit in key pages: stage each such page in the free ring slot
+        unsigned need = __ballot_sync(0xffffffffu, valid && in_page);
+        while (need) {
+            const int src = __ffs(need) - 1;
+            const int page = __shfl_sync(0xffffffffu, pc / G, src);
+            uint8_t* buf = sm.stage[issued & 1];  // not in flight: <= 1 load outstanding here
+            const uint4* gsrc = reinterpret_cast<const uint4*>(
+                c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + page] * kslot);
+            uint4 tmp[12];
+#pragma unroll
+            for (int i = 0; i < 12; ++i)
+                if (lane + 32 * i < kslot / 16) tmp[i] = gsrc[lane + 32 * i];
+#pragma unroll
+            for (int i = 0; i < 12; ++i)
+                if (lane + 32 * i < kslot / 16) reinterpret_cast<uint4*>(buf)[lane + 32 * i] = tmp[i];
+            __syncwarp();
+            const bool mine = valid && in_page && pc / G == page;
+            if (mine) {
+                const int tl = pc % G, sh = 2 * (tl & 3), byte = tl >> 2;
+                const uint8_t* hb = buf + D * G / 4;
+                const uint8_t* ib = buf + D * G / 4 + d_boost * G / 4;
+#pragma unroll 4
+                for (int d = 0; d < D; ++d) {
+                    uint32_t code = (buf[d * (G / 4) + byte] >> sh) & 3u;
+                    const uint32_t r = ib[d];
+                    if (r != kSentinel) code |= ((hb[r * (G / 4) + byte] >> sh) & 3u) << 2;
+                    const float s_ = half_bits_to_f32(ld_u16(buf + scale_off + 2 * d));
+                    const float z_ = half_bits_to_f32(ld_u16(buf + zero_off + 2 * d));
+                    const float kv = fmaf(static_cast<float>(code), s_, z_);
+#pragma unroll
+                    for (int g = 0; g < GROUP; ++g) lg[g] = fmaf(sm.qf[g][d], kv, lg[g]);
+                }
+            }
+            __syncwarp();
+            need &= ~__ballot_sync(0xffffffffu, mine);
+        }
+        // softmax of the chunk (log2 domain)
+        float m[4], l[4];
+#pragma unroll
+        for (int g = 0; g < GROUP; ++g) {
+            const float x = valid ? lg[g] : -INFINITY;
+            float mc = x;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+            const float p = valid ? ex2(x - mc) : 0.f;
+            float ps = p;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            m[g] = mc;
+            l[g] = ps;
+            sm.ps[g][lane] = p;
+        }
+        __syncwarp();
+        // P V over the chunk: lane owns channels 4 lane .. 4 lane + 3
+        float acc[4][4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+        const uint16_t* vsink = c.v_sink + (int64_t)u * S * D;
+        const uint16_t* vr = c.v_ring + (int64_t)u * W * D;
+#pragma unroll 1
+        for (int j0 = 0; j0 < cnt; j0 += 16) {
+            uint2 vv[16];
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+                const int tt = token_of(c0 + min(j0 + jj, cnt - 1));
+                const uint16_t* vrow = tt < S ? vsink + (int64_t)tt * D : vr + (int64_t)((tt - S) % W) * D;
+                vv[jj] = reinterpret_cast<const uint2*>(vrow)[lane];
+            }
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+                const float v0 = __uint_as_float(vv[jj].x << 16), v1 = __uint_as_float(vv[jj].x & 0xffff0000u);
+                const float v2 = __uint_as_float(vv[jj].y << 16), v3 = __uint_as_float(vv[jj].y & 0xffff0000u);
+#pragma unroll
+                for (int g = 0; g < GROUP; ++g) {
+                    const float pg = (j0 + jj < cnt) ? sm.ps[g][j0 + jj] : 0.f;
                     acc[g][0] = fmaf(pg, v0, acc[g][0]);
                     acc[g][1] = fmaf(pg, v1, acc[g][1]);
                     acc[g][2] = fmaf(pg, v2, acc[g][2]);
                     acc[g][3] = fmaf(pg, v3, acc[g][3]);
                 }
             }
-            __syncwarp();
         }
-        float* base = P.part + ((int64_t)u * (1 + P.cmax)) * GROUP * (D + 2);
+        __syncwarp();
+        float* base = P.part + ((int64_t)u * (P.fmax + P.cmax) + fc) * GROUP * (D + 2);
 #pragma unroll
         for (int g = 0; g < GROUP; ++g) {
             reinterpret_cast<float4*>(base + g * D)[lane] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
@@ -643,7 +666,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 issue(nu, np0);
                 first_issued = true;
             }
-            process_fp(u);
+            process_fp(u, p0);
             item_done = true;
         } else {
             if (p == p0) {
@@ -671,8 +694,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             item_done = p == p1;
             if (item_done) {
                 // partial of this chunk: slot 1 + chunk
-                const int slot = 1 + p0 / P.ppc;
-                float* base = P.part + ((int64_t)u * (1 + P.cmax) + slot) * GROUP * (D + 2);
+                const int slot = P.fmax + p0 / P.ppc;
+                float* base = P.part + ((int64_t)u * (P.fmax + P.cmax) + slot) * GROUP * (D + 2);
                 if (tig < 2) {
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
@@ -737,7 +760,7 @@ bool fast_attention_supported(const KittyCacheDesc& c) {
 }
 
 struct FastPlan {
-    int ppc, cmax, units, group;
+    int ppc, cmax, fmax, units, group;
     size_t ctr_bytes, part_bytes;
 };
 
@@ -753,8 +776,11 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     ppc = ppc < 1 ? 1 : (ppc > 8 ? 8 : ppc);
     p.ppc = ppc;
     p.cmax = (maxp + ppc - 1) / ppc;
+    const int nfp_max = min(max_tokens, c.cfg.s + c.cfg.r + c.cfg.g - 1);
+    p.fmax = (nfp_max + kFpChunk - 1) / kFpChunk;
+    if (p.fmax < 1) p.fmax = 1;
     p.ctr_bytes = (((size_t)(2 + p.units) * sizeof(int)) + 255) & ~size_t(255);
-    p.part_bytes = (size_t)p.units * (1 + p.cmax) * p.group * (D + 2) * sizeof(float);
+    p.part_bytes = (size_t)p.units * (p.fmax + p.cmax) * p.group * (D + 2) * sizeof(float);
     return p;
 }
 
@@ -792,10 +818,11 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     prm.out_dtype = out_dtype;
     prm.ppc = p.ppc;
     prm.cmax = p.cmax;
+    prm.fmax = p.fmax;
     prm.units = p.units;
     prm.ctr = static_cast<int*>(ws);
     prm.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ctr_bytes);
-    const long long items = (long long)p.units * (1 + p.cmax);
+    const long long items = (long long)p.units * (p.fmax + p.cmax);
     long long ctas = (items + kWarps - 1) / kWarps;
     const long long cap = (long long)num_sms() * kCtasPerSm;
     const int grid = static_cast<int>(ctas < cap ? ctas : cap);
