@@ -49,6 +49,7 @@ struct __align__(128) WarpSmem {
     uint16_t qa4[4][D];             // 4 * q * alpha (f16) for boosted-row gathers
     float qf[4][D];                 // q * alpha (f32) for the fp routine
     float ps[4][kFpChunk];          // fp routine probabilities
+    uint32_t ones[64];              // f16x2 (1, 1): scale operand of the aux B columns
     uint8_t inv[32];                // boosted channel of high_bits row j
     unsigned long long mbar[2];
 };
@@ -230,6 +231,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     sm.inv[lane] = 0;
+    sm.ones[lane] = kOnes;
+    sm.ones[lane + 32] = kOnes;
     __syncwarp();
     const Consts kc;
 
@@ -321,7 +324,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
     };
 
-    // merge the partials of unit u (called by the warp that completed it)
+    // merge the partials of unit u (run by the warp that completed its last
+    // item): log-sum-exp over the fp chunks and the page chunks, loads batched
+    // across lanes / partials so the merge is not latency-serialised.
     auto finish_unit = [&](int u) {
         __threadfence();
         int old = 0;
@@ -330,37 +335,83 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         const UnitGeom gm = unit_geom(c, u);
         const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
         const int nqc = (gm.vp + P.ppc - 1) / P.ppc;
-        if (old != nfc + nqc - 1) return;
+        const int nparts = nfc + nqc;
+        if (old != nparts - 1) return;
         __threadfence();
         const int b = u / hkv, h = u - b * hkv;
-        const float* pb = P.part + (int64_t)u * (P.fmax + P.cmax) * GROUP * (D + 2);
-        auto slot_of = [&](int i) { return i < nfc ? i : P.fmax + (i - nfc); };
-        const int nparts = nfc + nqc;
+        constexpr int kStride = GROUP * (D + 2);
+        const float* pb = P.part + (int64_t)u * (P.fmax + P.cmax) * kStride;
+        auto part_ptr = [&](int i) { return pb + (int64_t)(i < nfc ? i : P.fmax + (i - nfc)) * kStride; };
+        float M[GROUP], L[GROUP];
+#pragma unroll
         for (int g = 0; g < GROUP; ++g) {
-            float M = -INFINITY;
-            for (int i = 0; i < nparts; ++i)
-                M = fmaxf(M, __ldcg(pb + (int64_t)slot_of(i) * GROUP * (D + 2) + GROUP * D + 2 * g));
-            float L = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
-            for (int i = 0; i < nparts; ++i) {
-                const float* pi = pb + (int64_t)slot_of(i) * GROUP * (D + 2);
-                const float mi = __ldcg(pi + GROUP * D + 2 * g);
-                const float wgt = mi == -INFINITY ? 0.f : ex2(mi - M);
-                L += wgt * __ldcg(pi + GROUP * D + 2 * g + 1);
-                const float4 a = __ldcg(reinterpret_cast<const float4*>(pi + g * D) + lane);
-                o0 += wgt * a.x;
-                o1 += wgt * a.y;
-                o2 += wgt * a.z;
-                o3 += wgt * a.w;
+            M[g] = -INFINITY;
+            L[g] = 0.f;
+        }
+        for (int i = lane; i < nparts; i += 32) {
+            const float* ml = part_ptr(i) + GROUP * D;
+#pragma unroll
+            for (int g = 0; g < GROUP; ++g) M[g] = fmaxf(M[g], __ldcg(ml + 2 * g));
+        }
+#pragma unroll
+        for (int g = 0; g < GROUP; ++g) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
+        }
+        float o4[GROUP][4];
+#pragma unroll
+        for (int g = 0; g < GROUP; ++g) o4[g][0] = o4[g][1] = o4[g][2] = o4[g][3] = 0.f;
+        for (int i0 = 0; i0 < nparts; i0 += 32) {
+            float wl[GROUP];
+            const int mine = i0 + lane;
+            if (mine < nparts) {
+                const float* ml = part_ptr(mine) + GROUP * D;
+#pragma unroll
+                for (int g = 0; g < GROUP; ++g) {
+                    const float mi = __ldcg(ml + 2 * g);
+                    wl[g] = mi == -INFINITY ? 0.f : ex2(mi - M[g]);
+                    L[g] += wl[g] * __ldcg(ml + 2 * g + 1);
+                }
+            } else {
+#pragma unroll
+                for (int g = 0; g < GROUP; ++g) wl[g] = 0.f;
             }
-            const float inv = 1.f / L;
+            const int cnt = min(32, nparts - i0);
+            for (int j = 0; j < cnt; j += 4) {
+                float4 a[4][GROUP];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const float* pi = part_ptr(i0 + min(j + jj, cnt - 1));
+#pragma unroll
+                    for (int g = 0; g < GROUP; ++g) a[jj][g] = __ldcg(reinterpret_cast<const float4*>(pi + g * D) + lane);
+                }
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+#pragma unroll
+                    for (int g = 0; g < GROUP; ++g) {
+                        float w = __shfl_sync(0xffffffffu, wl[g], (j + jj) & 31);
+                        w = (j + jj < cnt) ? w : 0.f;
+                        o4[g][0] = fmaf(w, a[jj][g].x, o4[g][0]);
+                        o4[g][1] = fmaf(w, a[jj][g].y, o4[g][1]);
+                        o4[g][2] = fmaf(w, a[jj][g].z, o4[g][2]);
+                        o4[g][3] = fmaf(w, a[jj][g].w, o4[g][3]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < GROUP; ++g) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) L[g] += __shfl_xor_sync(0xffffffffu, L[g], o);
+            const float inv = 1.f / L[g];
             const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
             if (P.out_dtype == KITTY_F32) {
                 reinterpret_cast<float4*>(static_cast<float*>(P.out) + row * D)[lane] =
-                    make_float4(o0 * inv, o1 * inv, o2 * inv, o3 * inv);
+                    make_float4(o4[g][0] * inv, o4[g][1] * inv, o4[g][2] * inv, o4[g][3] * inv);
             } else {
                 uint2 v;
-                v.x = f32_to_bf16_bits(o0 * inv) | (f32_to_bf16_bits(o1 * inv) << 16);
-                v.y = f32_to_bf16_bits(o2 * inv) | (f32_to_bf16_bits(o3 * inv) << 16);
+                v.x = f32_to_bf16_bits(o4[g][0] * inv) | (f32_to_bf16_bits(o4[g][1] * inv) << 16);
+                v.y = f32_to_bf16_bits(o4[g][2] * inv) | (f32_to_bf16_bits(o4[g][3] * inv) << 16);
                 reinterpret_cast<uint2*>(static_cast<uint16_t*>(P.out) + row * D)[lane] = v;
             }
         }
@@ -506,7 +557,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     };
 
     // ---- one quantized K/V page pair in stage s ----------------------------------
-    float om[2], ol[2], oacc[8][4];
+    float om[2], ol[2], ob16[2], ob64[2], oacc[8][4];
     auto page_pair = [&](int s) {
         const uint8_t* kp = sm.stage[s];
         const uint8_t* vp = sm.stage[s] + kslot;
@@ -531,21 +582,23 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         float aux[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+        // aux lanes (B columns 4-7) read their "scale" from a ones buffer
+        const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
+        const uint32_t onesA = row0 ? kOnes : 0u;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             const int c0 = 16 * ks + 2 * tig;
-            uint32_t s0 = lds32(kp + scale_off + 2 * c0);
-            uint32_t s1 = lds32(kp + scale_off + 2 * (c0 + 8));
-            s0 = main_col ? s0 : kOnes;
-            s1 = main_col ? s1 : kOnes;
-            const uint32_t b0 = hmul2(qa[ks][0], s0);
-            const uint32_t b1 = hmul2(qa[ks][1], s1);
+            const uint32_t b0 = hmul2(qa[ks][0], lds32(sbase + 2 * c0));
+            const uint32_t b1 = hmul2(qa[ks][1], lds32(sbase + 2 * (c0 + 8)));
             const uint32_t w0 = kw[8 * c0 + gid], w1 = kw[8 * (c0 + 1) + gid];
             const uint32_t w2 = kw[8 * (c0 + 8) + gid], w3 = kw[8 * (c0 + 9) + gid];
             mma_codes(kc, acc, w0, w1, w2, w3, b0, b1);
-            const uint32_t z0 = lds32(kp + zero_off + 2 * c0);
-            const uint32_t z1 = lds32(kp + zero_off + 2 * (c0 + 8));
-            mma16816(aux, row0 ? kOnes : 0u, row0 ? z0 : 0u, row0 ? kOnes : 0u, row0 ? z1 : 0u, b0, b1);
+            uint32_t z0 = 0u, z1 = 0u;
+            if (row0) {
+                z0 = lds32(kp + zero_off + 2 * c0);
+                z1 = lds32(kp + zero_off + 2 * (c0 + 8));
+            }
+            mma16816(aux, onesA, z0, onesA, z1, b0, b1);
         }
 #pragma unroll
         for (int hk = 0; hk < NKH; ++hk) {
@@ -564,7 +617,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const uint32_t* hw = reinterpret_cast<const uint32_t*>(kp + D * G / 4);
             mma_codes(kc, acc, hw[8 * j0 + gid], hw[8 * (j0 + 1) + gid], hw[8 * (j0 + 8) + gid], hw[8 * (j0 + 9) + gid],
                       b0, b1);
-            mma16816(aux, row0 ? kOnes : 0u, 0u, row0 ? kOnes : 0u, 0u, b0, b1);
+            mma16816(aux, onesA, 0u, onesA, 0u, b0, b1);
         }
         // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha)
         float sumB[2], cst[2];
@@ -627,23 +680,37 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const uint32_t w0 = vw[8 * t0 + gid], w1 = vw[8 * (t0 + 1) + gid];
             const uint32_t w2 = vw[8 * (t0 + 8) + gid], w3 = vw[8 * (t0 + 9) + gid];
             mma_codes(kc, pacc, w0, w1, w2, w3, b0, b1);
-            const uint32_t z0 = lds32(vzero + 2 * t0);
-            const uint32_t z1 = lds32(vzero + 2 * (t0 + 8));
-            mma16816(vaux, row0 ? kOnes : 0u, row0 ? z0 : 0u, row0 ? kOnes : 0u, row0 ? z1 : 0u, b0, b1);
+            uint32_t z0 = 0u, z1 = 0u;
+            if (row0) {
+                z0 = lds32(vzero + 2 * t0);
+                z1 = lds32(vzero + 2 * (t0 + 8));
+            }
+            mma16816(vaux, onesA, z0, onesA, z1, b0, b1);
         }
-        // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z)
+        // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z).
+        // Row constants (zero points, the 1024 offset) accumulate per column in
+        // ob16 / ob64 and are added at the flush; the accumulators are only
+        // rescaled when a running max moved (warp vote).
+        const bool rescale = __any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const float sBv = __shfl_sync(0xffffffffu, vaux[j], tig & 1);
             const float lp = __shfl_sync(0xffffffffu, vaux[j], 2 + (tig & 1));
             const float zz = __shfl_sync(0xffffffffu, vaux[2 + j], 2 + (tig & 1));
-            ol[j] = ol[j] * corr[j] + lp;
-            const float c16 = zz - 64.f * sBv;
-            const float c64 = zz - 16.f * sBv;
+            ol[j] = fmaf(ol[j], corr[j], lp);
+            ob16[j] = fmaf(ob16[j], corr[j], zz - 64.f * sBv);
+            ob64[j] = fmaf(ob64[j], corr[j], zz - 16.f * sBv);
+            if (rescale) {
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    oacc[m][j] *= corr[j];
+                    oacc[m][2 + j] *= corr[j];
+                }
+            }
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                oacc[m][j] = fmaf(pacc[m][j], 1.f / 16.f, fmaf(oacc[m][j], corr[j], c16));
-                oacc[m][2 + j] = fmaf(pacc[m][2 + j], 1.f / 64.f, fmaf(oacc[m][2 + j], corr[j], c64));
+                oacc[m][j] = fmaf(pacc[m][j], 1.f / 16.f, oacc[m][j]);
+                oacc[m][2 + j] = fmaf(pacc[m][2 + j], 1.f / 64.f, oacc[m][2 + j]);
             }
             om[j] = mnew[j];
         }
@@ -675,6 +742,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 load_unit(u);
                 om[0] = om[1] = -INFINITY;
                 ol[0] = ol[1] = 0.f;
+                ob16[0] = ob16[1] = ob64[0] = ob64[1] = 0.f;
 #pragma unroll
                 for (int m = 0; m < 8; ++m) oacc[m][0] = oacc[m][1] = oacc[m][2] = oacc[m][3] = 0.f;
             }
@@ -704,7 +772,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
                             for (int m = 0; m < 8; ++m)
                                 *reinterpret_cast<float2*>(base + g * D + 16 * gid + 2 * m) =
-                                    make_float2(oacc[m][j], oacc[m][2 + j]);
+                                    make_float2(oacc[m][j] + ob16[j], oacc[m][2 + j] + ob64[j]);
                             if (gid == 0) {
                                 base[GROUP * D + 2 * g] = om[j];
                                 base[GROUP * D + 2 * g + 1] = ol[j];

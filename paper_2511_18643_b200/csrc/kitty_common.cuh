@@ -34,8 +34,12 @@ __device__ __forceinline__ uint32_t f32_to_half_bits(float f) {
     asm("cvt.u32.u16 %0, %1;" : "=r"(r) : "h"(h));
     return r;
 }
-__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
-    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+__device__ __forceinline__ uint32_t f32_to_bf16_bits(float f) {
+    unsigned short h;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(f));
+    uint32_t r;
+    asm("cvt.u32.u16 %0, %1;" : "=r"(r) : "h"(h));
+    return r;
 }
 
 // Byte offsets of the KTYP key body components (pages.py:215-221).
