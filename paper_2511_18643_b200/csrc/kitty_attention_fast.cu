@@ -34,24 +34,30 @@ namespace fastattn {
 constexpr int D = 128;
 constexpr int G = 128;
 constexpr int kWarps = 4;         // warps per CTA
-constexpr int kCtasPerSm = 2;
+constexpr int kCtasPerSm = 3;      // 12 warps per SM
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
-constexpr int kStageBytes = kKeySlotMax + 4608;
+constexpr int kValueSlot = 4608;
 constexpr int kPtStride = 136;     // f16 per row of the transposed-P buffer
 constexpr int kFpChunk = 32;       // fp tokens per online-softmax step
 constexpr float kAlpha = 0.12751743074f;  // log2(e) / sqrt(128)
 constexpr uint32_t kMagic = 0x64006400u;  // f16x2 (1024, 1024)
 constexpr uint32_t kOnes = 0x3C003C00u;   // f16x2 (1, 1)
 
+// Per-warp shared memory (13.3 KB): one key-page slot and one value-page slot,
+// each refilled by cp.async.bulk one page ahead of its use.
 struct __align__(128) WarpSmem {
-    uint8_t stage[2][kStageBytes];  // K page | V page (KTYP bodies)
-    uint32_t pt[8][kPtStride / 2];  // P^T as f16x2: rows 0-3 p*s, rows 4-7 p
-    uint16_t qa4[4][D];             // 4 * q * alpha (f16) for boosted-row gathers
-    float qf[4][D];                 // q * alpha (f32) for the fp routine
-    float ps[4][kFpChunk];          // fp routine probabilities
-    uint32_t ones[64];              // f16x2 (1, 1): scale operand of the aux B columns
-    uint8_t inv[32];                // boosted channel of high_bits row j
-    unsigned long long mbar[2];
+    uint8_t kbuf[kKeySlotMax];  // KTYP key body (also the fp routine's staged key page)
+    uint8_t vbuf[kValueSlot];   // KTYP value body
+    union {
+        uint32_t pt[8][kPtStride / 2];  // P^T as f16x2: rows 0-3 p*s, rows 4-7 p
+        struct {
+            float qf[4][D];          // q * alpha (f32) for the fp routine
+            float ps[4][kFpChunk];   // fp routine probabilities
+        } fp;
+    } u;
+    uint32_t ones[64];            // f16x2 (1, 1): scale operand of the aux B columns
+    uint8_t inv[32];              // boosted channel of high_bits row j
+    unsigned long long mbar[2];   // [0] key slot, [1] value slot
 };
 
 struct Params {
@@ -102,7 +108,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
@@ -173,23 +179,19 @@ __device__ __forceinline__ void conv_byte(const Consts& k, uint32_t w0, uint32_t
 // rows = (w0, w1) pair P0 and (w2, w3) pair P1.
 __device__ __forceinline__ void mma_codes(const Consts& k, float (&acc)[8][4], uint32_t w0, uint32_t w1,
                                           uint32_t w2, uint32_t w3, uint32_t b0, uint32_t b1) {
-    uint32_t e0, e1, o0, o1, E0, E1, O0, O1;
-    conv_byte<0>(k, w0, w1, e0, e1, o0, o1);
-    conv_byte<0>(k, w2, w3, E0, E1, O0, O1);
-    mma16816(acc[0], e0, e1, E0, E1, b0, b1);
-    mma16816(acc[1], o0, o1, O0, O1, b0, b1);
-    conv_byte<1>(k, w0, w1, e0, e1, o0, o1);
-    conv_byte<1>(k, w2, w3, E0, E1, O0, O1);
-    mma16816(acc[2], e0, e1, E0, E1, b0, b1);
-    mma16816(acc[3], o0, o1, O0, O1, b0, b1);
-    conv_byte<2>(k, w0, w1, e0, e1, o0, o1);
-    conv_byte<2>(k, w2, w3, E0, E1, O0, O1);
-    mma16816(acc[4], e0, e1, E0, E1, b0, b1);
-    mma16816(acc[5], o0, o1, O0, O1, b0, b1);
-    conv_byte<3>(k, w0, w1, e0, e1, o0, o1);
-    conv_byte<3>(k, w2, w3, E0, E1, O0, O1);
-    mma16816(acc[6], e0, e1, E0, E1, b0, b1);
-    mma16816(acc[7], o0, o1, O0, O1, b0, b1);
+    // all 8 tiles' A fragments first (32 registers): distinct registers let the
+    // HMMAs issue back to back instead of waiting on operand-read WAR hazards
+    uint32_t a[8][4];
+    conv_byte<0>(k, w0, w1, a[0][0], a[0][1], a[1][0], a[1][1]);
+    conv_byte<0>(k, w2, w3, a[0][2], a[0][3], a[1][2], a[1][3]);
+    conv_byte<1>(k, w0, w1, a[2][0], a[2][1], a[3][0], a[3][1]);
+    conv_byte<1>(k, w2, w3, a[2][2], a[2][3], a[3][2], a[3][3]);
+    conv_byte<2>(k, w0, w1, a[4][0], a[4][1], a[5][0], a[5][1]);
+    conv_byte<2>(k, w2, w3, a[4][2], a[4][3], a[5][2], a[5][3]);
+    conv_byte<3>(k, w0, w1, a[6][0], a[6][1], a[7][0], a[7][1]);
+    conv_byte<3>(k, w2, w3, a[6][2], a[6][3], a[7][2], a[7][3]);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) mma16816(acc[m], a[m][0], a[m][1], a[m][2], a[m][3], b0, b1);
 }
 
 struct UnitGeom {
@@ -224,6 +226,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     const int scale_off = D * G / 4 + d_boost * G / 4 + D;  // KTYP key scales
     const int zero_off = scale_off + 2 * D;
     const int hkv = c.cfg.h_kv;
+    const bool main_col = gid < 4;
+    const bool row0 = gid == 0;
 
     if (lane == 0) {
         mbar_init(&sm.mbar[0], 1);
@@ -235,8 +239,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     sm.ones[lane + 32] = kOnes;
     __syncwarp();
     const Consts kc;
+    const uint32_t onesA = row0 ? kOnes : 0u;
 
-    uint32_t issued = 0, consumed = 0;
+    uint32_t kph = 0, vph = 0;  // mbarrier parities of the two slots
 
     auto pull = [&]() -> int {
         int i = 0;
@@ -282,44 +287,42 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             if (kind != 3) return;
         }
     };
-    auto issue = [&](int u, int p) {
-        const int s = issued & 1;
+    auto issue_k = [&](int u, int p) {
         if (lane == 0) {
-            const uint8_t* ks = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * kslot;
-            const uint8_t* vs = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * vslot;
-            mbar_expect_tx(&sm.mbar[s], kslot + vslot);
-            bulk_g2s(sm.stage[s], ks, kslot, &sm.mbar[s]);
-            bulk_g2s(sm.stage[s] + kslot, vs, vslot, &sm.mbar[s]);
+            const uint8_t* src = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * kslot;
+            mbar_expect_tx(&sm.mbar[0], kslot);
+            bulk_g2s(sm.kbuf, src, kslot, &sm.mbar[0]);
         }
         __syncwarp();
-        ++issued;
+    };
+    auto issue_v = [&](int u, int p) {
+        if (lane == 0) {
+            const uint8_t* src = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * vslot;
+            mbar_expect_tx(&sm.mbar[1], vslot);
+            bulk_g2s(sm.vbuf, src, vslot, &sm.mbar[1]);
+        }
+        __syncwarp();
     };
 
-    // per-unit query state
+    // per-unit query state: B fragments of q*alpha (f16x2) for this lane's column
     int cur_unit = -1;
-    uint32_t qa[8][2];  // B fragments of q*alpha (f16x2) for this lane's column
+    uint32_t qa[8][2];
+    auto q_row = [&](int u, int g) {
+        const int b = u / hkv, h = u - b * hkv;
+        return P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g) * D;
+    };
     auto load_unit = [&](int u) {
         if (u == cur_unit) return;
         cur_unit = u;
-        const int b = u / hkv, h = u - b * hkv;
-        const uint16_t* qg = P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP) * D;
-        for (int g = 0; g < 4; ++g) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int d = 4 * lane + i;
-                const float v = g < GROUP ? bf16_to_f32(qg[g * D + d]) * kAlpha : 0.f;
-                sm.qf[g][d] = v;
-                sm.qa4[g][d] = static_cast<uint16_t>(f32_to_half_bits(4.f * v));
-            }
-        }
-        __syncwarp();
         const int col = gid & 3;
+        const uint16_t* qg = q_row(u, col < GROUP ? col : 0);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
                 const int d = 16 * ks + 2 * tig + 8 * hh;
-                qa[ks][hh] = pack_f16x2(sm.qf[col][d], sm.qf[col][d + 1]);
+                const uint32_t w = col < GROUP ? __ldg(reinterpret_cast<const unsigned int*>(qg + d)) : 0u;
+                qa[ks][hh] = pack_f16x2(__uint_as_float(w << 16) * kAlpha, __uint_as_float(w & 0xffff0000u) * kAlpha);
             }
         }
     };
@@ -377,16 +380,16 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 for (int g = 0; g < GROUP; ++g) wl[g] = 0.f;
             }
             const int cnt = min(32, nparts - i0);
-            for (int j = 0; j < cnt; j += 4) {
-                float4 a[4][GROUP];
+            for (int j = 0; j < cnt; j += 2) {
+                float4 a[2][GROUP];
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
+                for (int jj = 0; jj < 2; ++jj) {
                     const float* pi = part_ptr(i0 + min(j + jj, cnt - 1));
 #pragma unroll
                     for (int g = 0; g < GROUP; ++g) a[jj][g] = __ldcg(reinterpret_cast<const float4*>(pi + g * D) + lane);
                 }
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
+                for (int jj = 0; jj < 2; ++jj) {
 #pragma unroll
                     for (int g = 0; g < GROUP; ++g) {
                         float w = __shfl_sync(0xffffffffu, wl[g], (j + jj) & 31);
@@ -421,15 +424,24 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     // ---- one chunk of <= 32 full-precision tokens of a unit: the sink and the
     // value q-buffer + local (cache.py:196-208); keys of those tokens come from
     // the key sink, a key page (Alg. 1 from a shared-memory copy of the page)
-    // or the key q-buffer.  Lane = token for QK, lane = 4 channels for PV. ----
-    auto process_fp = [&](int u, int fc) {
-        load_unit(u);
+    // or the key q-buffer.  Lane = token for QK, lane = 4 channels for PV.
+    // `prefetch` is called once the key slot is free again. ----
+    auto process_fp = [&](int u, int fc, auto&& prefetch) {
         const UnitGeom gm = unit_geom(c, u);
         const int s_len = min(gm.n, S);
         const int c0 = fc * kFpChunk;
         const int cnt = min(kFpChunk, gm.nfp - c0);
         const int vbase = S + gm.vp * G;  // first value-fp token past the sink
         auto token_of = [&](int j) { return j < s_len ? j : vbase + (j - s_len); };
+        // q * alpha (f32) into shared memory
+#pragma unroll
+        for (int g = 0; g < GROUP; ++g) {
+            const uint2 w = __ldg(reinterpret_cast<const uint2*>(q_row(u, g)) + lane);
+            *reinterpret_cast<float4*>(&sm.u.fp.qf[g][4 * lane]) =
+                make_float4(__uint_as_float(w.x << 16) * kAlpha, __uint_as_float(w.x & 0xffff0000u) * kAlpha,
+                            __uint_as_float(w.y << 16) * kAlpha, __uint_as_float(w.y & 0xffff0000u) * kAlpha);
+        }
+        __syncwarp();
         const bool valid = lane < cnt;
         const int t = token_of(c0 + (valid ? lane : 0));
         const int pc = t - S;
@@ -438,45 +450,52 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         if (!in_page) {
             const uint16_t* krow = t < S ? c.k_sink + ((int64_t)u * S + t) * D
                                          : c.k_qbuf + ((int64_t)u * G + pc % G) * D;
-            uint4 w[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) w[i] = reinterpret_cast<const uint4*>(krow)[i];
+            for (int half = 0; half < 2; ++half) {
+                uint4 w[8];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float k8[8] = {__uint_as_float(w[i].x << 16), __uint_as_float(w[i].x & 0xffff0000u),
-                                     __uint_as_float(w[i].y << 16), __uint_as_float(w[i].y & 0xffff0000u),
-                                     __uint_as_float(w[i].z << 16), __uint_as_float(w[i].z & 0xffff0000u),
-                                     __uint_as_float(w[i].w << 16), __uint_as_float(w[i].w & 0xffff0000u)};
+                for (int i = 0; i < 8; ++i) w[i] = reinterpret_cast<const uint4*>(krow)[8 * half + i];
 #pragma unroll
-                for (int g = 0; g < GROUP; ++g) {
-                    const float4 qa_ = *reinterpret_cast<const float4*>(&sm.qf[g][8 * i]);
-                    const float4 qb_ = *reinterpret_cast<const float4*>(&sm.qf[g][8 * i + 4]);
-                    lg[g] = fmaf(qa_.x, k8[0], lg[g]);
-                    lg[g] = fmaf(qa_.y, k8[1], lg[g]);
-                    lg[g] = fmaf(qa_.z, k8[2], lg[g]);
-                    lg[g] = fmaf(qa_.w, k8[3], lg[g]);
-                    lg[g] = fmaf(qb_.x, k8[4], lg[g]);
-                    lg[g] = fmaf(qb_.y, k8[5], lg[g]);
-                    lg[g] = fmaf(qb_.z, k8[6], lg[g]);
-                    lg[g] = fmaf(qb_.w, k8[7], lg[g]);
+                for (int i = 0; i < 8; ++i) {
+                    const int d0 = 8 * (8 * half + i);
+                    const float k8[8] = {__uint_as_float(w[i].x << 16), __uint_as_float(w[i].x & 0xffff0000u),
+                                         __uint_as_float(w[i].y << 16), __uint_as_float(w[i].y & 0xffff0000u),
+                                         __uint_as_float(w[i].z << 16), __uint_as_float(w[i].z & 0xffff0000u),
+                                         __uint_as_float(w[i].w << 16), __uint_as_float(w[i].w & 0xffff0000u)};
+#pragma unroll
+                    for (int g = 0; g < GROUP; ++g) {
+                        const float4 qa_ = *reinterpret_cast<const float4*>(&sm.u.fp.qf[g][d0]);
+                        const float4 qb_ = *reinterpret_cast<const float4*>(&sm.u.fp.qf[g][d0 + 4]);
+                        lg[g] = fmaf(qa_.x, k8[0], lg[g]);
+                        lg[g] = fmaf(qa_.y, k8[1], lg[g]);
+                        lg[g] = fmaf(qa_.z, k8[2], lg[g]);
+                        lg[g] = fmaf(qa_.w, k8[3], lg[g]);
+                        lg[g] = fmaf(qb_.x, k8[4], lg[g]);
+                        lg[g] = fmaf(qb_.y, k8[5], lg[g]);
+                        lg[g] = fmaf(qb_.z, k8[6], lg[g]);
+                        lg[g] = fmaf(qb_.w, k8[7], lg[g]);
+                    }
                 }
             }
         }
-        // keys that sit in key pages: stage each such page in the free ring slot
+        // keys that sit in key pages: stage each such page in the (idle) key slot
         unsigned need = __ballot_sync(0xffffffffu, valid && in_page);
         while (need) {
             const int src = __ffs(need) - 1;
             const int page = __shfl_sync(0xffffffffu, pc / G, src);
-            uint8_t* buf = sm.stage[issued & 1];  // not in flight: <= 1 load outstanding here
+            uint8_t* buf = sm.kbuf;
             const uint4* gsrc = reinterpret_cast<const uint4*>(
                 c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + page] * kslot);
-            uint4 tmp[12];
 #pragma unroll
-            for (int i = 0; i < 12; ++i)
-                if (lane + 32 * i < kslot / 16) tmp[i] = gsrc[lane + 32 * i];
+            for (int i0 = 0; i0 < 12; i0 += 6) {
+                uint4 tmp[6];
 #pragma unroll
-            for (int i = 0; i < 12; ++i)
-                if (lane + 32 * i < kslot / 16) reinterpret_cast<uint4*>(buf)[lane + 32 * i] = tmp[i];
+                for (int i = 0; i < 6; ++i)
+                    if (lane + 32 * (i0 + i) < kslot / 16) tmp[i] = gsrc[lane + 32 * (i0 + i)];
+#pragma unroll
+                for (int i = 0; i < 6; ++i)
+                    if (lane + 32 * (i0 + i) < kslot / 16) reinterpret_cast<uint4*>(buf)[lane + 32 * (i0 + i)] = tmp[i];
+            }
             __syncwarp();
             const bool mine = valid && in_page && pc / G == page;
             if (mine) {
@@ -492,12 +511,13 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                     const float z_ = half_bits_to_f32(ld_u16(buf + zero_off + 2 * d));
                     const float kv = fmaf(static_cast<float>(code), s_, z_);
 #pragma unroll
-                    for (int g = 0; g < GROUP; ++g) lg[g] = fmaf(sm.qf[g][d], kv, lg[g]);
+                    for (int g = 0; g < GROUP; ++g) lg[g] = fmaf(sm.u.fp.qf[g][d], kv, lg[g]);
                 }
             }
             __syncwarp();
             need &= ~__ballot_sync(0xffffffffu, mine);
         }
+        prefetch();  // key slot is free: start the next page item's loads
         // softmax of the chunk (log2 domain)
         float m[4], l[4];
 #pragma unroll
@@ -512,7 +532,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
             m[g] = mc;
             l[g] = ps;
-            sm.ps[g][lane] = p;
+            sm.u.fp.ps[g][lane] = p;
         }
         __syncwarp();
         // P V over the chunk: lane owns channels 4 lane .. 4 lane + 3
@@ -536,7 +556,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 const float v2 = __uint_as_float(vv[jj].y << 16), v3 = __uint_as_float(vv[jj].y & 0xffff0000u);
 #pragma unroll
                 for (int g = 0; g < GROUP; ++g) {
-                    const float pg = (j0 + jj < cnt) ? sm.ps[g][j0 + jj] : 0.f;
+                    const float pg = (j0 + jj < cnt) ? sm.u.fp.ps[g][j0 + jj] : 0.f;
                     acc[g][0] = fmaf(pg, v0, acc[g][0]);
                     acc[g][1] = fmaf(pg, v1, acc[g][1]);
                     acc[g][2] = fmaf(pg, v2, acc[g][2]);
@@ -556,16 +576,14 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
     };
 
-    // ---- one quantized K/V page pair in stage s ----------------------------------
+    // ---- quantized pages: QK^T on the key slot, then P V on the value slot ----
     float om[2], ol[2], ob16[2], ob64[2], oacc[8][4];
-    auto page_pair = [&](int s) {
-        const uint8_t* kp = sm.stage[s];
-        const uint8_t* vp = sm.stage[s] + kslot;
-        const uint32_t* kw = reinterpret_cast<const uint32_t*>(kp);
-        const uint32_t* vw = reinterpret_cast<const uint32_t*>(vp);
-        const bool main_col = gid < 4;
-        const bool row0 = gid == 0;
+    float acc[8][4];  // logits, then probabilities, of the current page
+    float mnew[2], corr[2], b16[2], b64[2];
 
+    auto qk_page = [&]() {
+        const uint8_t* kp = sm.kbuf;
+        const uint32_t* kw = reinterpret_cast<const uint32_t*>(kp);
         // boosted rows -> channels (inverse of boost_idx)
         if (NKH > 0) {
             const uint32_t bw = lds32(kp + D * G / 4 + d_boost * G / 4 + 4 * lane);
@@ -576,15 +594,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
             __syncwarp();
         }
-
-        // ---- QK^T: logits of 128 tokens x (group | aux) columns
-        float acc[8][4];
         float aux[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
         // aux lanes (B columns 4-7) read their "scale" from a ones buffer
         const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
-        const uint32_t onesA = row0 ? kOnes : 0u;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             const int c0 = 16 * ks + 2 * tig;
@@ -600,37 +614,36 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
             mma16816(aux, onesA, z0, onesA, z1, b0, b1);
         }
+        if (NKH > 0) {
+            const int col = gid & 3;
+            const uint16_t* qg = q_row(cur_unit, col < GROUP ? col : 0);
 #pragma unroll
-        for (int hk = 0; hk < NKH; ++hk) {
-            const int j0 = 16 * hk + 2 * tig;
-            const int jj[4] = {j0, j0 + 1, j0 + 8, j0 + 9};
-            uint32_t hv[4];
+            for (int hk = 0; hk < NKH; ++hk) {
+                const int j0 = 16 * hk + 2 * tig;
+                const int jj[4] = {j0, j0 + 1, j0 + 8, j0 + 9};
+                float hv[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int ch = sm.inv[jj[i]];
-                const float q4 = half_bits_to_f32(sm.qa4[gid & 3][ch]);
-                const float sc = half_bits_to_f32(ld_u16(kp + scale_off + 2 * ch));
-                hv[i] = (main_col && jj[i] < d_boost) ? __float_as_uint(q4 * sc) : 0u;
+                for (int i = 0; i < 4; ++i) {
+                    const int ch = sm.inv[jj[i]];
+                    const float q4 = 4.f * kAlpha * bf16_to_f32(__ldg(reinterpret_cast<const unsigned short*>(qg) + ch));
+                    const float sc = half_bits_to_f32(ld_u16(kp + scale_off + 2 * ch));
+                    hv[i] = (main_col && col < GROUP && jj[i] < d_boost) ? q4 * sc : 0.f;
+                }
+                const uint32_t b0 = pack_f16x2(hv[0], hv[1]);
+                const uint32_t b1 = pack_f16x2(hv[2], hv[3]);
+                const uint32_t* hw = reinterpret_cast<const uint32_t*>(kp + D * G / 4);
+                mma_codes(kc, acc, hw[8 * j0 + gid], hw[8 * (j0 + 1) + gid], hw[8 * (j0 + 8) + gid],
+                          hw[8 * (j0 + 9) + gid], b0, b1);
+                mma16816(aux, onesA, 0u, onesA, 0u, b0, b1);
             }
-            const uint32_t b0 = pack_f16x2(__uint_as_float(hv[0]), __uint_as_float(hv[1]));
-            const uint32_t b1 = pack_f16x2(__uint_as_float(hv[2]), __uint_as_float(hv[3]));
-            const uint32_t* hw = reinterpret_cast<const uint32_t*>(kp + D * G / 4);
-            mma_codes(kc, acc, hw[8 * j0 + gid], hw[8 * (j0 + 1) + gid], hw[8 * (j0 + 8) + gid], hw[8 * (j0 + 9) + gid],
-                      b0, b1);
-            mma16816(aux, onesA, 0u, onesA, 0u, b0, b1);
         }
         // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha)
-        float sumB[2], cst[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            sumB[j] = __shfl_sync(0xffffffffu, aux[j], tig & 1);
-            cst[j] = __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
-        }
-        float b16[2], b64[2], mnew[2], corr[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            b16[j] = cst[j] - 64.f * sumB[j];
-            b64[j] = cst[j] - 16.f * sumB[j];
+            const float sumB = __shfl_sync(0xffffffffu, aux[j], tig & 1);
+            const float cst = __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
+            b16[j] = cst - 64.f * sumB;
+            b64[j] = cst - 16.f * sumB;
             float x16 = acc[0][j], x64 = acc[0][2 + j];
 #pragma unroll
             for (int m = 1; m < 8; ++m) {
@@ -646,27 +659,37 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             b16[j] -= mnew[j];
             b64[j] -= mnew[j];
         }
-        // P^T -> shared (rows 0-3: p * s_token, rows 4-7: p), tokens 16 gid + 2m (+1)
+        // probabilities in place (log2 domain)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                acc[m][j] = ex2(fmaf(acc[m][j], 1.f / 16.f, b16[j]));
+                acc[m][2 + j] = ex2(fmaf(acc[m][2 + j], 1.f / 64.f, b64[j]));
+            }
+        }
+    };
+
+    auto pv_page = [&]() {
+        const uint8_t* vp = sm.vbuf;
+        const uint32_t* vw = reinterpret_cast<const uint32_t*>(vp);
         const uint8_t* vscale = vp + G * D / 4;
+        // P^T -> shared (rows 0-3: p * s_token, rows 4-7: p), tokens 16 gid + 2m (+1)
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             const int tok = 16 * gid + 2 * m;
             const uint32_t sv = lds32(vscale + 2 * tok);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const float p0 = ex2(fmaf(acc[m][j], 1.f / 16.f, b16[j]));
-                const float p1 = ex2(fmaf(acc[m][2 + j], 1.f / 64.f, b64[j]));
-                const uint32_t pu = pack_f16x2(p0, p1);
+                const uint32_t pu = pack_f16x2(acc[m][j], acc[m][2 + j]);
                 if (tig < 2) {
                     const int g = 2 * tig + j;
-                    sm.pt[g][tok / 2] = hmul2(pu, sv);
-                    sm.pt[4 + g][tok / 2] = pu;
+                    sm.u.pt[g][tok / 2] = hmul2(pu, sv);
+                    sm.u.pt[4 + g][tok / 2] = pu;
                 }
             }
         }
         __syncwarp();
-
-        // ---- P V: 128 channels x (group | aux) columns over the page's tokens
         float pacc[8][4];
         float vaux[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -675,8 +698,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             const int t0 = 16 * ks + 2 * tig;
-            const uint32_t b0 = sm.pt[gid][t0 / 2];
-            const uint32_t b1 = sm.pt[gid][t0 / 2 + 4];
+            const uint32_t b0 = sm.u.pt[gid][t0 / 2];
+            const uint32_t b1 = sm.u.pt[gid][t0 / 2 + 4];
             const uint32_t w0 = vw[8 * t0 + gid], w1 = vw[8 * (t0 + 1) + gid];
             const uint32_t w2 = vw[8 * (t0 + 8) + gid], w3 = vw[8 * (t0 + 9) + gid];
             mma_codes(kc, pacc, w0, w1, w2, w3, b0, b1);
@@ -690,8 +713,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z).
         // Row constants (zero points, the 1024 offset) accumulate per column in
         // ob16 / ob64 and are added at the flush; the accumulators are only
-        // rescaled when a running max moved (warp vote).
-        const bool rescale = __any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f);
+        // rescaled when a running max of a real column moved (warp vote).
+        const bool real0 = tig < 2 && 2 * tig < GROUP, real1 = tig < 2 && 2 * tig + 1 < GROUP;
+        const bool rescale = __any_sync(0xffffffffu, (real0 && corr[0] != 1.f) || (real1 && corr[1] != 1.f));
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const float sBv = __shfl_sync(0xffffffffu, vaux[j], tig & 1);
@@ -714,31 +738,32 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
             om[j] = mnew[j];
         }
-        __syncwarp();
     };
 
-    // ---- work loop: one page pair (or one fp item) per iteration, single call
-    // sites so the hot body is emitted once --------------------------------------
+    // ---- work loop -------------------------------------------------------------------
     int kind, u, p0, p1;
     next_item(kind, u, p0, p1);
     int nkind = 0, nu = 0, np0 = 0, np1 = 0;
     if (kind != 0) next_item(nkind, nu, np0, np1);
-    bool first_issued = false;
+    bool k_pending = false, v_pending = false;  // loads of the current item's first page issued
     int p = p0;
 #pragma unroll 1
     while (kind != 0) {
         bool item_done;
         if (kind == 1) {
-            if (nkind == 2 && !first_issued) {
-                issue(nu, np0);
-                first_issued = true;
-            }
-            process_fp(u, p0);
+            process_fp(u, p0, [&]() {
+                if (nkind == 2) {
+                    issue_k(nu, np0);
+                    issue_v(nu, np0);
+                    k_pending = v_pending = true;
+                }
+            });
             item_done = true;
         } else {
             if (p == p0) {
-                if (!first_issued) issue(u, p0);
-                first_issued = false;
+                if (!k_pending) issue_k(u, p0);
+                if (!v_pending) issue_v(u, p0);
+                k_pending = v_pending = false;
                 load_unit(u);
                 om[0] = om[1] = -INFINITY;
                 ol[0] = ol[1] = 0.f;
@@ -746,22 +771,24 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
                 for (int m = 0; m < 8; ++m) oacc[m][0] = oacc[m][1] = oacc[m][2] = oacc[m][3] = 0.f;
             }
-            // keep one page pair in flight behind the one being computed
             const bool more = p + 1 < p1;
+            const bool chain = !more && nkind == 2;  // next item's first page follows
             const int iu = more ? u : nu;
             const int ip = more ? p + 1 : np0;
-            if (more || nkind == 2) {
-                issue(iu, ip);
-                if (!more) first_issued = true;
-            }
-            const int s = consumed & 1;
-            mbar_wait(&sm.mbar[s], (consumed >> 1) & 1);
-            page_pair(s);
-            ++consumed;
+            mbar_wait(&sm.mbar[0], kph);
+            kph ^= 1u;
+            qk_page();
+            __syncwarp();
+            if (more || chain) issue_k(iu, ip);  // key slot free
+            mbar_wait(&sm.mbar[1], vph);
+            vph ^= 1u;
+            pv_page();
+            __syncwarp();
+            if (more || chain) issue_v(iu, ip);  // value slot free
+            if (chain) k_pending = v_pending = true;
             ++p;
             item_done = p == p1;
             if (item_done) {
-                // partial of this chunk: slot 1 + chunk
                 const int slot = P.fmax + p0 / P.ppc;
                 float* base = P.part + ((int64_t)u * (P.fmax + P.cmax) + slot) * GROUP * (D + 2);
                 if (tig < 2) {
