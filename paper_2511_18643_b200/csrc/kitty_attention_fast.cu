@@ -68,6 +68,7 @@ struct Params {
     int ppc;    // page pairs per quantized item
     int cmax;   // quantized items per unit (grid bound)
     int fmax;   // fp-token chunk items per unit (grid bound)
+    int tail;   // last pages of a unit scheduled as single-page items (end of the queue)
     int units;
     int* ctr;   // [0] next item, [1] finished warps, [2 + u] arrivals of unit u
     float* part;
@@ -250,35 +251,45 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         return __shfl_sync(0xffffffffu, i, 0);
     };
     // item -> (kind, unit, a, b); kind 0 = end, 1 = fp chunk a, 2 = pages [a, b), 3 = empty.
-    // fp chunks and page chunks are interleaved so the latency-bound fp work
-    // of some warps overlaps the tensor-core work of the others.
-    const int nf = P.units * P.fmax, nq = P.units * P.cmax;
+    // Queue order: fp chunks interleaved with big page chunks (ppc pages), so the
+    // latency-bound fp work of some warps overlaps the tensor-core work of the
+    // others; then the last `tail` pages of every unit as single-page items, so
+    // the queue drains in small pieces and no SM idles behind a long item.
+    const int nf = P.units * P.fmax, nq = P.units * P.cmax, nt = P.units * P.tail;
     const int n2 = 2 * min(nf, nq);
     auto decode = [&](int it, int& kind, int& u, int& p0, int& p1) {
-        if (it >= nf + nq) {
+        if (it >= nf + nq + nt) {
             kind = 0;
             return;
         }
-        bool fp;
-        int idx;
+        int sect, idx;  // 0 fp, 1 big page chunk, 2 tail page
         if (it < n2) {
-            fp = (it & 1) == 0;
+            sect = (it & 1) ? 1 : 0;
             idx = it >> 1;
-        } else {
-            fp = nf > nq;
+        } else if (it < nf + nq) {
+            sect = nf > nq ? 0 : 1;
             idx = it - n2 + min(nf, nq);
+        } else {
+            sect = 2;
+            idx = it - nf - nq;
         }
         const int ch = idx / P.units;
         u = idx - ch * P.units;
         const UnitGeom gm = unit_geom(c, u);
-        if (fp) {
+        const int tl = min(gm.vp, P.tail);
+        const int big = gm.vp - tl;
+        if (sect == 0) {
             p0 = ch;
             p1 = 0;
             kind = (gm.n > 0 && ch * kFpChunk < gm.nfp) ? 1 : 3;
-        } else {
+        } else if (sect == 1) {
             p0 = ch * P.ppc;
-            p1 = min(gm.vp, p0 + P.ppc);
+            p1 = min(big, p0 + P.ppc);
             kind = (p0 < p1 && gm.n > 0) ? 2 : 3;
+        } else {
+            p0 = big + ch;
+            p1 = p0 + 1;
+            kind = (ch < tl && gm.n > 0) ? 2 : 3;
         }
     };
     auto next_item = [&](int& kind, int& u, int& p0, int& p1) {
@@ -337,14 +348,18 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         old = __shfl_sync(0xffffffffu, old, 0);
         const UnitGeom gm = unit_geom(c, u);
         const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
-        const int nqc = (gm.vp + P.ppc - 1) / P.ppc;
-        const int nparts = nfc + nqc;
+        const int tl = min(gm.vp, P.tail);
+        const int nbc = (gm.vp - tl + P.ppc - 1) / P.ppc;
+        const int nparts = nfc + nbc + tl;
         if (old != nparts - 1) return;
         __threadfence();
         const int b = u / hkv, h = u - b * hkv;
         constexpr int kStride = GROUP * (D + 2);
-        const float* pb = P.part + (int64_t)u * (P.fmax + P.cmax) * kStride;
-        auto part_ptr = [&](int i) { return pb + (int64_t)(i < nfc ? i : P.fmax + (i - nfc)) * kStride; };
+        const float* pb = P.part + (int64_t)u * (P.fmax + P.cmax + P.tail) * kStride;
+        auto part_ptr = [&](int i) {
+            const int slot = i < nfc ? i : (i < nfc + nbc ? P.fmax + (i - nfc) : P.fmax + P.cmax + (i - nfc - nbc));
+            return pb + (int64_t)slot * kStride;
+        };
         float M[GROUP], L[GROUP];
 #pragma unroll
         for (int g = 0; g < GROUP; ++g) {
@@ -565,7 +580,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
         }
         __syncwarp();
-        float* base = P.part + ((int64_t)u * (P.fmax + P.cmax) + fc) * GROUP * (D + 2);
+        float* base = P.part + ((int64_t)u * (P.fmax + P.cmax + P.tail) + fc) * GROUP * (D + 2);
 #pragma unroll
         for (int g = 0; g < GROUP; ++g) {
             reinterpret_cast<float4*>(base + g * D)[lane] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
@@ -789,8 +804,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             ++p;
             item_done = p == p1;
             if (item_done) {
-                const int slot = P.fmax + p0 / P.ppc;
-                float* base = P.part + ((int64_t)u * (P.fmax + P.cmax) + slot) * GROUP * (D + 2);
+                const UnitGeom gm = unit_geom(c, u);
+                const int big = gm.vp - min(gm.vp, P.tail);
+                const int slot = p0 < big ? P.fmax + p0 / P.ppc : P.fmax + P.cmax + (p0 - big);
+                float* base = P.part + ((int64_t)u * (P.fmax + P.cmax + P.tail) + slot) * GROUP * (D + 2);
                 if (tig < 2) {
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
@@ -855,7 +872,7 @@ bool fast_attention_supported(const KittyCacheDesc& c) {
 }
 
 struct FastPlan {
-    int ppc, cmax, fmax, units, group;
+    int ppc, cmax, fmax, tail, units, group;
     size_t ctr_bytes, part_bytes;
 };
 
@@ -870,12 +887,13 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     int ppc = static_cast<int>(pages / (2 * warps));
     ppc = ppc < 1 ? 1 : (ppc > 8 ? 8 : ppc);
     p.ppc = ppc;
+    p.tail = ppc > 1 ? 4 : 0;
     p.cmax = (maxp + ppc - 1) / ppc;
     const int nfp_max = min(max_tokens, c.cfg.s + c.cfg.r + c.cfg.g - 1);
     p.fmax = (nfp_max + kFpChunk - 1) / kFpChunk;
     if (p.fmax < 1) p.fmax = 1;
     p.ctr_bytes = (((size_t)(2 + p.units) * sizeof(int)) + 255) & ~size_t(255);
-    p.part_bytes = (size_t)p.units * (p.fmax + p.cmax) * p.group * (D + 2) * sizeof(float);
+    p.part_bytes = (size_t)p.units * (p.fmax + p.cmax + p.tail) * p.group * (D + 2) * sizeof(float);
     return p;
 }
 
@@ -914,10 +932,11 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     prm.ppc = p.ppc;
     prm.cmax = p.cmax;
     prm.fmax = p.fmax;
+    prm.tail = p.tail;
     prm.units = p.units;
     prm.ctr = static_cast<int*>(ws);
     prm.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ctr_bytes);
-    const long long items = (long long)p.units * (p.fmax + p.cmax);
+    const long long items = (long long)p.units * (p.fmax + p.cmax + p.tail);
     long long ctas = (items + kWarps - 1) / kWarps;
     const long long cap = (long long)num_sms() * kCtasPerSm;
     const int grid = static_cast<int>(ctas < cap ? ctas : cap);
