@@ -68,7 +68,9 @@ struct Params {
     int ppc;    // page pairs per quantized item
     int cmax;   // quantized items per unit (grid bound)
     int fmax;   // fp-token chunk items per unit (grid bound)
-    int tail;   // last pages of a unit scheduled as single-page items (end of the queue)
+    int cs[3];    // page-chunk size of schedule level 0 / 1 / 2
+    int cmx[3];   // chunks per unit bound of each level
+    int nslot;    // partial slots per unit: fmax + cmx[0] + cmx[1] + cmx[2]
     int units;
     int* ctr;   // [0] next item, [1] finished warps, [2 + u] arrivals of unit u
     float* part;
@@ -199,6 +201,14 @@ struct UnitGeom {
     int n, kp, vp, nfp;
 };
 
+// Pages of a unit are scheduled in three levels of decreasing chunk size:
+// [0, vp/2) in chunks of cs[0], [vp/2, 4vp/5) in cs[1], [4vp/5, vp) in 1-page
+// chunks; the queue serves level 0 (interleaved with the fp chunks) first, so
+// it drains in small pieces and no SM idles behind a long item.
+__host__ __device__ __forceinline__ int level_begin(int lv, int vp) {
+    return lv == 0 ? 0 : (lv == 1 ? vp / 2 : (lv == 2 ? (vp * 4) / 5 : vp));
+}
+
 __device__ __forceinline__ UnitGeom unit_geom(const KittyCacheDesc& c, int u) {
     UnitGeom g;
     g.n = c.unit_len[u];
@@ -251,46 +261,53 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         return __shfl_sync(0xffffffffu, i, 0);
     };
     // item -> (kind, unit, a, b); kind 0 = end, 1 = fp chunk a, 2 = pages [a, b), 3 = empty.
-    // Queue order: fp chunks interleaved with big page chunks (ppc pages), so the
-    // latency-bound fp work of some warps overlaps the tensor-core work of the
-    // others; then the last `tail` pages of every unit as single-page items, so
-    // the queue drains in small pieces and no SM idles behind a long item.
-    const int nf = P.units * P.fmax, nq = P.units * P.cmax, nt = P.units * P.tail;
-    const int n2 = 2 * min(nf, nq);
+    // Queue: fp chunks interleaved with level-0 page chunks (latency-bound fp
+    // work overlaps tensor-core work), then level-1 chunks, then level-2.
+    const int nf = P.units * P.fmax, nq0 = P.units * P.cmx[0];
+    const int nq1 = P.units * P.cmx[1], nq2 = P.units * P.cmx[2];
+    const int n2 = 2 * min(nf, nq0);
     auto decode = [&](int it, int& kind, int& u, int& p0, int& p1) {
-        if (it >= nf + nq + nt) {
+        int sect, idx;  // -1 fp, 0..2 page level
+        if (it < n2) {
+            sect = (it & 1) ? 0 : -1;
+            idx = it >> 1;
+        } else if (it < nf + nq0) {
+            sect = nf > nq0 ? -1 : 0;
+            idx = it - n2 + min(nf, nq0);
+        } else if (it < nf + nq0 + nq1) {
+            sect = 1;
+            idx = it - nf - nq0;
+        } else if (it < nf + nq0 + nq1 + nq2) {
+            sect = 2;
+            idx = it - nf - nq0 - nq1;
+        } else {
             kind = 0;
             return;
-        }
-        int sect, idx;  // 0 fp, 1 big page chunk, 2 tail page
-        if (it < n2) {
-            sect = (it & 1) ? 1 : 0;
-            idx = it >> 1;
-        } else if (it < nf + nq) {
-            sect = nf > nq ? 0 : 1;
-            idx = it - n2 + min(nf, nq);
-        } else {
-            sect = 2;
-            idx = it - nf - nq;
         }
         const int ch = idx / P.units;
         u = idx - ch * P.units;
         const UnitGeom gm = unit_geom(c, u);
-        const int tl = min(gm.vp, P.tail);
-        const int big = gm.vp - tl;
-        if (sect == 0) {
+        if (sect < 0) {
             p0 = ch;
             p1 = 0;
             kind = (gm.n > 0 && ch * kFpChunk < gm.nfp) ? 1 : 3;
-        } else if (sect == 1) {
-            p0 = ch * P.ppc;
-            p1 = min(big, p0 + P.ppc);
-            kind = (p0 < p1 && gm.n > 0) ? 2 : 3;
         } else {
-            p0 = big + ch;
-            p1 = p0 + 1;
-            kind = (ch < tl && gm.n > 0) ? 2 : 3;
+            const int lb = level_begin(sect, gm.vp), le = level_begin(sect + 1, gm.vp);
+            p0 = lb + ch * P.cs[sect];
+            p1 = min(le, p0 + P.cs[sect]);
+            kind = (p0 < p1 && gm.n > 0) ? 2 : 3;
         }
+    };
+    // partial slot of the page chunk starting at p0, and the chunk count of a unit
+    auto page_slot = [&](int p0_, int vp) {
+        const int lv = p0_ < level_begin(1, vp) ? 0 : (p0_ < level_begin(2, vp) ? 1 : 2);
+        int slot = P.fmax + (p0_ - level_begin(lv, vp)) / P.cs[lv];
+        for (int l = 0; l < lv; ++l) slot += P.cmx[l];
+        return slot;
+    };
+    auto page_chunks = [&](int lv, int vp) {
+        const int n = level_begin(lv + 1, vp) - level_begin(lv, vp);
+        return (n + P.cs[lv] - 1) / P.cs[lv];
     };
     auto next_item = [&](int& kind, int& u, int& p0, int& p1) {
         for (;;) {
@@ -348,16 +365,19 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         old = __shfl_sync(0xffffffffu, old, 0);
         const UnitGeom gm = unit_geom(c, u);
         const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
-        const int tl = min(gm.vp, P.tail);
-        const int nbc = (gm.vp - tl + P.ppc - 1) / P.ppc;
-        const int nparts = nfc + nbc + tl;
+        const int n0 = page_chunks(0, gm.vp), n1 = page_chunks(1, gm.vp), n2c = page_chunks(2, gm.vp);
+        const int nparts = nfc + n0 + n1 + n2c;
         if (old != nparts - 1) return;
         __threadfence();
         const int b = u / hkv, h = u - b * hkv;
         constexpr int kStride = GROUP * (D + 2);
-        const float* pb = P.part + (int64_t)u * (P.fmax + P.cmax + P.tail) * kStride;
+        const float* pb = P.part + (int64_t)u * P.nslot * kStride;
         auto part_ptr = [&](int i) {
-            const int slot = i < nfc ? i : (i < nfc + nbc ? P.fmax + (i - nfc) : P.fmax + P.cmax + (i - nfc - nbc));
+            int slot;
+            if (i < nfc) slot = i;
+            else if (i < nfc + n0) slot = P.fmax + (i - nfc);
+            else if (i < nfc + n0 + n1) slot = P.fmax + P.cmx[0] + (i - nfc - n0);
+            else slot = P.fmax + P.cmx[0] + P.cmx[1] + (i - nfc - n0 - n1);
             return pb + (int64_t)slot * kStride;
         };
         float M[GROUP], L[GROUP];
@@ -580,7 +600,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
         }
         __syncwarp();
-        float* base = P.part + ((int64_t)u * (P.fmax + P.cmax + P.tail) + fc) * GROUP * (D + 2);
+        float* base = P.part + ((int64_t)u * P.nslot + fc) * GROUP * (D + 2);
 #pragma unroll
         for (int g = 0; g < GROUP; ++g) {
             reinterpret_cast<float4*>(base + g * D)[lane] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
@@ -804,10 +824,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             ++p;
             item_done = p == p1;
             if (item_done) {
-                const UnitGeom gm = unit_geom(c, u);
-                const int big = gm.vp - min(gm.vp, P.tail);
-                const int slot = p0 < big ? P.fmax + p0 / P.ppc : P.fmax + P.cmax + (p0 - big);
-                float* base = P.part + ((int64_t)u * (P.fmax + P.cmax + P.tail) + slot) * GROUP * (D + 2);
+                const int slot = page_slot(p0, unit_geom(c, u).vp);
+                float* base = P.part + ((int64_t)u * P.nslot + slot) * GROUP * (D + 2);
                 if (tig < 2) {
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
@@ -872,7 +890,7 @@ bool fast_attention_supported(const KittyCacheDesc& c) {
 }
 
 struct FastPlan {
-    int ppc, cmax, fmax, tail, units, group;
+    int ppc, cmax, fmax, units, group, cs[3], cmx[3], nslot;
     size_t ctr_bytes, part_bytes;
 };
 
@@ -887,13 +905,20 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     int ppc = static_cast<int>(pages / (2 * warps));
     ppc = ppc < 1 ? 1 : (ppc > 8 ? 8 : ppc);
     p.ppc = ppc;
-    p.tail = ppc > 1 ? 4 : 0;
     p.cmax = (maxp + ppc - 1) / ppc;
+    p.cs[0] = ppc;
+    p.cs[1] = ppc / 4 > 1 ? ppc / 4 : 1;
+    p.cs[2] = 1;
+    for (int lv = 0; lv < 3; ++lv) {
+        const int n = level_begin(lv + 1, maxp) - level_begin(lv, maxp) + 2;
+        p.cmx[lv] = (n + p.cs[lv] - 1) / p.cs[lv];
+    }
     const int nfp_max = min(max_tokens, c.cfg.s + c.cfg.r + c.cfg.g - 1);
     p.fmax = (nfp_max + kFpChunk - 1) / kFpChunk;
     if (p.fmax < 1) p.fmax = 1;
     p.ctr_bytes = (((size_t)(2 + p.units) * sizeof(int)) + 255) & ~size_t(255);
-    p.part_bytes = (size_t)p.units * (p.fmax + p.cmax + p.tail) * p.group * (D + 2) * sizeof(float);
+    p.nslot = p.fmax + p.cmx[0] + p.cmx[1] + p.cmx[2];
+    p.part_bytes = (size_t)p.units * p.nslot * p.group * (D + 2) * sizeof(float);
     return p;
 }
 
@@ -932,11 +957,15 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     prm.ppc = p.ppc;
     prm.cmax = p.cmax;
     prm.fmax = p.fmax;
-    prm.tail = p.tail;
+    for (int lv = 0; lv < 3; ++lv) {
+        prm.cs[lv] = p.cs[lv];
+        prm.cmx[lv] = p.cmx[lv];
+    }
+    prm.nslot = p.nslot;
     prm.units = p.units;
     prm.ctr = static_cast<int*>(ws);
     prm.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ctr_bytes);
-    const long long items = (long long)p.units * (p.fmax + p.cmax + p.tail);
+    const long long items = (long long)p.units * p.nslot;
     long long ctas = (items + kWarps - 1) / kWarps;
     const long long cap = (long long)num_sms() * kCtasPerSm;
     const int grid = static_cast<int>(ctas < cap ? ctas : cap);
