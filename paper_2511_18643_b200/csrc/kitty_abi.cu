@@ -3,6 +3,7 @@
 // launches on the caller's stream and returns a KittyStatus.
 #include <cstdio>
 
+#include "kitty_attention.cuh"
 #include "kitty_codec.cuh"
 
 namespace {
@@ -184,6 +185,13 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv, 
     return cuda_status(kitty::launch_dense_attention(keys, values, h_kv, length, d, queries, n_q,
                                                      kv_head_map, out, workspace, workspace_bytes,
                                                      as_stream(stream)));
+}
+
+// Debug only (not part of include/kitty_b200.h): per-warp trace of the fused
+// attention kernel: {smid, t_start, t_end, fp items, pages, fp ns, merge ns,
+// wait ns, warp, 0} per warp, 10 int64 each.
+int kitty_debug_attention_trace(int enable, long long* host_out, int max_warps) {
+    return cuda_status(kitty::fast_attention_trace(enable, host_out, max_warps));
 }
 
 }  // extern "C"

@@ -76,6 +76,18 @@ struct Params {
     float* part;
 };
 
+// ---- optional per-warp trace (kitty_attention_trace): where does the time go ----
+constexpr int kTraceWarps = 16384;
+constexpr int kTraceFields = 10;
+__device__ long long g_trace[kTraceWarps * kTraceFields];
+__device__ int g_trace_on;
+
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---- small PTX helpers --------------------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -251,6 +263,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     __syncwarp();
     const Consts kc;
     const uint32_t onesA = row0 ? kOnes : 0u;
+    const bool trace = g_trace_on != 0;
+    long long tr_t0 = trace ? gtimer() : 0, tr_fp = 0, tr_merge = 0, tr_wait = 0;
+    int tr_nfp = 0, tr_npages = 0, tr_nmerge = 0;
 
     uint32_t kph = 0, vph = 0;  // mbarrier parities of the two slots
 
@@ -786,6 +801,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     while (kind != 0) {
         bool item_done;
         if (kind == 1) {
+            const long long tf0 = trace ? gtimer() : 0;
+            ++tr_nfp;
             process_fp(u, p0, [&]() {
                 if (nkind == 2) {
                     issue_k(nu, np0);
@@ -793,6 +810,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                     k_pending = v_pending = true;
                 }
             });
+            if (trace) tr_fp += gtimer() - tf0;
             item_done = true;
         } else {
             if (p == p0) {
@@ -810,8 +828,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const bool chain = !more && nkind == 2;  // next item's first page follows
             const int iu = more ? u : nu;
             const int ip = more ? p + 1 : np0;
+            const long long tw0 = trace ? gtimer() : 0;
             mbar_wait(&sm.mbar[0], kph);
             kph ^= 1u;
+            if (trace) tr_wait += gtimer() - tw0;
+            ++tr_npages;
             qk_page();
             __syncwarp();
             if (more || chain) issue_k(iu, ip);  // key slot free
@@ -845,13 +866,33 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
         }
         if (item_done) {
+            const long long tm0 = trace ? gtimer() : 0;
             finish_unit(u);
+            if (trace) tr_merge += gtimer() - tm0;
             kind = nkind;
             u = nu;
             p0 = np0;
             p1 = np1;
             p = p0;
             if (kind != 0) next_item(nkind, nu, np0, np1);
+        }
+    }
+    if (trace && lane == 0) {
+        const int wid = blockIdx.x * kWarps + warp;
+        if (wid < kTraceWarps) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            long long* r = g_trace + (int64_t)wid * kTraceFields;
+            r[0] = smid;
+            r[1] = tr_t0;
+            r[2] = gtimer();
+            r[3] = tr_nfp;
+            r[4] = tr_npages;
+            r[5] = tr_fp;
+            r[6] = tr_merge;
+            r[7] = tr_wait;
+            r[8] = warp;
+            r[9] = 0;
         }
     }
     // the last warp out resets the work queue for the next launch
@@ -975,6 +1016,13 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
         case 2: return launch_g<2>(prm, nkh, grid, st);
         default: return launch_g<4>(prm, nkh, grid, st);
     }
+}
+
+cudaError_t fast_attention_trace(int enable, long long* host_out, int max_warps) {
+    cudaError_t e = cudaMemcpyToSymbol(fastattn::g_trace_on, &enable, sizeof(int));
+    if (e != cudaSuccess || host_out == nullptr) return e;
+    const int n = max_warps < fastattn::kTraceWarps ? max_warps : fastattn::kTraceWarps;
+    return cudaMemcpyFromSymbol(host_out, fastattn::g_trace, sizeof(long long) * n * fastattn::kTraceFields);
 }
 
 }  // namespace kitty
