@@ -72,7 +72,7 @@ struct Params {
     int cmx[3];   // chunks per unit bound of each level
     int nslot;    // partial slots per unit: fmax + cmx[0] + cmx[1] + cmx[2]
     int units;
-    int* ctr;   // [0] next item, [1] finished warps, [2 + u] arrivals of unit u
+    int* ctr;   // [0] next item, [1] finished warps
     float* part;
 };
 
@@ -368,107 +368,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 qa[ks][hh] = pack_f16x2(__uint_as_float(w << 16) * kAlpha, __uint_as_float(w & 0xffff0000u) * kAlpha);
             }
         }
-    };
-
-    // merge the partials of unit u (run by the warp that completed its last
-    // item): log-sum-exp over the fp chunks and the page chunks, loads batched
-    // across lanes / partials so the merge is not latency-serialised.
-    auto finish_unit = [&](int u) {
-        __threadfence();
-        int old = 0;
-        if (lane == 0) old = atomicAdd(&P.ctr[2 + u], 1);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        const UnitGeom gm = unit_geom(c, u);
-        const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
-        const int n0 = page_chunks(0, gm.vp), n1 = page_chunks(1, gm.vp), n2c = page_chunks(2, gm.vp);
-        const int nparts = nfc + n0 + n1 + n2c;
-        if (old != nparts - 1) return;
-        __threadfence();
-        const int b = u / hkv, h = u - b * hkv;
-        constexpr int kStride = GROUP * (D + 2);
-        const float* pb = P.part + (int64_t)u * P.nslot * kStride;
-        auto part_ptr = [&](int i) {
-            int slot;
-            if (i < nfc) slot = i;
-            else if (i < nfc + n0) slot = P.fmax + (i - nfc);
-            else if (i < nfc + n0 + n1) slot = P.fmax + P.cmx[0] + (i - nfc - n0);
-            else slot = P.fmax + P.cmx[0] + P.cmx[1] + (i - nfc - n0 - n1);
-            return pb + (int64_t)slot * kStride;
-        };
-        float M[GROUP], L[GROUP];
-#pragma unroll
-        for (int g = 0; g < GROUP; ++g) {
-            M[g] = -INFINITY;
-            L[g] = 0.f;
-        }
-        for (int i = lane; i < nparts; i += 32) {
-            const float* ml = part_ptr(i) + GROUP * D;
-#pragma unroll
-            for (int g = 0; g < GROUP; ++g) M[g] = fmaxf(M[g], __ldcg(ml + 2 * g));
-        }
-#pragma unroll
-        for (int g = 0; g < GROUP; ++g) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
-        }
-        float o4[GROUP][4];
-#pragma unroll
-        for (int g = 0; g < GROUP; ++g) o4[g][0] = o4[g][1] = o4[g][2] = o4[g][3] = 0.f;
-        for (int i0 = 0; i0 < nparts; i0 += 32) {
-            float wl[GROUP];
-            const int mine = i0 + lane;
-            if (mine < nparts) {
-                const float* ml = part_ptr(mine) + GROUP * D;
-#pragma unroll
-                for (int g = 0; g < GROUP; ++g) {
-                    const float mi = __ldcg(ml + 2 * g);
-                    wl[g] = mi == -INFINITY ? 0.f : ex2(mi - M[g]);
-                    L[g] += wl[g] * __ldcg(ml + 2 * g + 1);
-                }
-            } else {
-#pragma unroll
-                for (int g = 0; g < GROUP; ++g) wl[g] = 0.f;
-            }
-            const int cnt = min(32, nparts - i0);
-            for (int j = 0; j < cnt; j += 2) {
-                float4 a[2][GROUP];
-#pragma unroll
-                for (int jj = 0; jj < 2; ++jj) {
-                    const float* pi = part_ptr(i0 + min(j + jj, cnt - 1));
-#pragma unroll
-                    for (int g = 0; g < GROUP; ++g) a[jj][g] = __ldcg(reinterpret_cast<const float4*>(pi + g * D) + lane);
-                }
-#pragma unroll
-                for (int jj = 0; jj < 2; ++jj) {
-#pragma unroll
-                    for (int g = 0; g < GROUP; ++g) {
-                        float w = __shfl_sync(0xffffffffu, wl[g], (j + jj) & 31);
-                        w = (j + jj < cnt) ? w : 0.f;
-                        o4[g][0] = fmaf(w, a[jj][g].x, o4[g][0]);
-                        o4[g][1] = fmaf(w, a[jj][g].y, o4[g][1]);
-                        o4[g][2] = fmaf(w, a[jj][g].z, o4[g][2]);
-                        o4[g][3] = fmaf(w, a[jj][g].w, o4[g][3]);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < GROUP; ++g) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) L[g] += __shfl_xor_sync(0xffffffffu, L[g], o);
-            const float inv = 1.f / L[g];
-            const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
-            if (P.out_dtype == KITTY_F32) {
-                reinterpret_cast<float4*>(static_cast<float*>(P.out) + row * D)[lane] =
-                    make_float4(o4[g][0] * inv, o4[g][1] * inv, o4[g][2] * inv, o4[g][3] * inv);
-            } else {
-                uint2 v;
-                v.x = f32_to_bf16_bits(o4[g][0] * inv) | (f32_to_bf16_bits(o4[g][1] * inv) << 16);
-                v.y = f32_to_bf16_bits(o4[g][2] * inv) | (f32_to_bf16_bits(o4[g][3] * inv) << 16);
-                reinterpret_cast<uint2*>(static_cast<uint16_t*>(P.out) + row * D)[lane] = v;
-            }
-        }
-        if (lane == 0) P.ctr[2 + u] = 0;  // reset for the next launch
     };
 
     // ---- one chunk of <= 32 full-precision tokens of a unit: the sink and the
@@ -866,9 +765,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
         }
         if (item_done) {
-            const long long tm0 = trace ? gtimer() : 0;
-            finish_unit(u);
-            if (trace) tr_merge += gtimer() - tm0;
             kind = nkind;
             u = nu;
             p0 = np0;
@@ -904,6 +800,102 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             P.ctr[1] = 0;
         }
     }
+}
+
+// K5: log-sum-exp merge of a unit's partials (fp chunks + page chunks).  One
+// CTA per unit, 4 warps per query row, each warp over a quarter of the parts;
+// loads are independent so the merge is one or two L2 round trips deep.
+template <int GROUP>
+__global__ void __launch_bounds__(GROUP * 128) combine_parts_kernel(Params P) {
+    constexpr int kSub = 4;  // warps per query row
+    __shared__ float sm_m[GROUP][kSub], sm_l[GROUP][kSub];
+    __shared__ float4 sm_acc[GROUP][kSub][32];
+    const int u = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = warp / kSub, sub = warp % kSub;
+    const KittyCacheDesc& c = P.c;
+    const UnitGeom gm = unit_geom(c, u);
+    if (gm.n == 0) return;
+    const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
+    int nch[3];
+    for (int lv = 0; lv < 3; ++lv) {
+        const int n = level_begin(lv + 1, gm.vp) - level_begin(lv, gm.vp);
+        nch[lv] = (n + P.cs[lv] - 1) / P.cs[lv];
+    }
+    const int nparts = nfc + nch[0] + nch[1] + nch[2];
+    constexpr int kStride = GROUP * (D + 2);
+    const float* pb = P.part + (int64_t)u * P.nslot * kStride;
+    auto part_ptr = [&](int i) {
+        int slot;
+        if (i < nfc) slot = i;
+        else if (i < nfc + nch[0]) slot = P.fmax + (i - nfc);
+        else if (i < nfc + nch[0] + nch[1]) slot = P.fmax + P.cmx[0] + (i - nfc - nch[0]);
+        else slot = P.fmax + P.cmx[0] + P.cmx[1] + (i - nfc - nch[0] - nch[1]);
+        return pb + (int64_t)slot * kStride;
+    };
+    // global max of the row over all parts
+    float M = -INFINITY;
+    for (int i = lane; i < nparts; i += 32) M = fmaxf(M, __ldcg(part_ptr(i) + GROUP * D + 2 * g));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    // this warp's share of the parts: i = sub, sub + 4, ...
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i0 = sub; i0 < nparts; i0 += kSub * 8) {
+        float4 a[8];
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int i = i0 + kSub * j;
+            if (i < nparts) {
+                const float* pi = part_ptr(i);
+                a[j] = __ldcg(reinterpret_cast<const float4*>(pi + g * D) + lane);
+                const float mi = __ldcg(pi + GROUP * D + 2 * g);
+                const float li = __ldcg(pi + GROUP * D + 2 * g + 1);
+                w[j] = mi == -INFINITY ? 0.f : ex2(mi - M);
+                L = fmaf(w[j], li, L);
+            } else {
+                a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                w[j] = 0.f;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            acc.x = fmaf(w[j], a[j].x, acc.x);
+            acc.y = fmaf(w[j], a[j].y, acc.y);
+            acc.z = fmaf(w[j], a[j].z, acc.z);
+            acc.w = fmaf(w[j], a[j].w, acc.w);
+        }
+    }
+    sm_acc[g][sub][lane] = acc;
+    if (lane == 0) sm_l[g][sub] = L;
+    __syncthreads();
+    if (sub == 0) {
+        float4 o = sm_acc[g][0][lane];
+        float Lt = sm_l[g][0];
+#pragma unroll
+        for (int k = 1; k < kSub; ++k) {
+            const float4 x = sm_acc[g][k][lane];
+            o.x += x.x;
+            o.y += x.y;
+            o.z += x.z;
+            o.w += x.w;
+            Lt += sm_l[g][k];
+        }
+        const float inv = 1.f / Lt;
+        const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
+        const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
+        if (P.out_dtype == KITTY_F32) {
+            reinterpret_cast<float4*>(static_cast<float*>(P.out) + row * D)[lane] =
+                make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
+        } else {
+            uint2 v;
+            v.x = f32_to_bf16_bits(o.x * inv) | (f32_to_bf16_bits(o.y * inv) << 16);
+            v.y = f32_to_bf16_bits(o.z * inv) | (f32_to_bf16_bits(o.w * inv) << 16);
+            reinterpret_cast<uint2*>(static_cast<uint16_t*>(P.out) + row * D)[lane] = v;
+        }
+    }
+    (void)sm_m;
 }
 
 }  // namespace fastattn
@@ -957,7 +949,7 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     const int nfp_max = min(max_tokens, c.cfg.s + c.cfg.r + c.cfg.g - 1);
     p.fmax = (nfp_max + kFpChunk - 1) / kFpChunk;
     if (p.fmax < 1) p.fmax = 1;
-    p.ctr_bytes = (((size_t)(2 + p.units) * sizeof(int)) + 255) & ~size_t(255);
+    p.ctr_bytes = 256;
     p.nslot = p.fmax + p.cmx[0] + p.cmx[1] + p.cmx[2];
     p.part_bytes = (size_t)p.units * p.nslot * p.group * (D + 2) * sizeof(float);
     return p;
@@ -976,6 +968,9 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     kfn<<<grid, kWarps * 32, sm, st>>>(prm);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    combine_parts_kernel<GROUP><<<prm.units, GROUP * 128, 0, st>>>(prm);
     return cudaGetLastError();
 }
 

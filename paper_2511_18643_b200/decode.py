@@ -51,7 +51,7 @@ class DecodeStep:
     def attention_launches(self) -> int:
         from .cache import KittyBatchCache  # noqa: F401
 
-        return 1 if self.fast_path() else 2
+        return 2  # attention + split combine (both paths)
 
     def fast_path(self) -> bool:
         c = self.cfg
