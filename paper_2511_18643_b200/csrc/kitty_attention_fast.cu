@@ -55,6 +55,7 @@ struct __align__(128) WarpSmem {
             float ps[4][kFpChunk];   // fp routine probabilities
         } fp;
     } u;
+    uint32_t qa[8][2][32];        // per lane: q*alpha B fragments (f16x2) of its column
     uint32_t ones[64];            // f16x2 (1, 1): scale operand of the aux B columns
     uint8_t inv[32];              // boosted channel of high_bits row j
     unsigned long long mbar[2];   // [0] key slot, [1] value slot
@@ -269,11 +270,14 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 
     uint32_t kph = 0, vph = 0;  // mbarrier parities of the two slots
 
+    // work tickets are fetched one pull ahead so the atomic's round trip overlaps
+    // the current item (lane 0 holds the outstanding ticket)
+    int tk = 0;
+    if (lane == 0) tk = atomicAdd(P.ctr, 1);
     auto pull = [&]() -> int {
-        int i = 0;
-        if (lane == 0) i = atomicAdd(P.ctr, 1);
-        __syncwarp();
-        return __shfl_sync(0xffffffffu, i, 0);
+        const int i = __shfl_sync(0xffffffffu, tk, 0);
+        if (lane == 0) tk = atomicAdd(P.ctr, 1);
+        return i;
     };
     // item -> (kind, unit, a, b); kind 0 = end, 1 = fp chunk a, 2 = pages [a, b), 3 = empty.
     // Queue: fp chunks interleaved with level-0 page chunks (latency-bound fp
@@ -349,7 +353,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 
     // per-unit query state: B fragments of q*alpha (f16x2) for this lane's column
     int cur_unit = -1;
-    uint32_t qa[8][2];
     auto q_row = [&](int u, int g) {
         const int b = u / hkv, h = u - b * hkv;
         return P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g) * D;
@@ -365,7 +368,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             for (int hh = 0; hh < 2; ++hh) {
                 const int d = 16 * ks + 2 * tig + 8 * hh;
                 const uint32_t w = col < GROUP ? __ldg(reinterpret_cast<const unsigned int*>(qg + d)) : 0u;
-                qa[ks][hh] = pack_f16x2(__uint_as_float(w << 16) * kAlpha, __uint_as_float(w & 0xffff0000u) * kAlpha);
+                sm.qa[ks][hh][lane] = pack_f16x2(__uint_as_float(w << 16) * kAlpha, __uint_as_float(w & 0xffff0000u) * kAlpha);
             }
         }
     };
@@ -548,11 +551,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
         // aux lanes (B columns 4-7) read their "scale" from a ones buffer
         const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
-#pragma unroll
+#pragma unroll 1
         for (int ks = 0; ks < 8; ++ks) {
             const int c0 = 16 * ks + 2 * tig;
-            const uint32_t b0 = hmul2(qa[ks][0], lds32(sbase + 2 * c0));
-            const uint32_t b1 = hmul2(qa[ks][1], lds32(sbase + 2 * (c0 + 8)));
+            const uint32_t b0 = hmul2(sm.qa[ks][0][lane], lds32(sbase + 2 * c0));
+            const uint32_t b1 = hmul2(sm.qa[ks][1][lane], lds32(sbase + 2 * (c0 + 8)));
             const uint32_t w0 = kw[8 * c0 + gid], w1 = kw[8 * (c0 + 1) + gid];
             const uint32_t w2 = kw[8 * (c0 + 8) + gid], w3 = kw[8 * (c0 + 9) + gid];
             mma_codes(kc, acc, w0, w1, w2, w3, b0, b1);
@@ -644,7 +647,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
         for (int m = 0; m < 8; ++m) pacc[m][0] = pacc[m][1] = pacc[m][2] = pacc[m][3] = 0.f;
         const uint8_t* vzero = vscale + 2 * G;
-#pragma unroll
+#pragma unroll 1
         for (int ks = 0; ks < 8; ++ks) {
             const int t0 = 16 * ks + 2 * tig;
             const uint32_t b0 = sm.u.pt[gid][t0 / 2];
@@ -791,9 +794,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             r[9] = 0;
         }
     }
-    // the last warp out resets the work queue for the next launch
+    // the last warp out resets the work queue for the next launch (after this
+    // warp's outstanding ticket returned: using its value orders the atomics)
     __syncwarp();
     if (lane == 0) {
+        asm volatile("" ::"r"(tk) : "memory");  // wait for the outstanding ticket
         const int done = atomicAdd(&P.ctr[1], 1);
         if (done == static_cast<int>(gridDim.x) * kWarps - 1) {
             P.ctr[0] = 0;
