@@ -34,7 +34,8 @@ namespace fastattn {
 constexpr int D = 128;
 constexpr int G = 128;
 constexpr int kWarps = 4;         // warps per CTA
-constexpr int kCtasPerSm = 3;      // 12 warps per SM
+constexpr int kCtasPerSm = 4;      // 16 warps per SM
+constexpr int kTmemCols = 32;      // per CTA: each warp parks its 32 output accumulators in its TMEM lane quarter
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
 constexpr int kPtStride = 136;     // f16 per row of the transposed-P buffer
@@ -130,6 +131,36 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+
+// Tensor memory as an extension of the register file: the running output
+// accumulators (32 fp32 per lane) live in TMEM between pages, so the QK phase
+// runs with 32 more free registers (16 warps / SM instead of 12).
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[8][4]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "f"(v[0][0]), "f"(v[0][1]), "f"(v[0][2]), "f"(v[0][3]), "f"(v[1][0]), "f"(v[1][1]), "f"(v[1][2]), "f"(v[1][3]),
+        "f"(v[2][0]), "f"(v[2][1]), "f"(v[2][2]), "f"(v[2][3]), "f"(v[3][0]), "f"(v[3][1]), "f"(v[3][2]), "f"(v[3][3]),
+        "f"(v[4][0]), "f"(v[4][1]), "f"(v[4][2]), "f"(v[4][3]), "f"(v[5][0]), "f"(v[5][1]), "f"(v[5][2]), "f"(v[5][3]),
+        "f"(v[6][0]), "f"(v[6][1]), "f"(v[6][2]), "f"(v[6][3]), "f"(v[7][0]), "f"(v[7][1]), "f"(v[7][2]), "f"(v[7][3])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[8][4]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=f"(v[0][0]), "=f"(v[0][1]), "=f"(v[0][2]), "=f"(v[0][3]), "=f"(v[1][0]), "=f"(v[1][1]), "=f"(v[1][2]),
+          "=f"(v[1][3]), "=f"(v[2][0]), "=f"(v[2][1]), "=f"(v[2][2]), "=f"(v[2][3]), "=f"(v[3][0]), "=f"(v[3][1]),
+          "=f"(v[3][2]), "=f"(v[3][3]), "=f"(v[4][0]), "=f"(v[4][1]), "=f"(v[4][2]), "=f"(v[4][3]), "=f"(v[5][0]),
+          "=f"(v[5][1]), "=f"(v[5][2]), "=f"(v[5][3]), "=f"(v[6][0]), "=f"(v[6][1]), "=f"(v[6][2]), "=f"(v[6][3]),
+          "=f"(v[7][0]), "=f"(v[7][1]), "=f"(v[7][2]), "=f"(v[7][3])
+        : "r"(taddr)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
@@ -253,11 +284,21 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     const bool main_col = gid < 4;
     const bool row0 = gid == 0;
 
+    __shared__ uint32_t tmem_base_sh;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "n"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
     if (lane == 0) {
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t taddr = tmem_base_sh + (static_cast<uint32_t>(32 * warp) << 16);
     sm.inv[lane] = 0;
     sm.ones[lane] = kOnes;
     sm.ones[lane + 32] = kOnes;
@@ -529,7 +570,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     };
 
     // ---- quantized pages: QK^T on the key slot, then P V on the value slot ----
-    float om[2], ol[2], ob16[2], ob64[2], oacc[8][4];
+    float om[2], ol[2], ob16[2], ob64[2];
+    bool ofresh = true;  // output accumulators in TMEM not yet written for this item
     float acc[8][4];  // logits, then probabilities, of the current page
     float mnew[2], corr[2], b16[2], b64[2];
 
@@ -668,6 +710,14 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         // rescaled when a running max of a real column moved (warp vote).
         const bool real0 = tig < 2 && 2 * tig < GROUP, real1 = tig < 2 && 2 * tig + 1 < GROUP;
         const bool rescale = __any_sync(0xffffffffu, (real0 && corr[0] != 1.f) || (real1 && corr[1] != 1.f));
+        float oacc[8][4];
+        if (ofresh) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) oacc[m][0] = oacc[m][1] = oacc[m][2] = oacc[m][3] = 0.f;
+        } else {
+            tmem_wait_st();
+            tmem_ld32(taddr, oacc);
+        }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const float sBv = __shfl_sync(0xffffffffu, vaux[j], tig & 1);
@@ -690,6 +740,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
             om[j] = mnew[j];
         }
+        tmem_st32(taddr, oacc);
+        ofresh = false;
     };
 
     // ---- work loop -------------------------------------------------------------------
@@ -723,8 +775,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 om[0] = om[1] = -INFINITY;
                 ol[0] = ol[1] = 0.f;
                 ob16[0] = ob16[1] = ob64[0] = ob64[1] = 0.f;
-#pragma unroll
-                for (int m = 0; m < 8; ++m) oacc[m][0] = oacc[m][1] = oacc[m][2] = oacc[m][3] = 0.f;
+                ofresh = true;
             }
             const bool more = p + 1 < p1;
             const bool chain = !more && nkind == 2;  // next item's first page follows
@@ -749,6 +800,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             if (item_done) {
                 const int slot = page_slot(p0, unit_geom(c, u).vp);
                 float* base = P.part + ((int64_t)u * P.nslot + slot) * GROUP * (D + 2);
+                float oacc[8][4];
+                tmem_wait_st();
+                tmem_ld32(taddr, oacc);
                 if (tig < 2) {
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
@@ -793,6 +847,13 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             r[8] = warp;
             r[9] = 0;
         }
+    }
+    tmem_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "n"(kTmemCols));
     }
     // the last warp out resets the work queue for the next launch (after this
     // warp's outstanding ticket returned: using its value orders the atomics)
