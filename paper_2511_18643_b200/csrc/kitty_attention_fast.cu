@@ -35,7 +35,7 @@ constexpr int D = 128;
 constexpr int G = 128;
 constexpr int kWarps = 4;         // warps per CTA
 constexpr int kCtasPerSm = 4;      // 16 warps per SM
-constexpr int kTmemCols = 32;      // per CTA: each warp parks its 32 output accumulators in its TMEM lane quarter
+constexpr int kTmemCols = 64;      // per CTA; per warp (its TMEM lane quarter): [0,32) output accumulators, [32,48) q fragments
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
 constexpr int kPtStride = 136;     // f16 per row of the transposed-P buffer
@@ -52,11 +52,10 @@ struct __align__(128) WarpSmem {
     union {
         uint32_t pt[8][kPtStride / 2];  // P^T as f16x2: rows 0-3 p*s, rows 4-7 p
         struct {
-            float qf[4][D];          // q * alpha (f32) for the fp routine
+            __half2 qf[4][D / 2];    // q * alpha (f16) for the fp routine
             float ps[4][kFpChunk];   // fp routine probabilities
         } fp;
     } u;
-    uint32_t qa[8][2][32];        // per lane: q*alpha B fragments (f16x2) of its column
     uint32_t ones[64];            // f16x2 (1, 1): scale operand of the aux B columns
     uint8_t inv[32];              // boosted channel of high_bits row j
     unsigned long long mbar[2];   // [0] key slot, [1] value slot
@@ -156,6 +155,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[8][4]) {
           "=f"(v[3][2]), "=f"(v[3][3]), "=f"(v[4][0]), "=f"(v[4][1]), "=f"(v[4][2]), "=f"(v[4][3]), "=f"(v[5][0]),
           "=f"(v[5][1]), "=f"(v[5][2]), "=f"(v[5][3]), "=f"(v[6][0]), "=f"(v[6][1]), "=f"(v[6][2]), "=f"(v[6][3]),
           "=f"(v[7][0]), "=f"(v[7][1]), "=f"(v[7][2]), "=f"(v[7][3])
+        : "r"(taddr)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[8][2]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(v[0][0]), "r"(v[0][1]), "r"(v[1][0]), "r"(v[1][1]), "r"(v[2][0]), "r"(v[2][1]), "r"(v[3][0]), "r"(v[3][1]),
+        "r"(v[4][0]), "r"(v[4][1]), "r"(v[5][0]), "r"(v[5][1]), "r"(v[6][0]), "r"(v[6][1]), "r"(v[7][0]), "r"(v[7][1])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[8][2]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[1][0]), "=r"(v[1][1]), "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[3][0]),
+          "=r"(v[3][1]), "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[5][0]), "=r"(v[5][1]), "=r"(v[6][0]), "=r"(v[6][1]),
+          "=r"(v[7][0]), "=r"(v[7][1])
         : "r"(taddr)
         : "memory");
 }
@@ -403,15 +422,18 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         cur_unit = u;
         const int col = gid & 3;
         const uint16_t* qg = q_row(u, col < GROUP ? col : 0);
+        uint32_t qa[8][2];
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
                 const int d = 16 * ks + 2 * tig + 8 * hh;
                 const uint32_t w = col < GROUP ? __ldg(reinterpret_cast<const unsigned int*>(qg + d)) : 0u;
-                sm.qa[ks][hh][lane] = pack_f16x2(__uint_as_float(w << 16) * kAlpha, __uint_as_float(w & 0xffff0000u) * kAlpha);
+                qa[ks][hh] = pack_f16x2(__uint_as_float(w << 16) * kAlpha, __uint_as_float(w & 0xffff0000u) * kAlpha);
             }
         }
+        tmem_wait_st();
+        tmem_st16(taddr + 32, qa);
     };
 
     // ---- one chunk of <= 32 full-precision tokens of a unit: the sink and the
@@ -430,9 +452,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
         for (int g = 0; g < GROUP; ++g) {
             const uint2 w = __ldg(reinterpret_cast<const uint2*>(q_row(u, g)) + lane);
-            *reinterpret_cast<float4*>(&sm.u.fp.qf[g][4 * lane]) =
-                make_float4(__uint_as_float(w.x << 16) * kAlpha, __uint_as_float(w.x & 0xffff0000u) * kAlpha,
-                            __uint_as_float(w.y << 16) * kAlpha, __uint_as_float(w.y & 0xffff0000u) * kAlpha);
+            sm.u.fp.qf[g][2 * lane] = __floats2half2_rn(__uint_as_float(w.x << 16) * kAlpha,
+                                                        __uint_as_float(w.x & 0xffff0000u) * kAlpha);
+            sm.u.fp.qf[g][2 * lane + 1] = __floats2half2_rn(__uint_as_float(w.y << 16) * kAlpha,
+                                                            __uint_as_float(w.y & 0xffff0000u) * kAlpha);
         }
         __syncwarp();
         const bool valid = lane < cnt;
@@ -457,8 +480,13 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                                          __uint_as_float(w[i].w << 16), __uint_as_float(w[i].w & 0xffff0000u)};
 #pragma unroll
                     for (int g = 0; g < GROUP; ++g) {
-                        const float4 qa_ = *reinterpret_cast<const float4*>(&sm.u.fp.qf[g][d0]);
-                        const float4 qb_ = *reinterpret_cast<const float4*>(&sm.u.fp.qf[g][d0 + 4]);
+                        const uint4 qh = *reinterpret_cast<const uint4*>(&sm.u.fp.qf[g][d0 / 2]);
+                        const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&qh.x));
+                        const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&qh.y));
+                        const float2 q45 = __half22float2(*reinterpret_cast<const __half2*>(&qh.z));
+                        const float2 q67 = __half22float2(*reinterpret_cast<const __half2*>(&qh.w));
+                        const float4 qa_ = make_float4(q01.x, q01.y, q23.x, q23.y);
+                        const float4 qb_ = make_float4(q45.x, q45.y, q67.x, q67.y);
                         lg[g] = fmaf(qa_.x, k8[0], lg[g]);
                         lg[g] = fmaf(qa_.y, k8[1], lg[g]);
                         lg[g] = fmaf(qa_.z, k8[2], lg[g]);
@@ -504,7 +532,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                     const float z_ = half_bits_to_f32(ld_u16(buf + zero_off + 2 * d));
                     const float kv = fmaf(static_cast<float>(code), s_, z_);
 #pragma unroll
-                    for (int g = 0; g < GROUP; ++g) lg[g] = fmaf(sm.u.fp.qf[g][d], kv, lg[g]);
+                    for (int g = 0; g < GROUP; ++g) {
+                        const __half2 qq = sm.u.fp.qf[g][d >> 1];
+                        lg[g] = fmaf((d & 1) ? __high2float(qq) : __low2float(qq), kv, lg[g]);
+                    }
                 }
             }
             __syncwarp();
@@ -593,11 +624,14 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
         // aux lanes (B columns 4-7) read their "scale" from a ones buffer
         const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
-#pragma unroll 1
+        uint32_t qa[8][2];
+        tmem_wait_st();
+        tmem_ld16(taddr + 32, qa);
+#pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             const int c0 = 16 * ks + 2 * tig;
-            const uint32_t b0 = hmul2(sm.qa[ks][0][lane], lds32(sbase + 2 * c0));
-            const uint32_t b1 = hmul2(sm.qa[ks][1][lane], lds32(sbase + 2 * (c0 + 8)));
+            const uint32_t b0 = hmul2(qa[ks][0], lds32(sbase + 2 * c0));
+            const uint32_t b1 = hmul2(qa[ks][1], lds32(sbase + 2 * (c0 + 8)));
             const uint32_t w0 = kw[8 * c0 + gid], w1 = kw[8 * (c0 + 1) + gid];
             const uint32_t w2 = kw[8 * (c0 + 8) + gid], w3 = kw[8 * (c0 + 9) + gid];
             mma_codes(kc, acc, w0, w1, w2, w3, b0, b1);
@@ -689,7 +723,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
         for (int m = 0; m < 8; ++m) pacc[m][0] = pacc[m][1] = pacc[m][2] = pacc[m][3] = 0.f;
         const uint8_t* vzero = vscale + 2 * G;
-#pragma unroll 1
+#pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             const int t0 = 16 * ks + 2 * tig;
             const uint32_t b0 = sm.u.pt[gid][t0 / 2];
