@@ -34,7 +34,7 @@ namespace fastattn {
 constexpr int D = 128;
 constexpr int G = 128;
 constexpr int kWarps = 4;         // warps per CTA
-constexpr int kCtasPerSm = 4;      // 16 warps per SM
+constexpr int kCtasPerSm = 3;      // 12 warps per SM
 constexpr int kTmemCols = 64;      // per CTA; per warp (its TMEM lane quarter): [0,32) output accumulators, [32,48) q fragments
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
@@ -712,8 +712,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 const uint32_t pu = pack_f16x2(acc[m][j], acc[m][2 + j]);
                 if (tig < 2) {
                     const int g = 2 * tig + j;
-                    sm.u.pt[g][tok / 2] = hmul2(pu, sv);
-                    sm.u.pt[4 + g][tok / 2] = pu;
+                    const int w = 8 * gid + (m ^ gid);  // XOR swizzle: conflict-free stores and loads
+                    sm.u.pt[g][w] = hmul2(pu, sv);
+                    sm.u.pt[4 + g][w] = pu;
                 }
             }
         }
@@ -726,8 +727,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             const int t0 = 16 * ks + 2 * tig;
-            const uint32_t b0 = sm.u.pt[gid][t0 / 2];
-            const uint32_t b1 = sm.u.pt[gid][t0 / 2 + 4];
+            const uint32_t b0 = sm.u.pt[gid][8 * ks + (tig ^ ks)];
+            const uint32_t b1 = sm.u.pt[gid][8 * ks + ((tig + 4) ^ ks)];
             const uint32_t w0 = vw[8 * t0 + gid], w1 = vw[8 * (t0 + 1) + gid];
             const uint32_t w2 = vw[8 * (t0 + 8) + gid], w3 = vw[8 * (t0 + 9) + gid];
             mma_codes(kc, pacc, w0, w1, w2, w3, b0, b1);
