@@ -34,7 +34,7 @@ namespace fastattn {
 constexpr int D = 128;
 constexpr int G = 128;
 constexpr int kWarps = 4;         // warps per CTA
-constexpr int kCtasPerSm = 3;      // 12 warps per SM
+constexpr int kCtasPerSm = 2;      // 8 warps per SM
 constexpr int kTmemCols = 64;      // per CTA; per warp (its TMEM lane quarter): [0,32) output accumulators, [32,48) q fragments
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
@@ -44,11 +44,12 @@ constexpr float kAlpha = 0.12751743074f;  // log2(e) / sqrt(128)
 constexpr uint32_t kMagic = 0x64006400u;  // f16x2 (1024, 1024)
 constexpr uint32_t kOnes = 0x3C003C00u;   // f16x2 (1, 1)
 
-// Per-warp shared memory (13.3 KB): one key-page slot and one value-page slot,
-// each refilled by cp.async.bulk one page ahead of its use.
+// Per-warp shared memory (23 KB): a 2-stage ring of (key page, value page)
+// slots; the pair for page i+1 is in flight (cp.async.bulk) while page i is
+// computed.
 struct __align__(128) WarpSmem {
-    uint8_t kbuf[kKeySlotMax];  // KTYP key body (also the fp routine's staged key page)
-    uint8_t vbuf[kValueSlot];   // KTYP value body
+    uint8_t kbuf[2][kKeySlotMax];  // KTYP key bodies (a free one also stages the fp routine's key page)
+    uint8_t vbuf[2][kValueSlot];   // KTYP value bodies
     union {
         uint32_t pt[8][kPtStride / 2];  // P^T as f16x2: rows 0-3 p*s, rows 4-7 p
         struct {
@@ -58,7 +59,7 @@ struct __align__(128) WarpSmem {
     } u;
     uint32_t ones[64];            // f16x2 (1, 1): scale operand of the aux B columns
     uint8_t inv[32];              // boosted channel of high_bits row j
-    unsigned long long mbar[2];   // [0] key slot, [1] value slot
+    unsigned long long mbar[2];   // one per stage
 };
 
 struct Params {
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     long long tr_t0 = trace ? gtimer() : 0, tr_fp = 0, tr_merge = 0, tr_wait = 0;
     int tr_nfp = 0, tr_npages = 0, tr_nmerge = 0;
 
-    uint32_t kph = 0, vph = 0;  // mbarrier parities of the two slots
+    uint32_t issued = 0, consumed = 0;  // page pairs put in flight / consumed (stage = count & 1)
 
     // work tickets are fetched one pull ahead so the atomic's round trip overlaps
     // the current item (lane 0 holds the outstanding ticket)
@@ -394,21 +395,17 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             if (kind != 3) return;
         }
     };
-    auto issue_k = [&](int u, int p) {
+    auto issue = [&](int u, int p) {
+        const int st = issued & 1;
         if (lane == 0) {
-            const uint8_t* src = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * kslot;
-            mbar_expect_tx(&sm.mbar[0], kslot);
-            bulk_g2s(sm.kbuf, src, kslot, &sm.mbar[0]);
+            const uint8_t* ks = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * kslot;
+            const uint8_t* vs = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * vslot;
+            mbar_expect_tx(&sm.mbar[st], kslot + vslot);
+            bulk_g2s(sm.kbuf[st], ks, kslot, &sm.mbar[st]);
+            bulk_g2s(sm.vbuf[st], vs, vslot, &sm.mbar[st]);
         }
         __syncwarp();
-    };
-    auto issue_v = [&](int u, int p) {
-        if (lane == 0) {
-            const uint8_t* src = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * vslot;
-            mbar_expect_tx(&sm.mbar[1], vslot);
-            bulk_g2s(sm.vbuf, src, vslot, &sm.mbar[1]);
-        }
-        __syncwarp();
+        ++issued;
     };
 
     // per-unit query state: B fragments of q*alpha (f16x2) for this lane's column
@@ -504,7 +501,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         while (need) {
             const int src = __ffs(need) - 1;
             const int page = __shfl_sync(0xffffffffu, pc / G, src);
-            uint8_t* buf = sm.kbuf;
+            uint8_t* buf = sm.kbuf[issued & 1];  // <= 1 pair in flight here: this stage is free
             const uint4* gsrc = reinterpret_cast<const uint4*>(
                 c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + page] * kslot);
 #pragma unroll
@@ -606,8 +603,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     float acc[8][4];  // logits, then probabilities, of the current page
     float mnew[2], corr[2], b16[2], b64[2];
 
-    auto qk_page = [&]() {
-        const uint8_t* kp = sm.kbuf;
+    auto qk_page = [&](int st) {
+        const uint8_t* kp = sm.kbuf[st];
         const uint32_t* kw = reinterpret_cast<const uint32_t*>(kp);
         // boosted rows -> channels (inverse of boost_idx)
         if (NKH > 0) {
@@ -698,8 +695,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
     };
 
-    auto pv_page = [&]() {
-        const uint8_t* vp = sm.vbuf;
+    auto pv_page = [&](int st) {
+        const uint8_t* vp = sm.vbuf[st];
         const uint32_t* vw = reinterpret_cast<const uint32_t*>(vp);
         const uint8_t* vscale = vp + G * D / 4;
         // P^T -> shared (rows 0-3: p * s_token, rows 4-7: p), tokens 16 gid + 2m (+1)
@@ -784,7 +781,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     next_item(kind, u, p0, p1);
     int nkind = 0, nu = 0, np0 = 0, np1 = 0;
     if (kind != 0) next_item(nkind, nu, np0, np1);
-    bool k_pending = false, v_pending = false;  // loads of the current item's first page issued
+    bool pending = false;  // the current item's first page pair is already in flight
     int p = p0;
 #pragma unroll 1
     while (kind != 0) {
@@ -793,43 +790,41 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const long long tf0 = trace ? gtimer() : 0;
             ++tr_nfp;
             process_fp(u, p0, [&]() {
-                if (nkind == 2) {
-                    issue_k(nu, np0);
-                    issue_v(nu, np0);
-                    k_pending = v_pending = true;
+                if (nkind == 2 && !pending) {
+                    issue(nu, np0);
+                    pending = true;
                 }
             });
             if (trace) tr_fp += gtimer() - tf0;
             item_done = true;
         } else {
             if (p == p0) {
-                if (!k_pending) issue_k(u, p0);
-                if (!v_pending) issue_v(u, p0);
-                k_pending = v_pending = false;
+                if (!pending) issue(u, p0);
+                pending = false;
                 load_unit(u);
                 om[0] = om[1] = -INFINITY;
                 ol[0] = ol[1] = 0.f;
                 ob16[0] = ob16[1] = ob64[0] = ob64[1] = 0.f;
                 ofresh = true;
             }
+            // next page pair into the other stage: this item's next page, or the
+            // next item's first page
             const bool more = p + 1 < p1;
-            const bool chain = !more && nkind == 2;  // next item's first page follows
-            const int iu = more ? u : nu;
-            const int ip = more ? p + 1 : np0;
+            const bool chain = !more && nkind == 2;
+            if (more) issue(u, p + 1);
+            if (chain) {
+                issue(nu, np0);
+                pending = true;
+            }
+            const int st = consumed & 1;
             const long long tw0 = trace ? gtimer() : 0;
-            mbar_wait(&sm.mbar[0], kph);
-            kph ^= 1u;
+            mbar_wait(&sm.mbar[st], (consumed >> 1) & 1);
             if (trace) tr_wait += gtimer() - tw0;
             ++tr_npages;
-            qk_page();
+            qk_page(st);
+            pv_page(st);
             __syncwarp();
-            if (more || chain) issue_k(iu, ip);  // key slot free
-            mbar_wait(&sm.mbar[1], vph);
-            vph ^= 1u;
-            pv_page();
-            __syncwarp();
-            if (more || chain) issue_v(iu, ip);  // value slot free
-            if (chain) k_pending = v_pending = true;
+            ++consumed;
             ++p;
             item_done = p == p1;
             if (item_done) {

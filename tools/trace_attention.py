@@ -36,7 +36,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 lib = kb.load_library()
 lib.kitty_debug_attention_trace.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
-n = 148 * 3 * 4
+n = 148 * 2 * 4
 buf = np.zeros((16384, 10), np.int64)
 lib.kitty_debug_attention_trace(1, None, 0)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
