@@ -13,7 +13,8 @@ import os
 from .errors import ConfigError, DeviceError, KittyError, PageFormatError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkitty_b200.so")
+# KITTY_B200_LIB points at an alternative in-tree build (kernel experiments only)
+LIB_PATH = os.environ.get("KITTY_B200_LIB") or os.path.join(_HERE, "libkitty_b200.so")
 
 KITTY_OK, KITTY_ERR_CONFIG, KITTY_ERR_INVALID, KITTY_ERR_PAGE_FORMAT, KITTY_ERR_CUDA, KITTY_ERR_UNSUPPORTED = range(6)
 STATUS_NONFINITE, STATUS_PAGE_FORMAT, STATUS_OVERFLOW = 1, 2, 4

@@ -182,6 +182,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[8][2]) {
 
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// D = A x B (C = 0): lets ptxas feed RZ instead of zeroing accumulators.
+__device__ __forceinline__ void mma16816_z(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                           uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%10,%10,%10};\n"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.f));
+}
+
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
@@ -244,6 +253,7 @@ __device__ __forceinline__ void conv_byte(const Consts& k, uint32_t w0, uint32_t
 
 // acc[8][4] += A(2-bit codes of rows r0..r3, word gid) x B for one k-step.
 // rows = (w0, w1) pair P0 and (w2, w3) pair P1.
+template <bool FIRST = false>
 __device__ __forceinline__ void mma_codes(const Consts& k, float (&acc)[8][4], uint32_t w0, uint32_t w1,
                                           uint32_t w2, uint32_t w3, uint32_t b0, uint32_t b1) {
     // all 8 tiles' A fragments first (32 registers): distinct registers let the
@@ -258,7 +268,12 @@ __device__ __forceinline__ void mma_codes(const Consts& k, float (&acc)[8][4], u
     conv_byte<3>(k, w0, w1, a[6][0], a[6][1], a[7][0], a[7][1]);
     conv_byte<3>(k, w2, w3, a[6][2], a[6][3], a[7][2], a[7][3]);
 #pragma unroll
-    for (int m = 0; m < 8; ++m) mma16816(acc[m], a[m][0], a[m][1], a[m][2], a[m][3], b0, b1);
+    for (int m = 0; m < 8; ++m) {
+        if (FIRST)
+            mma16816_z(acc[m], a[m][0], a[m][1], a[m][2], a[m][3], b0, b1);
+        else
+            mma16816(acc[m], a[m][0], a[m][1], a[m][2], a[m][3], b0, b1);
+    }
 }
 
 struct UnitGeom {
@@ -324,7 +339,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     sm.ones[lane + 32] = kOnes;
     __syncwarp();
     const Consts kc;
-    const uint32_t onesA = row0 ? kOnes : 0u;
     const bool trace = g_trace_on != 0;
     long long tr_t0 = trace ? gtimer() : 0, tr_fp = 0, tr_merge = 0, tr_wait = 0;
     int tr_nfp = 0, tr_npages = 0, tr_nmerge = 0;
@@ -616,9 +630,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
             __syncwarp();
         }
-        float aux[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+        float aux[4];
         // aux lanes (B columns 4-7) read their "scale" from a ones buffer
         const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
         uint32_t qa[8][2];
@@ -631,13 +643,17 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const uint32_t b1 = hmul2(qa[ks][1], lds32(sbase + 2 * (c0 + 8)));
             const uint32_t w0 = kw[8 * c0 + gid], w1 = kw[8 * (c0 + 1) + gid];
             const uint32_t w2 = kw[8 * (c0 + 8) + gid], w3 = kw[8 * (c0 + 9) + gid];
-            mma_codes(kc, acc, w0, w1, w2, w3, b0, b1);
-            uint32_t z0 = 0u, z1 = 0u;
-            if (row0) {
-                z0 = lds32(kp + zero_off + 2 * c0);
-                z1 = lds32(kp + zero_off + 2 * (c0 + 8));
+            // aux tile: only rows 0 (ones) and 8 (zero points) are read back, so
+            // every lane may load (rows 1-7 / 9-15 carry harmless copies)
+            const uint32_t z0 = lds32(kp + zero_off + 2 * c0);
+            const uint32_t z1 = lds32(kp + zero_off + 2 * (c0 + 8));
+            if (ks == 0) {
+                mma_codes<true>(kc, acc, w0, w1, w2, w3, b0, b1);
+                mma16816_z(aux, kOnes, z0, kOnes, z1, b0, b1);
+            } else {
+                mma_codes(kc, acc, w0, w1, w2, w3, b0, b1);
+                mma16816(aux, kOnes, z0, kOnes, z1, b0, b1);
             }
-            mma16816(aux, onesA, z0, onesA, z1, b0, b1);
         }
         if (NKH > 0) {
             const int col = gid & 3;
@@ -659,7 +675,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 const uint32_t* hw = reinterpret_cast<const uint32_t*>(kp + D * G / 4);
                 mma_codes(kc, acc, hw[8 * j0 + gid], hw[8 * (j0 + 1) + gid], hw[8 * (j0 + 8) + gid],
                           hw[8 * (j0 + 9) + gid], b0, b1);
-                mma16816(aux, onesA, 0u, onesA, 0u, b0, b1);
+                mma16816(aux, kOnes, 0u, kOnes, 0u, b0, b1);
             }
         }
         // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha)
@@ -717,9 +733,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
         __syncwarp();
         float pacc[8][4];
-        float vaux[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int m = 0; m < 8; ++m) pacc[m][0] = pacc[m][1] = pacc[m][2] = pacc[m][3] = 0.f;
+        float vaux[4];
         const uint8_t* vzero = vscale + 2 * G;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
@@ -728,13 +742,15 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const uint32_t b1 = sm.u.pt[gid][8 * ks + ((tig + 4) ^ ks)];
             const uint32_t w0 = vw[8 * t0 + gid], w1 = vw[8 * (t0 + 1) + gid];
             const uint32_t w2 = vw[8 * (t0 + 8) + gid], w3 = vw[8 * (t0 + 9) + gid];
-            mma_codes(kc, pacc, w0, w1, w2, w3, b0, b1);
-            uint32_t z0 = 0u, z1 = 0u;
-            if (row0) {
-                z0 = lds32(vzero + 2 * t0);
-                z1 = lds32(vzero + 2 * (t0 + 8));
+            const uint32_t z0 = lds32(vzero + 2 * t0);
+            const uint32_t z1 = lds32(vzero + 2 * (t0 + 8));
+            if (ks == 0) {
+                mma_codes<true>(kc, pacc, w0, w1, w2, w3, b0, b1);
+                mma16816_z(vaux, kOnes, z0, kOnes, z1, b0, b1);
+            } else {
+                mma_codes(kc, pacc, w0, w1, w2, w3, b0, b1);
+                mma16816(vaux, kOnes, z0, kOnes, z1, b0, b1);
             }
-            mma16816(vaux, onesA, z0, onesA, z1, b0, b1);
         }
         // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z).
         // Row constants (zero points, the 1024 offset) accumulate per column in
