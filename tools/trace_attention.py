@@ -65,3 +65,15 @@ print(f"per-SM last warp end: min {per_sm_end.min():.1f} p50 {np.median(per_sm_e
 order = np.argsort(end)[-8:]
 for i in order:
     print(f"  late warp sm {r[i, 0]} end {end[i]:.1f} fp {r[i, 3]} pages {r[i, 4]} fp_us {r[i, 5] / 1e3:.1f} merge_us {r[i, 6] / 1e3:.1f}")
+
+# compute-only: same launch with page loads skipped (stale shared-memory pages)
+lib.kitty_debug_attention_trace(3, None, 0)
+cache.attend(q)
+torch.cuda.synchronize()
+lib.kitty_debug_attention_trace(0, buf.ctypes.data, 16384)
+r = buf[:n]
+r = r[r[:, 1] > 0]
+t0 = r[:, 1].min()
+end = (r[:, 2] - t0) / 1e3
+print(f"[compute-only] warp end p50 {np.percentile(end, 50):.1f} max {end.max():.1f} us; page time per warp "
+      f"{((end * 1e3 - r[:, 5] / 1e3) / np.maximum(r[:, 4], 1)).mean():.0f} ns")
