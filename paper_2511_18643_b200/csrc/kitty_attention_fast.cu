@@ -215,6 +215,12 @@ __device__ __forceinline__ float ex2(float x) {
     return r;
 }
 
+__device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
+    uint32_t r;
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t lds32(const void* p) { return *reinterpret_cast<const uint32_t*>(p); }
 
 // Two 32-bit words = 16 tokens (K: one channel row) or 16 channels (V: one
@@ -230,25 +236,32 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
 }
 
 struct Consts {
-    uint32_t m_lo, m_hi, magic;
+    uint32_t m0, m1, m2, m3, magic;
     __device__ __forceinline__ Consts() {
-        m_lo = 0x00300030u;
-        m_hi = 0x00C000C0u;
+        m0 = 0x03000300u;  // code 0 of the byte, from its copy in bits 8-15: weight 256
+        m1 = 0x000C000Cu;  // code 1, bits 2-3: weight 4
+        m2 = 0x00300030u;  // code 2, bits 4-5: weight 16
+        m3 = 0x00C000C0u;  // code 3, bits 6-7: weight 64
         magic = kMagic;
-        asm volatile("" : "+r"(m_lo), "+r"(m_hi), "+r"(magic));
+        asm volatile("" : "+r"(m0), "+r"(m1), "+r"(m2), "+r"(m3), "+r"(magic));
     }
 };
 
+// Byte b of two rows -> the fp16x2 A operands of its 4 codes: one PRMT puts
+// byte b of w0 in bytes 0 and 1 and byte b of w1 in bytes 2 and 3, then one
+// LOP3 per code keeps that code's two bits inside the mantissa and ORs the
+// exponent of 1024: f16 = 1024 + w * code with w = 256 / 4 / 16 / 64 for
+// codes 0 / 1 / 2 / 3 (the weight and the 1024 are removed per row after the
+// MMA; w >= 4 keeps the offset cancellation far below fp16 operand rounding).
 template <int B>
-__device__ __forceinline__ void conv_byte(const Consts& k, uint32_t w0, uint32_t w1, uint32_t& e_lo,
-                                          uint32_t& e_hi, uint32_t& o_lo, uint32_t& o_hi) {
+__device__ __forceinline__ void conv_byte(const Consts& k, uint32_t w0, uint32_t w1, uint32_t& c0,
+                                          uint32_t& c1, uint32_t& c2, uint32_t& c3) {
     constexpr uint32_t sel = B | (B << 4) | ((4 + B) << 8) | ((4 + B) << 12);
     const uint32_t x = prmt(w0, w1, sel);
-    const uint32_t y = x * 16u;
-    e_lo = and_or(y, k.m_lo, k.magic);
-    e_hi = and_or(y, k.m_hi, k.magic);
-    o_lo = and_or(x, k.m_lo, k.magic);
-    o_hi = and_or(x, k.m_hi, k.magic);
+    c0 = and_or(x, k.m0, k.magic);
+    c1 = and_or(x, k.m1, k.magic);
+    c2 = and_or(x, k.m2, k.magic);
+    c3 = and_or(x, k.m3, k.magic);
 }
 
 // acc[8][4] += A(2-bit codes of rows r0..r3, word gid) x B for one k-step.
@@ -615,10 +628,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     };
 
     // ---- quantized pages: QK^T on the key slot, then P V on the value slot ----
-    float om[2], ol[2], ob16[2], ob64[2];
+    float om[2], ol[2], ob[4][2];  // running max / sum; per-weight-class row constants
     bool ofresh = true;  // output accumulators in TMEM not yet written for this item
-    float acc[8][4];  // logits, then probabilities, of the current page
-    float mnew[2], corr[2], b16[2], b64[2];
+    float acc[8][4];     // logits of the current page
+    uint32_t pu[8][2];   // its probabilities, f16x2 (token pairs)
+    float mnew[2], corr[2], bw[4][2];
 
     auto qk_page = [&](int st) {
         const uint8_t* kp = sm.kbuf[st];
@@ -681,36 +695,42 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 mma16816(aux, kOnes, 0u, kOnes, 0u, b0, b1);
             }
         }
-        // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha)
+        // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha).
+        // Row weights: even tiles hold codes 0 / 1 of a byte (w 256 / 4), odd tiles 2 / 3 (w 16 / 64).
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const float sumB = __shfl_sync(0xffffffffu, aux[j], tig & 1);
             const float cst = __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
-            b16[j] = cst - 64.f * sumB;
-            b64[j] = cst - 16.f * sumB;
-            float x16 = acc[0][j], x64 = acc[0][2 + j];
+            bw[0][j] = cst - 4.f * sumB;    // w 256
+            bw[1][j] = cst - 256.f * sumB;  // w 4
+            bw[2][j] = cst - 64.f * sumB;   // w 16
+            bw[3][j] = cst - 16.f * sumB;   // w 64
+            float x0 = acc[0][j], x1 = acc[0][2 + j], x2 = acc[1][j], x3 = acc[1][2 + j];
 #pragma unroll
-            for (int m = 1; m < 8; ++m) {
-                x16 = fmaxf(x16, acc[m][j]);
-                x64 = fmaxf(x64, acc[m][2 + j]);
+            for (int m = 2; m < 8; m += 2) {
+                x0 = fmaxf(x0, acc[m][j]);
+                x1 = fmaxf(x1, acc[m][2 + j]);
+                x2 = fmaxf(x2, acc[m + 1][j]);
+                x3 = fmaxf(x3, acc[m + 1][2 + j]);
             }
-            float pm = fmaxf(fmaf(x16, 1.f / 16.f, b16[j]), fmaf(x64, 1.f / 64.f, b64[j]));
+            float pm = fmaxf(fmaxf(fmaf(x0, 1.f / 256.f, bw[0][j]), fmaf(x1, 1.f / 4.f, bw[1][j])),
+                             fmaxf(fmaf(x2, 1.f / 16.f, bw[2][j]), fmaf(x3, 1.f / 64.f, bw[3][j])));
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 4));
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 8));
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 16));
             mnew[j] = fmaxf(om[j], pm);
             corr[j] = ex2(om[j] - mnew[j]);
-            b16[j] -= mnew[j];
-            b64[j] -= mnew[j];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) bw[c4][j] -= mnew[j];
         }
-        // probabilities in place (log2 domain)
+        // probabilities (log2 domain), two tokens per f16x2 ex2: pu[m][j] = (p(tok), p(tok + 1))
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
+            const float wlo = (m & 1) ? 1.f / 16.f : 1.f / 256.f, whi = (m & 1) ? 1.f / 64.f : 1.f / 4.f;
+            const int clo = (m & 1) ? 2 : 0, chi = (m & 1) ? 3 : 1;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                acc[m][j] = ex2(fmaf(acc[m][j], 1.f / 16.f, b16[j]));
-                acc[m][2 + j] = ex2(fmaf(acc[m][2 + j], 1.f / 64.f, b64[j]));
-            }
+            for (int j = 0; j < 2; ++j)
+                pu[m][j] = ex2_h2(pack_f16x2(fmaf(acc[m][j], wlo, bw[clo][j]), fmaf(acc[m][2 + j], whi, bw[chi][j])));
         }
     };
 
@@ -725,12 +745,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const uint32_t sv = lds32(vscale + 2 * tok);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const uint32_t pu = pack_f16x2(acc[m][j], acc[m][2 + j]);
                 if (tig < 2) {
                     const int g = 2 * tig + j;
                     const int w = 8 * gid + (m ^ gid);  // XOR swizzle: conflict-free stores and loads
-                    sm.u.pt[g][w] = hmul2(pu, sv);
-                    sm.u.pt[4 + g][w] = pu;
+                    sm.u.pt[g][w] = hmul2(pu[m][j], sv);
+                    sm.u.pt[4 + g][w] = pu[m][j];
                 }
             }
         }
@@ -757,7 +776,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
         // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z).
         // Row constants (zero points, the 1024 offset) accumulate per column in
-        // ob16 / ob64 and are added at the flush; the accumulators are only
+        // ob[weight class] and are added at the flush; the accumulators are only
         // rescaled when a running max of a real column moved (warp vote).
         const bool real0 = tig < 2 && 2 * tig < GROUP, real1 = tig < 2 && 2 * tig + 1 < GROUP;
         const bool rescale = __any_sync(0xffffffffu, (real0 && corr[0] != 1.f) || (real1 && corr[1] != 1.f));
@@ -775,8 +794,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const float lp = __shfl_sync(0xffffffffu, vaux[j], 2 + (tig & 1));
             const float zz = __shfl_sync(0xffffffffu, vaux[2 + j], 2 + (tig & 1));
             ol[j] = fmaf(ol[j], corr[j], lp);
-            ob16[j] = fmaf(ob16[j], corr[j], zz - 64.f * sBv);
-            ob64[j] = fmaf(ob64[j], corr[j], zz - 16.f * sBv);
+            ob[0][j] = fmaf(ob[0][j], corr[j], zz - 4.f * sBv);
+            ob[1][j] = fmaf(ob[1][j], corr[j], zz - 256.f * sBv);
+            ob[2][j] = fmaf(ob[2][j], corr[j], zz - 64.f * sBv);
+            ob[3][j] = fmaf(ob[3][j], corr[j], zz - 16.f * sBv);
             if (rescale) {
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
@@ -786,8 +807,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                oacc[m][j] = fmaf(pacc[m][j], 1.f / 16.f, oacc[m][j]);
-                oacc[m][2 + j] = fmaf(pacc[m][2 + j], 1.f / 64.f, oacc[m][2 + j]);
+                oacc[m][j] = fmaf(pacc[m][j], (m & 1) ? 1.f / 16.f : 1.f / 256.f, oacc[m][j]);
+                oacc[m][2 + j] = fmaf(pacc[m][2 + j], (m & 1) ? 1.f / 64.f : 1.f / 4.f, oacc[m][2 + j]);
             }
             om[j] = mnew[j];
         }
@@ -823,7 +844,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 load_unit(u);
                 om[0] = om[1] = -INFINITY;
                 ol[0] = ol[1] = 0.f;
-                ob16[0] = ob16[1] = ob64[0] = ob64[1] = 0.f;
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) ob[c4][0] = ob[c4][1] = 0.f;
                 ofresh = true;
             }
             // next page pair into the other stage: this item's next page, or the
@@ -860,7 +882,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
                             for (int m = 0; m < 8; ++m)
                                 *reinterpret_cast<float2*>(base + g * D + 16 * gid + 2 * m) =
-                                    make_float2(oacc[m][j] + ob16[j], oacc[m][2 + j] + ob64[j]);
+                                    make_float2(oacc[m][j] + ob[(m & 1) ? 2 : 0][j],
+                                                oacc[m][2 + j] + ob[(m & 1) ? 3 : 1][j]);
                             if (gid == 0) {
                                 base[GROUP * D + 2 * g] = om[j];
                                 base[GROUP * D + 2 * g + 1] = ol[j];
