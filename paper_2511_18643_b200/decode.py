@@ -55,7 +55,7 @@ class DecodeStep:
 
     def fast_path(self) -> bool:
         c = self.cfg
-        return c.d == 128 and c.g == 128 and c.group_size in (1, 2, 4) and c.d_boost <= 32
+        return c.d == 128 and c.g == 128 and c.group_size in (1, 2, 4, 8) and c.d_boost <= 32
 
     def _launch(self):
         lib, st = self.lib, _stream()
