@@ -136,6 +136,7 @@ def run_kitty(args):
     if args.boost is not None:
         frac = args.boost
     cfg = kb.KittyConfig(h_kv=h_kv, h_q=h_q, boost_fraction=frac)
+    kb.select_attention_kernel(args.kernel)
     steps, warmup = args.steps, args.warmup
     max_tokens = ctx + warmup + steps + 2 * (warmup + steps) + 8
     gen = torch.Generator(device=dev)
@@ -461,6 +462,8 @@ def main():
     ap.add_argument("--boost", type=float, default=None)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel", choices=["default", "tc"], default="default",
+                    help="decode-attention kernel (experiments): default dispatch or the tcgen05 kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -190,6 +190,18 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv,
                           const int32_t* kv_head_map, float* out, void* workspace,
                           size_t workspace_bytes, void* stream);
 
+/* ---- debug / experiments (not part of the reference interface) ------- */
+
+/* Select the decode-attention kernel: 0 = default dispatch (mma.sync kernel
+ * for GQA groups <= 4, tcgen05 kernel for group 8), 1 = the tcgen05 kernel
+ * wherever it applies.  Process-wide; not thread-safe. */
+int kitty_debug_select_attention(int impl);
+/* Event timeline of CTA 0 of the tcgen05 kernel: enable != 0 records the next
+ * launches; host_out (optional) receives max_rows x 16 int64 timestamps. */
+int kitty_debug_tc_trace(int enable, long long* host_out, int max_rows);
+/* Per-warp trace of the mma.sync kernel (same convention, 10 fields). */
+int kitty_debug_attention_trace(int enable, long long* host_out, int max_warps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,6 +80,9 @@ SIGNATURES = [
     ("kitty_dense_attention_workspace_bytes", c_size_t, [c_int32, c_int32, c_int32]),
     ("kitty_dense_attention", ctypes.c_int,
      [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("kitty_debug_select_attention", ctypes.c_int, [ctypes.c_int]),
+    ("kitty_debug_tc_trace", ctypes.c_int, [ctypes.c_int, c_void_p, ctypes.c_int]),
+    ("kitty_debug_attention_trace", ctypes.c_int, [ctypes.c_int, c_void_p, ctypes.c_int]),
 ]
 
 _lib = None
@@ -133,6 +136,12 @@ def raise_status(word: int, what: str = "") -> None:
     if word & STATUS_OVERFLOW:
         raise KittyError(f"{what}: cache capacity (block table) exceeded")
     raise KittyError(f"{what}: device status 0x{word:x}")
+
+
+def select_attention_kernel(impl: str) -> None:
+    """Experiments: "default" (mma.sync kernel for GQA groups <= 4, tcgen05 for
+    group 8) or "tc" (the tcgen05 kernel wherever it applies)."""
+    check(load_library().kitty_debug_select_attention({"default": 0, "tc": 1}[impl]), "select attention")
 
 
 def exported_symbols() -> list[str]:

@@ -208,12 +208,17 @@ static int generic_splits(int max_tokens) {
     return max_tokens <= 0 ? 1 : (max_tokens + kGenericChunk - 1) / kGenericChunk;
 }
 
+static int g_attention_impl = 0;
+void set_attention_impl(int impl) { g_attention_impl = impl; }
+
 size_t attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
     const int units = c.num_seqs * c.cfg.h_kv;
     const int group = c.cfg.h_q / c.cfg.h_kv;
     size_t generic = (size_t)units * generic_splits(max_tokens) * group * (c.cfg.d + 2) * sizeof(float);
     size_t fast = fast_attention_workspace_bytes(c, max_tokens);
-    return generic > fast ? generic : fast;
+    size_t tc = tc_attention_workspace_bytes(c, max_tokens);
+    size_t w = generic > fast ? generic : fast;
+    return w > tc ? w : tc;
 }
 
 cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, void* out,
@@ -221,7 +226,11 @@ cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, 
                                     cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
     if (units == 0) return cudaSuccess;
-    if (fast_attention_supported(c)) return launch_fast_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
+    // mma.sync kernel for GQA groups <= 4 (fastest measured); the
+    // tcgen05 kernel for group 8 and when selected
+    if (fast_attention_supported(c) && !(g_attention_impl == 1 && tc_attention_supported(c)))
+        return launch_fast_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
+    if (tc_attention_supported(c)) return launch_tc_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
     const int group = c.cfg.h_q / c.cfg.h_kv;
     const int d = c.cfg.d;
     const int splits = generic_splits(max_tokens);

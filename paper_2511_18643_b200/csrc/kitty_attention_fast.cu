@@ -33,6 +33,8 @@ namespace fastattn {
 
 constexpr int D = 128;
 constexpr int G = 128;
+// floats per partial record (acc[group][D], then (m, l) per row), padded to 16 B
+__host__ __device__ constexpr int part_stride(int group) { return (group * (D + 2) + 3) & ~3; }
 constexpr int kWarps = 4;         // warps per CTA
 constexpr int kCtasPerSm = 2;      // 8 warps per SM
 constexpr int kTmemCols = 64;      // per CTA; per warp (its TMEM lane quarter): [0,32) output accumulators, [32,48) q fragments
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
         }
         __syncwarp();
-        float* base = P.part + ((int64_t)u * P.nslot + fc) * GROUP * (D + 2);
+        float* base = P.part + ((int64_t)u * P.nslot + fc) * part_stride(GROUP);
 #pragma unroll
         for (int g = 0; g < GROUP; ++g) {
             reinterpret_cast<float4*>(base + g * D)[lane] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
@@ -870,7 +872,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             item_done = p == p1;
             if (item_done) {
                 const int slot = page_slot(p0, unit_geom(c, u).vp);
-                float* base = P.part + ((int64_t)u * P.nslot + slot) * GROUP * (D + 2);
+                float* base = P.part + ((int64_t)u * P.nslot + slot) * part_stride(GROUP);
                 float oacc[8][4];
                 tmem_wait_st();
                 tmem_ld32(taddr, oacc);
@@ -961,7 +963,7 @@ __global__ void __launch_bounds__(GROUP * 128) combine_parts_kernel(Params P) {
         nch[lv] = (n + P.cs[lv] - 1) / P.cs[lv];
     }
     const int nparts = nfc + nch[0] + nch[1] + nch[2];
-    constexpr int kStride = GROUP * (D + 2);
+    constexpr int kStride = part_stride(GROUP);
     const float* pb = P.part + (int64_t)u * P.nslot * kStride;
     auto part_ptr = [&](int i) {
         int slot;
@@ -1089,7 +1091,7 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     if (p.fmax < 1) p.fmax = 1;
     p.ctr_bytes = 256;
     p.nslot = p.fmax + p.cmx[0] + p.cmx[1] + p.cmx[2];
-    p.part_bytes = (size_t)p.units * p.nslot * p.group * (D + 2) * sizeof(float);
+    p.part_bytes = (size_t)p.units * p.nslot * part_stride(p.group) * sizeof(float);
     return p;
 }
 

@@ -42,25 +42,33 @@ namespace tcattn {
 
 constexpr int D = 128;
 constexpr int G = 128;
-constexpr int NST = 6;             // TMA ring stages
+// floats per partial record (acc[group][D], then (m, l) per row), padded to 16 B
+__host__ __device__ constexpr int part_stride(int group) { return (group * (D + 2) + 3) & ~3; }
+constexpr int NDESC = 8;           // page-descriptor ring (scheduler -> converters)
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
 constexpr int kFpChunk = 32;       // fp tokens per fp item
 constexpr int kFpWarps = 2;
-constexpr int kThreads = (14 + kFpWarps) * 32;  // WG-A 0-3, WG-B 4-7, WG-C 8-11, TMA 12, MMA 13, FP 14-15
+constexpr int kCtasPerSm = 1;    // independent page pipelines per SM
+constexpr int kThreads = (14 + kFpWarps) * 32;  // WG-A 0-3, WG-B 4-7, WG-C 8-11, scheduler 12, MMA 13, FP 14-15
 constexpr float kAlpha = 0.12751743074f;        // log2(e) / sqrt(128)
 constexpr int kQuant = 16000;                   // fixed-point range of the int8 (lo, hi) pairs (< 2^14)
 constexpr int kTileA = 1024 * 16;               // 128 x 128 u8 operand tile
 constexpr int kTileAK = 1024 * 20;              // + 32 boosted rows
+constexpr int NB = 16;                          // B row bytes of both MMAs: (lo, hi) per query, padded
 
 constexpr uint32_t FL_FIRST = 1, FL_LAST = 2, FL_END = 4;
 
-struct StageInfo {
-    int unit, page, flags, slot;
+// One page pair of an item, written by the scheduler; q rows of the unit follow
+// (bulk-copied) on an item's first page.
+struct PageDesc {
+    const uint8_t* kp;
+    const uint8_t* vp;
+    int unit, flags, slot, pad;
 };
 struct KInfo {
-    float stepx, stepz;
-    int flags, unit, slot, pad[3];
+    float stepx;
+    int flags, unit, slot;
 };
 struct RingEntry {
     float corr[8];
@@ -69,40 +77,30 @@ struct RingEntry {
     int pad[15];
 };
 
-// Shared-memory layout of one CTA (dynamic, 1024-aligned regions).
+// Shared-memory layout of one CTA (dynamic, 1024-aligned operand tiles).
 template <int GROUP>
 struct Smem {
-    static constexpr int NX = GROUP * 2 > 8 ? GROUP * 2 : 8;  // bytes of the q*s columns in a B row
-    static constexpr int NQK = 2 * NX;                          // B row: (q s | q z) columns
-    static constexpr int NCH = NQK / 16;                        // 16-byte MN chunks per B row
-    static constexpr int NP = 16;                               // value-MMA B row (p s lo/hi, padded)
-    static constexpr int kStage = kKeySlotMax + kValueSlot + GROUP * D * 2;
-    static constexpr int kStageAl = (kStage + 127) / 128 * 128;
-    static constexpr int kBQK = 160 * NQK;
-    // offsets
-    static constexpr int o_ring = 0;
-    static constexpr int o_ak = (o_ring + NST * kStageAl + 1023) / 1024 * 1024;
+    static constexpr int kDesc = (32 + GROUP * D * 2 + 127) / 128 * 128;
+    static constexpr int o_desc = 0;
+    static constexpr int o_ak = (NDESC * kDesc + 1023) / 1024 * 1024;
     static constexpr int o_av = o_ak + 2 * kTileAK;
-    static constexpr int o_ones = o_av + 2 * kTileA;
-    static constexpr int o_bqk = o_ones + 4096;
-    static constexpr int o_bp = o_bqk + 2 * kBQK;
-    static constexpr int o_vmeta = o_bp + 2 * 128 * NP;          // [2][128] float2 (s, z)
-    static constexpr int o_fp = o_vmeta + 2 * 128 * 8;           // per fp warp scratch
+    static constexpr int o_bqk = o_av + 2 * kTileA;
+    static constexpr int o_bp = o_bqk + 2 * 160 * NB;
+    static constexpr int o_vmeta = o_bp + 2 * 128 * NB;          // [2][128] float2 (s, z)
+    static constexpr int o_zx = o_vmeta + 2 * 128 * 8;            // [2][4 warps][8] partial sum_d q alpha z_d
+    static constexpr int o_fp = o_zx + 2 * 4 * 8 * 4;             // per fp warp scratch
     static constexpr int kFpBytes = kKeySlotMax + GROUP * D * 2 + GROUP * kFpChunk * 4;
     static constexpr int kFpAl = (kFpBytes + 127) / 128 * 128;
     static constexpr int o_ring4 = o_fp + kFpWarps * kFpAl;      // RingEntry[4]
-    static constexpr int o_misc = o_ring4 + 4 * sizeof(RingEntry);
-    // misc: stage info [NST], kinfo [2], vinfo [2] (float invp), xch [3][4][16] floats, barriers
-    static constexpr int o_sinfo = o_misc;
-    static constexpr int o_kinfo = o_sinfo + NST * 16;
-    static constexpr int o_vinfo = o_kinfo + 2 * 32;
-    static constexpr int o_xch = o_vinfo + 16;
-    static constexpr int o_bar = o_xch + 3 * 64 * 4;  // two page-max buffers + one item-end sum buffer
-    static constexpr int kBars = 2 * NST + 9 * 2;
+    static constexpr int o_kinfo = o_ring4 + 4 * sizeof(RingEntry);
+    static constexpr int o_vinfo = o_kinfo + 2 * 16;
+    static constexpr int o_xch = o_vinfo + 16;                    // [3][64] floats: page-max x2, item sums
+    static constexpr int o_bar = o_xch + 3 * 64 * 4;
+    static constexpr int kBars = 2 * NDESC + 8 * 2;
     static constexpr int o_tmem = o_bar + kBars * 8;
     static constexpr int kBytes = o_tmem + 16;
-    // TMEM columns: S[b] = (D1 | D2) at b * 2 NQK, O[b] at 4 NQK + b * NP
-    static constexpr int kTmemCols = (4 * NQK + 2 * NP) <= 128 ? 128 : 256;
+    // TMEM columns: S[b] at 16 b, O[b] at 32 + 16 b
+    static constexpr int kTmemCols = 64;
 };
 
 struct Params {
@@ -119,6 +117,17 @@ struct Params {
     float* part;
 };
 
+// ---- optional event trace of CTA 0 (kitty_debug_attention_trace) ----
+constexpr int kTrPages = 512;
+constexpr int kTrFields = 16;
+__device__ long long g_tr[kTrPages * kTrFields];
+__device__ int g_tr_on;
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---- PTX helpers -------------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -132,13 +141,16 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase
+// completes instead of polling the barrier (polling competes with the
+// converters for issue slots and the shared-memory pipe).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(bar),
-        "r"(phase)
+        "r"(phase), "r"(1000000)
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -437,7 +449,7 @@ __device__ void fp_chunk(const Params& P, uint8_t* scratch, int u, int fc, int l
         }
     }
     __syncwarp();
-    float* base = P.part + ((int64_t)u * P.nslot + fc) * GROUP * (D + 2);
+    float* base = P.part + ((int64_t)u * P.nslot + fc) * part_stride(GROUP);
 #pragma unroll
     for (int g = 0; g < GROUP; ++g) {
         reinterpret_cast<float4*>(base + g * D)[lane] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
@@ -451,52 +463,126 @@ __device__ void fp_chunk(const Params& P, uint8_t* scratch, int u, int fc, int l
 
 // ---- the kernel --------------------------------------------------------------------
 
+__device__ __forceinline__ uint4 ldg_na128(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ldg64(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg16(const void* p) {
+    unsigned short v;
+    asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg8(const void* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+// max of the 4 f16 of (x, y) as float
+__device__ __forceinline__ float hmax4(uint2 v) {
+    const uint32_t m = hmax2(v.x, v.y);
+    return fmaxf(h2f(m & 0xffffu), h2f(m >> 16));
+}
+
+// Sum of v[g] over the 32 lanes for every g: reduce-scatter over the top
+// log2(N) lane bits, then a butterfly; lane l ends with the sum for query
+// scatter_query<N>(l) in v[0].
+template <int N>
+__device__ __forceinline__ void warp_sum_scatter(float (&v)[N], int lane) {
+    int n = N;
+    int m = 16;
+#pragma unroll
+    for (int lv = 0; lv < 3; ++lv) {
+        if (n > 1) {
+            const int half = n / 2;
+            const bool hi = (lane & m) != 0;
+#pragma unroll
+            for (int k = 0; k < N / 2; ++k) {
+                if (k < half) {
+                    const float keep = hi ? v[half + k] : v[k];
+                    const float send = hi ? v[k] : v[half + k];
+                    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                }
+            }
+            n = half;
+            m >>= 1;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        if (m > 0) {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
+            m >>= 1;
+        }
+    }
+}
+template <int N>
+__device__ __forceinline__ int scatter_query(int lane) {
+    return N == 1 ? 0 : (N == 2 ? (lane >> 4) & 1 : (N == 4 ? (lane >> 3) & 3 : (lane >> 2) & 7));
+}
+template <int N>
+__device__ __forceinline__ bool scatter_owner(int lane) {
+    return (lane & (32 / N - 1)) == 0;
+}
+
 template <int GROUP>
-__global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) tc_attention_kernel(Params P) {
     using L = Smem<GROUP>;
-    constexpr int NX = L::NX, NQK = L::NQK, NCH = L::NCH, NP = L::NP;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = smem_u32(smem);
     const KittyCacheDesc& c = P.c;
     const int d_boost = c.cfg.d_boost;
-    const int kslot = static_cast<int>(c.key_slot_bytes);
-    const int vslot = static_cast<int>(c.value_slot_bytes);
     const int scale_off = D * G / 4 + d_boost * G / 4 + D;
     const int zero_off = scale_off + 2 * D;
     const int idx_off = D * G / 4 + d_boost * G / 4;
 
-    auto stage_k = [&](int s) { return sbase + L::o_ring + s * L::kStageAl; };
-    auto stage_v = [&](int s) { return stage_k(s) + kKeySlotMax; };
-    auto stage_q = [&](int s) { return stage_k(s) + kKeySlotMax + kValueSlot; };
-    StageInfo* sinfo = reinterpret_cast<StageInfo*>(smem + L::o_sinfo);
+    auto desc_ptr = [&](int i) { return reinterpret_cast<const PageDesc*>(smem + L::o_desc + (i % NDESC) * L::kDesc); };
+    auto desc_q = [&](int i) { return sbase + L::o_desc + (i % NDESC) * L::kDesc + 32; };
     KInfo* kinfo = reinterpret_cast<KInfo*>(smem + L::o_kinfo);
     float* vinfo = reinterpret_cast<float*>(smem + L::o_vinfo);
     float* xch = reinterpret_cast<float*>(smem + L::o_xch);
+    float* zx = reinterpret_cast<float*>(smem + L::o_zx);
     RingEntry* ring = reinterpret_cast<RingEntry*>(smem + L::o_ring4);
     const uint32_t bar0 = sbase + L::o_bar;
-    auto b_full = [&](int s) { return bar0 + 8 * s; };
-    auto b_empty = [&](int s) { return bar0 + 8 * (NST + s); };
-    auto b_kready = [&](int b) { return bar0 + 8 * (2 * NST + b); };
-    auto b_sfull = [&](int b) { return bar0 + 8 * (2 * NST + 2 + b); };
-    auto b_sfree = [&](int b) { return bar0 + 8 * (2 * NST + 4 + b); };
-    auto b_vready = [&](int b) { return bar0 + 8 * (2 * NST + 6 + b); };
-    auto b_pready = [&](int b) { return bar0 + 8 * (2 * NST + 8 + b); };
-    auto b_vfree = [&](int b) { return bar0 + 8 * (2 * NST + 10 + b); };
-    auto b_ofull = [&](int b) { return bar0 + 8 * (2 * NST + 12 + b); };
-    auto b_ofree = [&](int b) { return bar0 + 8 * (2 * NST + 14 + b); };
+    auto b_dfull = [&](int s) { return bar0 + 8 * s; };
+    auto b_dempty = [&](int s) { return bar0 + 8 * (NDESC + s); };
+    auto b_kready = [&](int b) { return bar0 + 8 * (2 * NDESC + b); };
+    auto b_sfull = [&](int b) { return bar0 + 8 * (2 * NDESC + 2 + b); };
+    auto b_sfree = [&](int b) { return bar0 + 8 * (2 * NDESC + 4 + b); };
+    auto b_vready = [&](int b) { return bar0 + 8 * (2 * NDESC + 6 + b); };
+    auto b_pready = [&](int b) { return bar0 + 8 * (2 * NDESC + 8 + b); };
+    auto b_vfree = [&](int b) { return bar0 + 8 * (2 * NDESC + 10 + b); };
+    auto b_ofull = [&](int b) { return bar0 + 8 * (2 * NDESC + 12 + b); };
+    auto b_ofree = [&](int b) { return bar0 + 8 * (2 * NDESC + 14 + b); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::o_tmem);
+    const bool tr = g_tr_on != 0 && blockIdx.x == 0;
+    auto TR = [&](int i, int f) {
+        if (tr && (threadIdx.x & 31) == 0 && i < kTrPages) g_tr[i * kTrFields + f] = gtimer();
+    };
 
-    // ---- setup: TMEM, barriers, constant tiles ----
+    // ---- setup: TMEM, barriers, zeroed B tiles ----
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "n"(L::kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(b_full(s), 1);
-            mbar_init(b_empty(s), 8);
+        for (int s = 0; s < NDESC; ++s) {
+            mbar_init(b_dfull(s), 1);
+            mbar_init(b_dempty(s), 8);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(b_kready(b), 4);
@@ -510,13 +596,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // A_ones (K = 32 rows of 4^j per permuted token row) and zeroed B tiles
-    for (int i = tid; i < 4096 / 16; i += kThreads) {
-        // byte (mchunk, k, r) at a_off(mchunk, k) + r; weight 4^(r / 4)
-        sts128(sbase + L::o_ones + 16 * i, 0x01010101u, 0x04040404u, 0x10101010u, 0x40404040u);
-    }
-    for (int i = tid; i < 2 * L::kBQK / 16; i += kThreads) sts128(sbase + L::o_bqk + 16 * i, 0u, 0u, 0u, 0u);
-    for (int i = tid; i < 2 * 128 * NP / 16; i += kThreads) sts128(sbase + L::o_bp + 16 * i, 0u, 0u, 0u, 0u);
+    for (int i = tid; i < 2 * 160 * NB / 16; i += kThreads) sts128(sbase + L::o_bqk + 16 * i, 0u, 0u, 0u, 0u);
+    for (int i = tid; i < 2 * 128 * NB / 16; i += kThreads) sts128(sbase + L::o_bp + 16 * i, 0u, 0u, 0u, 0u);
     if (tid < 4) ring[tid].tag = -1;
     fence_async_smem();
     tc_fence_before();
@@ -525,24 +606,56 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
     const uint32_t tmem = *tmem_slot;
 
     if (warp < 4) {
-        // ===================== WG-A: key pages -> operand tiles, B = q * (s | z) =====================
+        // ============ WG-A: key pages (global -> registers) -> u8 operand tile, B = q alpha s ============
         const int d = tid;  // channel
         float qa[GROUP];
+#pragma unroll
+        for (int g = 0; g < GROUP; ++g) qa[g] = 0.f;
         float qmax = 0.f;
-        for (int i = 0;; ++i) {
-            const int s = i % NST, b = i & 1;
-            mbar_wait(b_full(s), (i / NST) & 1);
-            const StageInfo si = sinfo[s];
+        int end_at = 0x7fffffff;
+        struct KR {
+            uint4 c0, c1;
+            uint32_t hb0, hb1, s16, z16, idx;
+            uint2 s4;
+            int unit, flags, slot;
+        };
+        // packed page -> registers, PF pages ahead of its conversion
+        auto kload = [&](KR& r, int i) {
+            if (i > end_at) {
+                r.flags = FL_END;
+                return;
+            }
+            mbar_wait(b_dfull(i % NDESC), (i / NDESC) & 1);
+            const PageDesc pd = *desc_ptr(i);
+            r.unit = pd.unit;
+            r.flags = pd.flags;
+            r.slot = pd.slot;
+            if (pd.flags & FL_END) {
+                end_at = i;
+                return;
+            }
+            const uint8_t* kp = pd.kp;
+            r.c0 = ldg_na128(kp + 32 * d);
+            r.c1 = ldg_na128(kp + 32 * d + 16);
+            r.hb0 = (d >> 3) < d_boost ? ldg32(kp + D * G / 4 + 32 * (d >> 3) + 4 * (d & 7)) : 0u;
+            r.hb1 = (d >> 3) + 16 < d_boost ? ldg32(kp + D * G / 4 + 32 * ((d >> 3) + 16) + 4 * (d & 7)) : 0u;
+            r.s4 = ldg64(kp + scale_off + 8 * lane);
+            r.s16 = ldg16(kp + scale_off + 2 * d);  // combined only at use: keeps the load in flight
+            r.z16 = ldg16(kp + zero_off + 2 * d);
+            r.idx = ldg8(kp + idx_off + d);
+        };
+        auto kproc = [&](KR& r, int i) -> bool {
+            const int b = i & 1;
             if (i >= 2) mbar_wait(b_sfree(b), ((i >> 1) - 1) & 1);
-            if (si.flags & FL_END) {
+            if (warp == 0) TR(i, 2);
+            if (r.flags & FL_END) {
                 if (d == 0) kinfo[b].flags = FL_END;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(b_kready(b));
-                break;
+                return false;
             }
-            const uint32_t kp = stage_k(s);
-            if (si.flags & FL_FIRST) {
-                const uint32_t qs = stage_q(s);
+            if (r.flags & FL_FIRST) {
+                const uint32_t qs = desc_q(i);
                 float mx = 0.f;
 #pragma unroll
                 for (int g = 0; g < GROUP; ++g) {
@@ -555,96 +668,82 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                 for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
                 qmax = mx * kAlpha;
             }
-            // per-page bounds: max scale, max |zero| over the 128 channels (every warp redundantly)
-            float smax, zmax;
-            {
-                const uint2 sv = lds64(kp + scale_off + 8 * lane);
-                const uint2 zv = lds64(kp + zero_off + 8 * lane);
-                const __half2 s2 = __hmax2(*reinterpret_cast<const __half2*>(&sv.x), *reinterpret_cast<const __half2*>(&sv.y));
-                const __half2 z2 = __hmax2(__habs2(*reinterpret_cast<const __half2*>(&zv.x)), __habs2(*reinterpret_cast<const __half2*>(&zv.y)));
-                __half2 m2 = __halves2half2(__hmax(__low2half(s2), __high2half(s2)), __hmax(__low2half(z2), __high2half(z2)));
-                uint32_t mu = *reinterpret_cast<uint32_t*>(&m2);
+            // page bound: max scale over the 128 channels (every warp redundantly)
+            float smax = hmax4(r.s4);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mu = hmax2(mu, __shfl_xor_sync(0xffffffffu, mu, o));
-                m2 = *reinterpret_cast<__half2*>(&mu);
-                smax = __low2float(m2);
-                zmax = __high2float(m2);
-            }
-            const float bx = 4.f * qmax * smax, bz = qmax * zmax;
-            const float invx = bx > 0.f ? kQuant / bx : 0.f, invz = bz > 0.f ? kQuant / bz : 0.f;
+            for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+            const float bx = 4.f * qmax * smax;
+            const float invx = bx > 0.f ? __fdividef((float)kQuant, bx) : 0.f;
+            if (warp == 0) TR(i, 10);
             const uint32_t ak = sbase + L::o_ak + b * kTileAK;
-            const uint32_t bq = sbase + L::o_bqk + b * L::kBQK;
-            // dense_low row d: 32 bytes = 128 tokens -> 128 u8 (code * 4^j), 8 MN chunks
+            const uint32_t bq = sbase + L::o_bqk + b * 160 * NB;
             {
-                const uint4 wa = lds128(kp + 32 * d), wb = lds128(kp + 32 * d + 16);
-                const uint32_t w[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+                const uint32_t w[8] = {r.c0.x, r.c0.y, r.c0.z, r.c0.w, r.c1.x, r.c1.y, r.c1.z, r.c1.w};
                 const uint32_t dst = ak + a_off(0, d);
 #pragma unroll
                 for (int i8 = 0; i8 < 8; ++i8) sts128(dst + 128 * i8, w[i8] & M0, w[i8] & M1, w[i8] & M2, w[i8] & M3);
             }
-            // high_bits rows (boosted channels) -> K rows 128 + r
-            for (int r = d >> 3; r < d_boost; r += 16) {
-                const uint32_t w = lds32(kp + D * G / 4 + 32 * r + 4 * (d & 7));
-                sts128(ak + a_off(d & 7, 128 + r), w & M0, w & M1, w & M2, w & M3);
-            }
-            // B rows: (lo, hi) of q alpha s_d per query, then of q alpha z_d
-            {
-                const float s_d = h2f(lds16(kp + scale_off + 2 * d));
-                const float z_d = h2f(lds16(kp + zero_off + 2 * d));
-                const float sx = s_d * invx, sz = z_d * invz;
-                uint32_t xw[GROUP > 1 ? GROUP / 2 : 1], zw[GROUP > 1 ? GROUP / 2 : 1];
+            if ((d >> 3) < d_boost)
+                sts128(ak + a_off(d & 7, 128 + (d >> 3)), r.hb0 & M0, r.hb0 & M1, r.hb0 & M2, r.hb0 & M3);
+            if ((d >> 3) + 16 < d_boost)
+                sts128(ak + a_off(d & 7, 144 + (d >> 3)), r.hb1 & M0, r.hb1 & M1, r.hb1 & M2, r.hb1 & M3);
+            if (warp == 0) TR(i, 11);
+            const float s_d = h2f(r.s16), z_d = h2f(r.z16);
+            const float sx = s_d * invx;
+            auto brow = [&](uint32_t addr, float f) {
+                int x[GROUP];
 #pragma unroll
-                for (int g = 0; g < GROUP; g += 2) {
-                    const int x0 = f2i(qa[g] * sx), z0 = f2i(qa[g] * sz);
-                    const int x1 = GROUP > 1 ? f2i(qa[g + 1 < GROUP ? g + 1 : g] * sx) : 0;
-                    const int z1 = GROUP > 1 ? f2i(qa[g + 1 < GROUP ? g + 1 : g] * sz) : 0;
-                    xw[g / 2] = GROUP > 1 ? enc_pair(x0, x1) : (enc16(x0) & 0xffffu);
-                    zw[g / 2] = GROUP > 1 ? enc_pair(z0, z1) : (enc16(z0) & 0xffffu);
-                }
-                const uint32_t row = bq + 16 * (d & 7) + 128 * NCH * (d >> 3);
-                if (GROUP == 8) {
-                    sts128(row, xw[0], xw[GROUP > 4 ? 1 : 0], xw[GROUP > 4 ? 2 : 0], xw[GROUP > 4 ? 3 : 0]);
-                    sts128(row + 128, zw[0], zw[GROUP > 4 ? 1 : 0], zw[GROUP > 4 ? 2 : 0], zw[GROUP > 4 ? 3 : 0]);
-                } else if (GROUP == 4) {
-                    sts128(row, xw[0], xw[GROUP > 2 ? 1 : 0], zw[0], zw[GROUP > 2 ? 1 : 0]);
-                } else {
-                    sts128(row, xw[0], 0u, zw[0], 0u);
-                }
-                const uint32_t bi = lds8(kp + idx_off + d);
-                if ((int)bi < d_boost) {
-                    const float s4 = 4.f * sx;
-                    uint32_t bw[GROUP > 1 ? GROUP / 2 : 1];
+                for (int g = 0; g < GROUP; ++g) x[g] = f2i(qa[g] * f);
+                if (GROUP == 8)
+                    sts128(addr, enc_pair(x[0], x[1 % GROUP]), enc_pair(x[2 % GROUP], x[3 % GROUP]),
+                           enc_pair(x[4 % GROUP], x[5 % GROUP]), enc_pair(x[6 % GROUP], x[7 % GROUP]));
+                else if (GROUP == 4)
+                    sts64(addr, enc_pair(x[0], x[1 % GROUP]), enc_pair(x[2 % GROUP], x[3 % GROUP]));
+                else if (GROUP == 2)
+                    sts32(addr, enc_pair(x[0], x[1 % GROUP]));
+                else
+                    sts32(addr, enc16(x[0]) & 0xffffu);
+            };
+            brow(bq + NB * d, sx);
+            if ((int)r.idx < d_boost) brow(bq + NB * (128 + (int)r.idx), 4.f * sx);
+            if (warp == 0) TR(i, 12);
+            // sum_d q alpha z_d in fp32: per-warp partials for the softmax warps
+            float zz[GROUP];
 #pragma unroll
-                    for (int g = 0; g < GROUP; g += 2) {
-                        const int x0 = f2i(qa[g] * s4);
-                        const int x1 = GROUP > 1 ? f2i(qa[g + 1 < GROUP ? g + 1 : g] * s4) : 0;
-                        bw[g / 2] = GROUP > 1 ? enc_pair(x0, x1) : (enc16(x0) & 0xffffu);
-                    }
-                    const int k = 128 + (int)bi;
-                    const uint32_t brow = bq + 16 * (k & 7) + 128 * NCH * (k >> 3);
-                    if (GROUP == 8)
-                        sts128(brow, bw[0], bw[GROUP > 4 ? 1 : 0], bw[GROUP > 4 ? 2 : 0], bw[GROUP > 4 ? 3 : 0]);
-                    else if (GROUP == 4)
-                        sts64(brow, bw[0], bw[GROUP > 2 ? 1 : 0]);
-                    else
-                        sts32(brow, bw[0]);
-                }
-            }
+            for (int g = 0; g < GROUP; ++g) zz[g] = qa[g] * z_d;
+            warp_sum_scatter<GROUP>(zz, lane);
+            if (scatter_owner<GROUP>(lane)) zx[(b * 4 + warp) * 8 + scatter_query<GROUP>(lane)] = zz[0];
+            if (warp == 0) TR(i, 13);
             if (d == 0) {
                 KInfo ki;
                 ki.stepx = bx / kQuant;
-                ki.stepz = bz / kQuant;
-                ki.flags = si.flags;
-                ki.unit = si.unit;
-                ki.slot = si.slot;
+                ki.flags = r.flags;
+                ki.unit = r.unit;
+                ki.slot = r.slot;
                 kinfo[b] = ki;
             }
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(b_kready(b));
-                mbar_arrive(b_empty(s));
+                mbar_arrive(b_dempty(i % NDESC));
             }
+            if (warp == 0) TR(i, 3);
+            return true;
+        };
+        KR r0, r1, r2, r3;
+        kload(r0, 0);
+        kload(r1, 1);
+        kload(r2, 2);
+        for (int i = 0;; i += 4) {
+            kload(r3, i + 3);
+            if (!kproc(r0, i)) break;
+            kload(r0, i + 4);
+            if (!kproc(r1, i + 1)) break;
+            kload(r1, i + 5);
+            if (!kproc(r2, i + 2)) break;
+            kload(r2, i + 6);
+            if (!kproc(r3, i + 3)) break;
         }
     } else if (warp < 8) {
         // ===================== WG-B: softmax (thread = TMEM lane = token) =====================
@@ -659,6 +758,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
             const uint32_t ph = (i >> 1) & 1;
             mbar_wait(b_sfull(b), ph);
             mbar_wait(b_kready(b), ph);
+            if (warp == 4) TR(i, 5);
             const KInfo ki = kinfo[b];
             if (ki.flags & FL_END) break;
             if (ki.flags & FL_FIRST) {
@@ -669,22 +769,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                     lz[g] = 0.f;
                 }
             }
+            float zg[GROUP];
+#pragma unroll
+            for (int g = 0; g < GROUP; ++g)
+                zg[g] = zx[(b * 4 + 0) * 8 + g] + zx[(b * 4 + 1) * 8 + g] + zx[(b * 4 + 2) * 8 + g] + zx[(b * 4 + 3) * 8 + g];
             tc_fence_after();
-            uint32_t xs[2 * GROUP], zs[2 * GROUP];
-            tmem_ld<2 * GROUP>(lane_base + b * 2 * NQK, xs);
-            tmem_ld<2 * GROUP>(lane_base + b * 2 * NQK + NQK + NX, zs);
+            uint32_t xs[2 * GROUP];
+            tmem_ld<2 * GROUP>(lane_base + b * 16, xs);
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(b_sfree(b));
-            const float fx = ki.stepx * wj, fz = ki.stepz * wj;
+            if (warp == 4) TR(i, 14);
+            const float fx = ki.stepx * wj;
             float lg[GROUP];
 #pragma unroll
-            for (int g = 0; g < GROUP; ++g) {
-                const int sx = (int)xs[2 * g] + 128 * (int)xs[2 * g + 1];
-                const int sz = (int)zs[2 * g] + 128 * (int)zs[2 * g + 1];
-                lg[g] = (float)sx * fx + (float)sz * fz;
-            }
+            for (int g = 0; g < GROUP; ++g) lg[g] = fmaf((float)((int)xs[2 * g] + 128 * (int)xs[2 * g + 1]), fx, zg[g]);
             // page max over the 128 tokens (f16x2 pairs), one named barrier
             constexpr int NPAIR = GROUP > 1 ? GROUP / 2 : 1;
             uint32_t hm[NPAIR];
@@ -694,7 +794,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
             for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
                 for (int k = 0; k < NPAIR; ++k) hm[k] = hmax2(hm[k], __shfl_xor_sync(0xffffffffu, hm[k], o));
-            float* xb = xch + (i & 1) * 4 * 16;
+            float* xb = xch + (i & 1) * 64;
             if (lane == 0)
 #pragma unroll
                 for (int k = 0; k < NPAIR; ++k) reinterpret_cast<uint32_t*>(xb)[wq * 4 + k] = hm[k];
@@ -704,18 +804,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                 const uint32_t* xu = reinterpret_cast<const uint32_t*>(xb);
                 hm[k] = hmax2(hmax2(xu[k], xu[4 + k]), hmax2(xu[8 + k], xu[12 + k]));
             }
+            if (warp == 4) TR(i, 15);
             float pm[GROUP];
 #pragma unroll
             for (int g = 0; g < GROUP; ++g) {
                 const __half2 h2 = *reinterpret_cast<const __half2*>(&hm[g / 2]);
                 pm[g] = (g & 1) ? __high2float(h2) : __low2float(h2);
             }
-            // vmeta of this page (s_t, z_t) + the P scale; B_P of page i - 2 consumed
             mbar_wait(b_vready(b), ph);
             if (i >= 2) mbar_wait(b_vfree(b), ((i >> 1) - 1) & 1);
             const float2 sz = *reinterpret_cast<const float2*>(smem + L::o_vmeta + b * 1024 + 8 * t);
-            const float invp = vinfo[b];
-            const float sc = sz.x * invp;
+            const float sc = sz.x * vinfo[b];
             float corr[GROUP];
             int xp[GROUP];
 #pragma unroll
@@ -728,17 +827,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                 mrun[g] = mn;
                 xp[g] = min(f2i(p * sc), 16383);
             }
-            const uint32_t prow = sbase + L::o_bp + b * 128 * NP + NP * t;
-            if (GROUP == 8) {
+            const uint32_t prow = sbase + L::o_bp + b * 128 * NB + NB * t;
+            if (GROUP == 8)
                 sts128(prow, enc_pair(xp[0], xp[1 % GROUP]), enc_pair(xp[2 % GROUP], xp[3 % GROUP]),
                        enc_pair(xp[4 % GROUP], xp[5 % GROUP]), enc_pair(xp[6 % GROUP], xp[7 % GROUP]));
-            } else if (GROUP == 4) {
+            else if (GROUP == 4)
                 sts64(prow, enc_pair(xp[0], xp[1 % GROUP]), enc_pair(xp[2 % GROUP], xp[3 % GROUP]));
-            } else if (GROUP == 2) {
+            else if (GROUP == 2)
                 sts32(prow, enc_pair(xp[0], xp[1 % GROUP]));
-            } else {
+            else
                 sts32(prow, enc16(xp[0]) & 0xffffu);
-            }
             RingEntry& re = ring[i & 3];
             if (ki.flags & FL_LAST) {
                 // item done: sum l, l_z over the 128 tokens; (m, l) -> partial, l_z -> correction warps
@@ -752,24 +850,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                 for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
                     for (int k = 0; k < 2 * GROUP; ++k) red[k] += __shfl_xor_sync(0xffffffffu, red[k], o);
-                float* xs2 = xch + 128;  // [4 warps][16]
+                float* xs2 = xch + 128;
                 if (lane == 0)
 #pragma unroll
                     for (int k = 0; k < 2 * GROUP; ++k) xs2[wq * 16 + k] = red[k];
                 named_sync(1, 128);
                 if (m == 0) {
-                    const int u = ki.unit;
-                    float* base = P.part + ((int64_t)u * P.nslot + ki.slot) * GROUP * (D + 2);
+                    float* base = P.part + ((int64_t)ki.unit * P.nslot + ki.slot) * part_stride(GROUP);
 #pragma unroll
                     for (int g = 0; g < GROUP; ++g) {
-                        const float lt = xs2[g] + xs2[16 + g] + xs2[32 + g] + xs2[48 + g];
-                        const float lzt = xs2[GROUP + g] + xs2[16 + GROUP + g] + xs2[32 + GROUP + g] + xs2[48 + GROUP + g];
                         base[GROUP * D + 2 * g] = mrun[g];
-                        base[GROUP * D + 2 * g + 1] = lt;
-                        re.lz[g] = lzt;
+                        base[GROUP * D + 2 * g + 1] = xs2[g] + xs2[16 + g] + xs2[32 + g] + xs2[48 + g];
+                        re.lz[g] = xs2[GROUP + g] + xs2[16 + GROUP + g] + xs2[32 + GROUP + g] + xs2[48 + GROUP + g];
                     }
                 }
-                named_sync(1, 128);  // xs2 reusable
+                named_sync(1, 128);
             }
             if (m == 0) {
 #pragma unroll
@@ -780,6 +875,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(b_pready(b));
+            if (warp == 4) TR(i, 6);
         }
     } else if (warp < 12) {
         // ===================== WG-C: value pages -> operand tiles; output correction =====================
@@ -791,15 +887,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
         float o[GROUP];
 #pragma unroll
         for (int g = 0; g < GROUP; ++g) o[g] = 0.f;
-        StageInfo prev;
-        prev.flags = 0;
-        float prev_step = 0.f;
+        int end_at = 0x7fffffff;
+        struct VR {
+            uint4 c0, c1;
+            uint32_t s16, z16;
+            uint2 s4;
+            int unit, flags, slot;
+        };
+        int pflags = 0, punit = 0, pslot = 0;
+        float pstep = 0.f;
         auto correct = [&](int j) {
             const int b = j & 1;
             mbar_wait(b_ofull(b), (j >> 1) & 1);
+            if (warp == 8) TR(j, 9);
             tc_fence_after();
             uint32_t ov[2 * GROUP];
-            tmem_ld<2 * GROUP>(lane_base + 4 * NQK + b * NP, ov);
+            tmem_ld<2 * GROUP>(lane_base + 32 + b * 16, ov);
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -808,14 +911,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
             while (*reinterpret_cast<volatile int*>(&re.tag) != j) {
             }
             __threadfence_block();
-            const float f = prev_step * wch;
+            const float f = pstep * wch;
 #pragma unroll
-            for (int g = 0; g < GROUP; ++g) {
-                const int v = (int)ov[2 * g] + 128 * (int)ov[2 * g + 1];
-                o[g] = fmaf(o[g], re.corr[g], (float)v * f);
-            }
-            if (prev.flags & FL_LAST) {
-                float* base = P.part + ((int64_t)prev.unit * P.nslot + prev.slot) * GROUP * (D + 2);
+            for (int g = 0; g < GROUP; ++g) o[g] = fmaf(o[g], re.corr[g], (float)((int)ov[2 * g] + 128 * (int)ov[2 * g + 1]) * f);
+            if (pflags & FL_LAST) {
+                float* base = P.part + ((int64_t)punit * P.nslot + pslot) * part_stride(GROUP);
 #pragma unroll
                 for (int g = 0; g < GROUP; ++g) {
                     base[g * D + ch] = o[g] + re.lz[g];
@@ -823,74 +923,100 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                 }
             }
         };
-        int i = 0;
-        for (;; ++i) {
-            const int s = i % NST, b = i & 1;
-            mbar_wait(b_full(s), (i / NST) & 1);
-            const StageInfo si = sinfo[s];
-            if (si.flags & FL_END) break;
+        auto vload = [&](VR& v, int i) {
+            if (i > end_at) {
+                v.flags = FL_END;
+                return;
+            }
+            mbar_wait(b_dfull(i % NDESC), (i / NDESC) & 1);
+            const PageDesc pd = *desc_ptr(i);
+            v.unit = pd.unit;
+            v.flags = pd.flags;
+            v.slot = pd.slot;
+            if (pd.flags & FL_END) {
+                end_at = i;
+                return;
+            }
+            const uint8_t* vp = pd.vp;
+            v.c0 = ldg_na128(vp + 32 * r);
+            v.c1 = ldg_na128(vp + 32 * r + 16);
+            v.s16 = ldg16(vp + G * D / 4 + 2 * r);
+            v.z16 = ldg16(vp + G * D / 4 + 2 * G + 2 * r);
+            v.s4 = ldg64(vp + G * D / 4 + 8 * lane);
+        };
+        auto vproc = [&](VR& v, int i) -> bool {
+            const int b = i & 1;
+            if (v.flags & FL_END) {
+                if (i >= 1) correct(i - 1);
+                return false;
+            }
             if (i >= 2) mbar_wait(b_vfree(b), ((i >> 1) - 1) & 1);
-            const uint32_t vp = stage_v(s);
             const uint32_t av = sbase + L::o_av + b * kTileA;
             {
-                const uint4 wa = lds128(vp + 32 * r), wb = lds128(vp + 32 * r + 16);
-                const uint32_t w[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+                const uint32_t w[8] = {v.c0.x, v.c0.y, v.c0.z, v.c0.w, v.c1.x, v.c1.y, v.c1.z, v.c1.w};
                 const uint32_t dst = av + a_off(0, r);
 #pragma unroll
                 for (int i8 = 0; i8 < 8; ++i8) sts128(dst + 128 * i8, w[i8] & M0, w[i8] & M1, w[i8] & M2, w[i8] & M3);
             }
-            const float s_t = h2f(lds16(vp + G * D / 4 + 2 * r));
-            const float z_t = h2f(lds16(vp + G * D / 4 + 2 * G + 2 * r));
-            *reinterpret_cast<float2*>(smem + L::o_vmeta + b * 1024 + 8 * r) = make_float2(s_t, z_t);
-            float smax;
-            {
-                const uint2 sv = lds64(vp + G * D / 4 + 8 * lane);
-                const __half2 s2 = __hmax2(*reinterpret_cast<const __half2*>(&sv.x), *reinterpret_cast<const __half2*>(&sv.y));
-                __half2 m2 = __halves2half2(__hmax(__low2half(s2), __high2half(s2)), __low2half(s2));
-                uint32_t mu = *reinterpret_cast<uint32_t*>(&m2);
+            *reinterpret_cast<float2*>(smem + L::o_vmeta + b * 1024 + 8 * r) = make_float2(h2f(v.s16), h2f(v.z16));
+            float smax = hmax4(v.s4);
 #pragma unroll
-                for (int o2 = 16; o2 > 0; o2 >>= 1) mu = hmax2(mu, __shfl_xor_sync(0xffffffffu, mu, o2));
-                m2 = *reinterpret_cast<__half2*>(&mu);
-                smax = __low2float(m2) * 1.125f;  // p <= 2^(f16 max rounding) < 1.125
-            }
-            const float invp = smax > 0.f ? kQuant / smax : 0.f;
+            for (int o2 = 16; o2 > 0; o2 >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o2));
+            smax *= 1.125f;  // p <= 2^(f16 max rounding) < 1.125
+            const float invp = smax > 0.f ? __fdividef((float)kQuant, smax) : 0.f;
             if (r == 0) vinfo[b] = invp;
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(b_vready(b));
-                mbar_arrive(b_empty(s));
+                mbar_arrive(b_dempty(i % NDESC));
             }
+            if (warp == 8) TR(i, 8);
             if (i >= 1) correct(i - 1);
-            prev = si;
-            prev_step = smax / kQuant;
+            pflags = v.flags;
+            punit = v.unit;
+            pslot = v.slot;
+            pstep = smax / kQuant;
+            return true;
+        };
+        VR v0, v1, v2, v3;
+        vload(v0, 0);
+        vload(v1, 1);
+        vload(v2, 2);
+        for (int i = 0;; i += 4) {
+            vload(v3, i + 3);
+            if (!vproc(v0, i)) break;
+            vload(v0, i + 4);
+            if (!vproc(v1, i + 1)) break;
+            vload(v1, i + 5);
+            if (!vproc(v2, i + 2)) break;
+            vload(v2, i + 6);
+            if (!vproc(v3, i + 3)) break;
         }
-        if (i >= 1) correct(i - 1);
     } else if (warp == 12) {
-        // ===================== TMA producer =====================
+        // ===================== scheduler: work items -> page descriptors =====================
         if (lane == 0) {
             const int units = P.units;
             const int nq0 = units * P.cmx[0], nq1 = units * P.cmx[1], nq2 = units * P.cmx[2];
             int tk = atomicAdd(P.ctr, 1);
             int it = 0;
             for (;;) {
-                // next non-empty page item
                 int u = 0, p0 = 0, p1 = 0, slot = 0;
                 bool have = false;
                 while (!have) {
-                    const int t = tk;
-                    if (t >= nq0 + nq1 + nq2) break;
+                    const int tt = tk;
+                    if (tt >= nq0 + nq1 + nq2) break;
                     tk = atomicAdd(P.ctr, 1);
                     int sect, idx;
-                    if (t < nq0) {
+                    if (tt < nq0) {
                         sect = 0;
-                        idx = t;
-                    } else if (t < nq0 + nq1) {
+                        idx = tt;
+                    } else if (tt < nq0 + nq1) {
                         sect = 1;
-                        idx = t - nq0;
+                        idx = tt - nq0;
                     } else {
                         sect = 2;
-                        idx = t - nq0 - nq1;
+                        idx = tt - nq0 - nq1;
                     }
                     const int chn = idx / units;
                     u = idx - chn * units;
@@ -904,40 +1030,40 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                         for (int l2 = 0; l2 < sect; ++l2) slot += P.cmx[l2];
                     }
                 }
-                const int s = it % NST;
-                if (it >= NST) mbar_wait(b_empty(s), ((it / NST) - 1) & 1);
-                if (!have) {
-                    sinfo[s].flags = FL_END;
-                    mbar_arrive(b_full(s));
-                    break;
-                }
                 const int b_ = u / c.cfg.h_kv, h_ = u - b_ * c.cfg.h_kv;
                 const uint16_t* qsrc = P.q + ((int64_t)b_ * c.cfg.h_q + (int64_t)h_ * GROUP) * D;
-                for (int p = p0; p < p1; ++p) {
-                    const int st = it % NST;
-                    if (p > p0 && it >= NST) mbar_wait(b_empty(st), ((it / NST) - 1) & 1);
-                    StageInfo si;
-                    si.unit = u;
-                    si.page = p;
-                    si.flags = (p == p0 ? FL_FIRST : 0) | (p == p1 - 1 ? FL_LAST : 0);
-                    si.slot = slot;
-                    sinfo[st] = si;
-                    const uint8_t* ks = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * kslot;
-                    const uint8_t* vs = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * vslot;
-                    const uint32_t qbytes = p == p0 ? GROUP * D * 2 : 0;
-                    mbar_expect_tx(b_full(st), kslot + vslot + qbytes);
-                    bulk_g2s(stage_k(st), ks, kslot, b_full(st));
-                    bulk_g2s(stage_v(st), vs, vslot, b_full(st));
-                    if (qbytes) bulk_g2s(stage_q(st), qsrc, qbytes, b_full(st));
+                const int n_pages = have ? p1 - p0 : 1;
+                for (int k = 0; k < n_pages; ++k) {
+                    const int s = it % NDESC;
+                    if (it >= NDESC) mbar_wait(b_dempty(s), ((it / NDESC) - 1) & 1);
+                    PageDesc* pd = reinterpret_cast<PageDesc*>(smem + L::o_desc + s * L::kDesc);
+                    if (!have) {
+                        pd->flags = FL_END;
+                        mbar_arrive(b_dfull(s));
+                        break;
+                    }
+                    const int p = p0 + k;
+                    pd->kp = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes;
+                    pd->vp = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes;
+                    pd->unit = u;
+                    pd->flags = (p == p0 ? FL_FIRST : 0) | (p == p1 - 1 ? FL_LAST : 0);
+                    pd->slot = slot;
+                    if (p == p0) {
+                        mbar_expect_tx(b_dfull(s), GROUP * D * 2);
+                        bulk_g2s(desc_q(s), qsrc, GROUP * D * 2, b_dfull(s));
+                    } else {
+                        mbar_arrive(b_dfull(s));
+                    }
+                    TR(it, 0);
                     ++it;
                 }
+                if (!have) break;
             }
         }
     } else if (warp == 13) {
         // ===================== MMA issuer =====================
         if (lane == 0) {
-            constexpr uint32_t id_qk = idesc_i8(NQK), id_pv = idesc_i8(NP);
-            const uint32_t ones = sbase + L::o_ones;
+            constexpr uint32_t id = idesc_i8(NB);
             const int nkb = d_boost > 0 ? 1 : 0;
             auto issue_pv = [&](int j) {
                 const int b = j & 1;
@@ -947,12 +1073,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                 if (j >= 2) mbar_wait(b_ofree(b), ((j >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t av = sbase + L::o_av + b * kTileA;
-                const uint32_t bp = sbase + L::o_bp + b * 128 * NP;
+                const uint32_t bp = sbase + L::o_bp + b * 128 * NB;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    umma_i8(tmem + 4 * NQK + b * NP, sdesc(av + 4096 * k, 1024, 128), sdesc(bp + 512 * k, 128, 128), id_pv, k > 0);
+                    umma_i8(tmem + 32 + b * 16, sdesc(av + 4096 * k, 1024, 128), sdesc(bp + 512 * k, 128, 128), id, k > 0);
                 umma_commit(b_ofull(b));
                 umma_commit(b_vfree(b));
+                TR(j, 7);
             };
             int i = 0;
             for (;; ++i) {
@@ -961,17 +1088,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_attention_kernel(Params P) {
                 if (kinfo[b].flags & FL_END) break;
                 tc_fence_after();
                 const uint32_t ak = sbase + L::o_ak + b * kTileAK;
-                const uint32_t bq = sbase + L::o_bqk + b * L::kBQK;
-                const uint32_t d1 = tmem + b * 2 * NQK, d2 = d1 + NQK;
+                const uint32_t bq = sbase + L::o_bqk + b * 160 * NB;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    umma_i8(d1, sdesc(ak + 4096 * k, 1024, 128), sdesc(bq + 4 * 128 * NCH * k, 128 * NCH, 128), id_qk, k > 0);
-                if (nkb)
-                    umma_i8(d1, sdesc(ak + 4096 * 4, 1024, 128), sdesc(bq + 4 * 128 * NCH * 4, 128 * NCH, 128), id_qk, 1);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    umma_i8(d2, sdesc(ones, 1024, 128), sdesc(bq + 4 * 128 * NCH * k, 128 * NCH, 128), id_qk, k > 0);
+                    umma_i8(tmem + b * 16, sdesc(ak + 4096 * k, 1024, 128), sdesc(bq + 512 * k, 128, 128), id, k > 0);
+                if (nkb) umma_i8(tmem + b * 16, sdesc(ak + 4096 * 4, 1024, 128), sdesc(bq + 512 * 4, 128, 128), id, 1);
                 umma_commit(b_sfull(b));
+                TR(i, 4);
                 if (i >= 1) issue_pv(i - 1);
             }
             if (i >= 1) issue_pv(i - 1);
@@ -1032,7 +1155,7 @@ __global__ void __launch_bounds__(GROUP * 128) combine_kernel(Params P) {
         nch[lv] = (n + P.cs[lv] - 1) / P.cs[lv];
     }
     const int nparts = nfc + nch[0] + nch[1] + nch[2];
-    constexpr int kStride = GROUP * (D + 2);
+    constexpr int kStride = part_stride(GROUP);
     const float* pb = P.part + (int64_t)u * P.nslot * kStride;
     auto part_ptr = [&](int i) {
         int slot;
@@ -1120,7 +1243,7 @@ static int num_sms() {
     return sms;
 }
 
-bool fast_attention_supported(const KittyCacheDesc& c) {
+bool tc_attention_supported(const KittyCacheDesc& c) {
     const int group = c.cfg.h_q / c.cfg.h_kv;
     return c.cfg.d == D && c.cfg.g == G && c.cfg.key_bits == 2 && c.cfg.value_bits == 2 &&
            (group == 1 || group == 2 || group == 4 || group == 8) && c.cfg.d_boost <= 32 &&
@@ -1153,12 +1276,12 @@ static TcPlan plan(const KittyCacheDesc& c, int max_tokens) {
     if (p.fmax < 1) p.fmax = 1;
     p.nslot = p.fmax + p.cmx[0] + p.cmx[1] + p.cmx[2];
     p.ctr_bytes = 256;
-    p.part_bytes = (size_t)p.units * p.nslot * p.group * (D + 2) * sizeof(float);
+    p.part_bytes = (size_t)p.units * p.nslot * part_stride(p.group) * sizeof(float);
     return p;
 }
 
-size_t fast_attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
-    if (!fast_attention_supported(c)) return 0;
+size_t tc_attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
+    if (!tc_attention_supported(c)) return 0;
     const TcPlan p = plan(c, max_tokens);
     return p.ctr_bytes + p.part_bytes;
 }
@@ -1169,15 +1292,15 @@ static cudaError_t launch_t(const Params& prm, cudaStream_t st) {
     const int sm = Smem<GROUP>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    kfn<<<num_sms(), kThreads, sm, st>>>(prm);
+    kfn<<<num_sms() * kCtasPerSm, kThreads, sm, st>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     combine_kernel<GROUP><<<prm.units, GROUP * 128, 0, st>>>(prm);
     return cudaGetLastError();
 }
 
-cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, void* out, int out_dtype,
-                                  int max_tokens, void* ws, size_t ws_bytes, cudaStream_t st) {
+cudaError_t launch_tc_attention(const KittyCacheDesc& c, const uint16_t* q, void* out, int out_dtype,
+                                int max_tokens, void* ws, size_t ws_bytes, cudaStream_t st) {
     const TcPlan p = plan(c, max_tokens);
     if (ws_bytes < p.ctr_bytes + p.part_bytes) return cudaErrorInvalidValue;
     Params prm;
@@ -1202,6 +1325,11 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     }
 }
 
-cudaError_t fast_attention_trace(int, long long*, int) { return cudaSuccess; }
+cudaError_t tc_attention_trace(int enable, long long* host_out, int max_rows) {
+    cudaError_t e = cudaMemcpyToSymbol(tcattn::g_tr_on, &enable, sizeof(int));
+    if (e != cudaSuccess || host_out == nullptr) return e;
+    const int n = max_rows < tcattn::kTrPages ? max_rows : tcattn::kTrPages;
+    return cudaMemcpyFromSymbol(host_out, tcattn::g_tr, sizeof(long long) * n * tcattn::kTrFields);
+}
 
 }  // namespace kitty

@@ -220,8 +220,17 @@ def _c1_like(rng, b, h_kv, h_q, n, d=128):
     return _bf16(k), _bf16(v), _bf16(q)
 
 
-@pytest.mark.parametrize("n,group", [(4096, 4), (1000, 8), (160, 4), (33, 4), (290, 8)])
-def test_batched_attention_default_shape_vs_oracle(cuda, n, group):
+@pytest.fixture(params=["default", "tc"])
+def kernel(request, cuda):
+    """Both decode-attention kernels: the default dispatch (mma.sync kernel for
+    GQA groups <= 4, tcgen05 for group 8) and the tcgen05 kernel everywhere."""
+    cuda.select_attention_kernel(request.param)
+    yield request.param
+    cuda.select_attention_kernel("default")
+
+
+@pytest.mark.parametrize("n,group", [(4096, 4), (1000, 8), (160, 4), (33, 4), (290, 8), (700, 1), (1500, 2)])
+def test_batched_attention_default_shape_vs_oracle(cuda, kernel, n, group):
     # C1 (1 seq, 8 kv / 32 q, 4K) and ragged-page lengths; bf16 out, max-abs <= 1e-2
     rng = np.random.default_rng(n + group)
     b, h_kv = 2, 8 if n == 4096 else 2
@@ -245,7 +254,7 @@ def test_batched_attention_default_shape_vs_oracle(cuda, n, group):
         assert np.max(np.abs(out[bi] - oc16.attend(q[bi]))) <= 1e-2
 
 
-def test_decode_loop_matches_oracle(cuda):
+def test_decode_loop_matches_oracle(cuda, kernel):
     # simulate-decode (cli.py:304-315) on the device: prompt, then steps of
     # append + attend, crossing key and value pack boundaries
     rng = np.random.default_rng(77)

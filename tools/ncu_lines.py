@@ -1,0 +1,77 @@
+"""Attribute an ncu source-page capture (SASS) to CUDA source lines and to
+warp-role line ranges, using nvdisasm line info of the built object.
+
+    python tools/ncu_lines.py REP.ncu-rep OBJ.o KERNEL_MANGLED [role=a-b ...]
+"""
+import csv
+import io
+import os
+import re
+import subprocess
+import sys
+import tempfile
+from collections import defaultdict
+
+
+def line_map(obj, func):
+    tmp = tempfile.mkdtemp()
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, capture_output=True, check=True)
+    cubin = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
+    out = subprocess.run(["nvdisasm", "--print-line-info", os.path.join(tmp, cubin)], capture_output=True, text=True).stdout
+    m, cur, inside = {}, None, False
+    for ln in out.splitlines():
+        if ln.startswith(".text."):
+            inside = ln.strip().rstrip(":") == ".text." + func
+            continue
+        if not inside:
+            continue
+        g = re.search(r'line (\d+)', ln) if "//##" in ln else None
+        if g:
+            cur = int(g.group(1))
+            continue
+        a = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+        if a and cur is not None:
+            m[int(a.group(1), 16)] = cur
+    return m
+
+
+def main(rep, obj, func, *roles):
+    lm = line_map(obj, func)
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[1]
+    idx = {k: i for i, k in enumerate(hdr)}
+    base = None
+    per_line = defaultdict(lambda: [0, 0])
+    for r in rows[2:]:
+        if len(r) < len(hdr) or not r[0].startswith("0x"):
+            continue
+        addr = int(r[0], 16)
+        base = addr if base is None else base
+        off = addr - base
+        line = lm.get(off, -1)
+        per_line[line][0] += int(r[idx["Warp Stall Sampling (All Samples)"]] or 0)
+        per_line[line][1] += int(r[idx["Instructions Executed"]] or 0)
+    tot_s = sum(v[0] for v in per_line.values())
+    tot_i = sum(v[1] for v in per_line.values())
+    spans = []
+    for rr in roles:
+        name, ab = rr.split("=")
+        a, b = (int(x) for x in ab.split("-"))
+        spans.append((name, a, b))
+    agg = defaultdict(lambda: [0, 0])
+    for line, (s, n) in per_line.items():
+        name = next((nm for nm, a, b in spans if a <= line <= b), "other")
+        agg[name][0] += s
+        agg[name][1] += n
+    print(f"{'role':12s} {'stall samples':>14s} {'%':>6s} {'warp-instr':>12s} {'%':>6s}")
+    for name, (s, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+        print(f"{name:12s} {s:14d} {100 * s / max(tot_s, 1):6.1f} {n:12d} {100 * n / max(tot_i, 1):6.1f}")
+    print("\ntop lines by samples:")
+    for line, (s, n) in sorted(per_line.items(), key=lambda kv: -kv[1][0])[:40]:
+        print(f"  line {line:5d}  samples {s:8d} ({100 * s / max(tot_s, 1):5.1f}%)  instr {n:10d}")
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
