@@ -25,6 +25,9 @@
 //  * warp-shuffle online softmax in the log2 domain; partials (m, l, acc) per
 //    item go to the workspace and the last item of a unit merges them (LSE)
 //    and writes the bf16/f32 output -- no separate combine launch.
+#include <cstdio>
+#include <cstdlib>
+
 #include "kitty_attention.cuh"
 #include "kitty_codec.cuh"
 
@@ -299,8 +302,16 @@ struct UnitGeom {
 // [0, vp/2) in chunks of cs[0], [vp/2, 4vp/5) in cs[1], [4vp/5, vp) in 1-page
 // chunks; the queue serves level 0 (interleaved with the fp chunks) first, so
 // it drains in small pieces and no SM idles behind a long item.
+// level boundaries as per-mille of vp (tuning knobs, set once by the host plan)
+__constant__ int c_lvl[2] = {500, 800};
+static int h_lvl[2] = {500, 800};
 __host__ __device__ __forceinline__ int level_begin(int lv, int vp) {
-    return lv == 0 ? 0 : (lv == 1 ? vp / 2 : (lv == 2 ? (vp * 4) / 5 : vp));
+#ifdef __CUDA_ARCH__
+    const int* lvl = c_lvl;
+#else
+    const int* lvl = h_lvl;
+#endif
+    return lv == 0 ? 0 : (lv == 1 ? (vp * lvl[0]) / 1000 : (lv == 2 ? (vp * lvl[1]) / 1000 : vp));
 }
 
 __device__ __forceinline__ UnitGeom unit_geom(const KittyCacheDesc& c, int u) {
@@ -1075,12 +1086,20 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     const int maxp = past / G + 1;
     const long long pages = (long long)p.units * maxp;
     const long long warps = (long long)num_sms() * kCtasPerSm * kWarps;
+    static int ppc_max = 8, cs1_div = 4, inited = 0;
+    if (!inited) {
+        inited = 1;
+        if (const char* e = getenv("KITTY_SCHED")) {  // experiments: "l1,l2,ppc_max,cs1_div"
+            sscanf(e, "%d,%d,%d,%d", &h_lvl[0], &h_lvl[1], &ppc_max, &cs1_div);
+            cudaMemcpyToSymbol(c_lvl, h_lvl, sizeof(h_lvl));
+        }
+    }
     int ppc = static_cast<int>(pages / (2 * warps));
-    ppc = ppc < 1 ? 1 : (ppc > 8 ? 8 : ppc);
+    ppc = ppc < 1 ? 1 : (ppc > ppc_max ? ppc_max : ppc);
     p.ppc = ppc;
     p.cmax = (maxp + ppc - 1) / ppc;
     p.cs[0] = ppc;
-    p.cs[1] = ppc / 4 > 1 ? ppc / 4 : 1;
+    p.cs[1] = ppc / cs1_div > 1 ? ppc / cs1_div : 1;
     p.cs[2] = 1;
     for (int lv = 0; lv < 3; ++lv) {
         const int n = level_begin(lv + 1, maxp) - level_begin(lv, maxp) + 2;
