@@ -37,7 +37,7 @@ torch.cuda.synchronize()
 lib = kb.load_library()
 lib.kitty_debug_tc_trace.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
 lib.kitty_debug_select_attention(1)
-buf = np.zeros((512, 16), np.int64)
+buf = np.zeros((512, 24), np.int64)
 lib.kitty_debug_tc_trace(1, None, 0)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
@@ -51,14 +51,14 @@ n = int(valid.sum())
 t0 = buf[valid][:, 0].min()
 r = np.where(buf > 0, buf - t0, -1)
 print(f"CTA 0 pages: {n}, last event at {r.max() / 1e3:.1f} us")
-names = ["tma", "A.full", "A.sfree", "A.kready", "mma.qk", "B.sfull", "B.pready", "mma.pv", "C.vready", "C.ofull", "A.bound", "A.conv", "A.brow", "A.fence", "B.tmld", "B.max"]
-print("page " + " ".join(f"{x:>9s}" for x in names))
+names = ["tma", "A.full", "A.sfree", "A.kready", "mma.qk", "B.sfull", "B.pready", "mma.pv", "C.vready", "C.ofull", "A.bound", "A.conv", "A.brow", "A.fence", "B.tmld", "B.max", "B.vready", "B.vfree", "B.sts", "B.ring", "B.fence"]
+print("page " + " ".join(f"{x:>9s}" for x in names[:16]))
 for i in list(range(min(args.rows, n))) + list(range(max(args.rows, n - 10), n)):
-    print(f"{i:4d} " + " ".join(f"{x / 1e3:9.2f}" for x in r[i]))
+    print(f"{i:4d} " + " ".join(f"{x / 1e3:9.2f}" for x in r[i][:16]))
 d = np.diff(r[:n], axis=0)
-print("median per-page delta (us): " + " ".join(f"{np.median(d[:, f]) / 1e3:.3f}" for f in range(16)))
+print("median per-page delta (us): " + " ".join(f"{np.median(d[:, f]) / 1e3:.3f}" for f in range(21)))
 lat = lambda a, b: np.median(r[:n, b] - r[:n, a]) / 1e3
 print(f"median latencies (us): tma->A.full {lat(0, 1):.2f}  A.full->A.kready {lat(1, 3):.2f}  A.kready->qk {lat(3, 4):.2f}  "
       f"qk->B.sfull {lat(4, 5):.2f}  B.sfull->pready {lat(5, 6):.2f}  pready->pv {lat(6, 7):.2f}  pv->C.ofull {lat(7, 9):.2f}")
 print(f"WG-A: sfree->bound {lat(2, 10):.3f} bound->conv-done {lat(10, 11):.3f} conv->brow-done {lat(11, 12):.3f} brow->zsum-done {lat(12, 13):.3f} zsum->kready {lat(13, 3):.3f}")
-print(f"WG-B: sfull->tmld {lat(5, 14):.3f} tmld->max {lat(14, 15):.3f} max->pready {lat(15, 6):.3f}")
+print(f"WG-B: sfull->tmld {lat(5, 14):.3f} tmld->max {lat(14, 15):.3f} max->vready {lat(15, 16):.3f} vready->vfree {lat(16, 17):.3f} vfree->sts {lat(17, 18):.3f} sts->ring {lat(18, 19):.3f} ring->fence {lat(19, 20):.3f} fence->pready {lat(20, 6):.3f}")
