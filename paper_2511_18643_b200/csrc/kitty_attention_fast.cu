@@ -29,6 +29,7 @@
 #include <cstdlib>
 
 #include "kitty_attention.cuh"
+#include "kitty_combine.cuh"
 #include "kitty_codec.cuh"
 
 namespace kitty {
@@ -120,11 +121,18 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
         : "memory");
 }
 
+// Pages are read once per step: stream them through L2 with evict_first so the
+// split-KV partials (re-read by the combine right after) stay resident.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first())
         : "memory");
 }
 
@@ -365,8 +373,12 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     sm.ones[lane + 32] = kOnes;
     __syncwarp();
     const Consts kc;
-    const bool trace = (g_trace_on & 1) != 0;
-    const bool noload = (g_trace_on & 2) != 0;
+#ifndef KITTY_TRACE
+#define KITTY_TRACE 0
+#endif
+    // tracing is compiled in only with -DKITTY_TRACE=1 (the timer reads cost ~30 instructions / page)
+    const bool trace = KITTY_TRACE && (g_trace_on & 1) != 0;
+    const bool noload = KITTY_TRACE && (g_trace_on & 2) != 0;
     long long tr_t0 = trace ? gtimer() : 0, tr_fp = 0, tr_merge = 0, tr_wait = 0;
     int tr_nfp = 0, tr_npages = 0, tr_nmerge = 0;
 
@@ -453,6 +465,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 
     // per-unit query state: B fragments of q*alpha (f16x2) for this lane's column
     int cur_unit = -1;
+    const uint16_t* q_cur = P.q;  // q rows of cur_unit (no per-page division)
     auto q_row = [&](int u, int g) {
         const int b = u / hkv, h = u - b * hkv;
         return P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g) * D;
@@ -460,6 +473,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     auto load_unit = [&](int u) {
         if (u == cur_unit) return;
         cur_unit = u;
+        q_cur = q_row(u, 0);
         const int col = gid & 3;
         const uint16_t* qg = q_row(u, col < GROUP ? col : 0);
         uint32_t qa[8][2];
@@ -687,7 +701,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
         if (NKH > 0) {
             const int col = gid & 3;
-            const uint16_t* qg = q_row(cur_unit, col < GROUP ? col : 0);
+            const uint16_t* qg = q_cur + (col < GROUP ? col : 0) * D;
 #pragma unroll
             for (int hk = 0; hk < NKH; ++hk) {
                 const int j0 = 16 * hk + 2 * tig;
@@ -957,13 +971,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 // CTA per unit, 4 warps per query row, each warp over a quarter of the parts;
 // loads are independent so the merge is one or two L2 round trips deep.
 template <int GROUP>
-__global__ void __launch_bounds__(GROUP * 128) combine_parts_kernel(Params P) {
-    constexpr int kSub = 4;  // warps per query row
-    __shared__ float sm_m[GROUP][kSub], sm_l[GROUP][kSub];
-    __shared__ float4 sm_acc[GROUP][kSub][32];
-    const int u = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = warp / kSub, sub = warp % kSub;
+__global__ void __launch_bounds__(kMergeWarps * 32) combine_parts_kernel(Params P) {
+    const int u = blockIdx.x / GROUP, g = blockIdx.x - (blockIdx.x / GROUP) * GROUP;
     const KittyCacheDesc& c = P.c;
     const UnitGeom gm = unit_geom(c, u);
     if (gm.n == 0) return;
@@ -975,78 +984,15 @@ __global__ void __launch_bounds__(GROUP * 128) combine_parts_kernel(Params P) {
     }
     const int nparts = nfc + nch[0] + nch[1] + nch[2];
     constexpr int kStride = part_stride(GROUP);
-    const float* pb = P.part + (int64_t)u * P.nslot * kStride;
-    auto part_ptr = [&](int i) {
-        int slot;
-        if (i < nfc) slot = i;
-        else if (i < nfc + nch[0]) slot = P.fmax + (i - nfc);
-        else if (i < nfc + nch[0] + nch[1]) slot = P.fmax + P.cmx[0] + (i - nfc - nch[0]);
-        else slot = P.fmax + P.cmx[0] + P.cmx[1] + (i - nfc - nch[0] - nch[1]);
-        return pb + (int64_t)slot * kStride;
+    auto slot_of = [&](int i) {
+        if (i < nfc) return i;
+        if (i < nfc + nch[0]) return P.fmax + (i - nfc);
+        if (i < nfc + nch[0] + nch[1]) return P.fmax + P.cmx[0] + (i - nfc - nch[0]);
+        return P.fmax + P.cmx[0] + P.cmx[1] + (i - nfc - nch[0] - nch[1]);
     };
-    // global max of the row over all parts
-    float M = -INFINITY;
-    for (int i = lane; i < nparts; i += 32) M = fmaxf(M, __ldcg(part_ptr(i) + GROUP * D + 2 * g));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    // this warp's share of the parts: i = sub, sub + 4, ...
-    float L = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i0 = sub; i0 < nparts; i0 += kSub * 8) {
-        float4 a[8];
-        float w[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int i = i0 + kSub * j;
-            if (i < nparts) {
-                const float* pi = part_ptr(i);
-                a[j] = __ldcg(reinterpret_cast<const float4*>(pi + g * D) + lane);
-                const float mi = __ldcg(pi + GROUP * D + 2 * g);
-                const float li = __ldcg(pi + GROUP * D + 2 * g + 1);
-                w[j] = mi == -INFINITY ? 0.f : ex2(mi - M);
-                L = fmaf(w[j], li, L);
-            } else {
-                a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-                w[j] = 0.f;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            acc.x = fmaf(w[j], a[j].x, acc.x);
-            acc.y = fmaf(w[j], a[j].y, acc.y);
-            acc.z = fmaf(w[j], a[j].z, acc.z);
-            acc.w = fmaf(w[j], a[j].w, acc.w);
-        }
-    }
-    sm_acc[g][sub][lane] = acc;
-    if (lane == 0) sm_l[g][sub] = L;
-    __syncthreads();
-    if (sub == 0) {
-        float4 o = sm_acc[g][0][lane];
-        float Lt = sm_l[g][0];
-#pragma unroll
-        for (int k = 1; k < kSub; ++k) {
-            const float4 x = sm_acc[g][k][lane];
-            o.x += x.x;
-            o.y += x.y;
-            o.z += x.z;
-            o.w += x.w;
-            Lt += sm_l[g][k];
-        }
-        const float inv = 1.f / Lt;
-        const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
-        const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
-        if (P.out_dtype == KITTY_F32) {
-            reinterpret_cast<float4*>(static_cast<float*>(P.out) + row * D)[lane] =
-                make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
-        } else {
-            uint2 v;
-            v.x = f32_to_bf16_bits(o.x * inv) | (f32_to_bf16_bits(o.y * inv) << 16);
-            v.y = f32_to_bf16_bits(o.z * inv) | (f32_to_bf16_bits(o.w * inv) << 16);
-            reinterpret_cast<uint2*>(static_cast<uint16_t*>(P.out) + row * D)[lane] = v;
-        }
-    }
-    (void)sm_m;
+    const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
+    const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
+    lse_merge_row<GROUP>(P.part + (int64_t)u * P.nslot * kStride, kStride, nparts, slot_of, g, P.out, P.out_dtype, row);
 }
 
 }  // namespace fastattn
@@ -1129,7 +1075,7 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     kfn<<<grid, kWarps * 32, sm, st>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    combine_parts_kernel<GROUP><<<prm.units, GROUP * 128, 0, st>>>(prm);
+    combine_parts_kernel<GROUP><<<prm.units * GROUP, kMergeWarps * 32, 0, st>>>(prm);
     return cudaGetLastError();
 }
 

@@ -35,6 +35,7 @@
 // Every item writes a partial (acc, m, l) per query row; combine_kernel merges
 // a unit's partials (log-sum-exp) and writes the bf16 / f32 output.
 #include "kitty_attention.cuh"
+#include "kitty_combine.cuh"
 #include "kitty_codec.cuh"
 
 namespace kitty {
@@ -119,7 +120,7 @@ struct Params {
 
 // ---- optional event trace of CTA 0 (kitty_debug_attention_trace) ----
 constexpr int kTrPages = 512;
-constexpr int kTrFields = 16;
+constexpr int kTrFields = 24;
 __device__ long long g_tr[kTrPages * kTrFields];
 __device__ int g_tr_on;
 __device__ __forceinline__ long long gtimer() {
@@ -812,7 +813,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tc_attention_kernel(Para
                 pm[g] = (g & 1) ? __high2float(h2) : __low2float(h2);
             }
             mbar_wait(b_vready(b), ph);
+            if (warp == 4) TR(i, 16);
             if (i >= 2) mbar_wait(b_vfree(b), ((i >> 1) - 1) & 1);
+            if (warp == 4) TR(i, 17);
             const float2 sz = *reinterpret_cast<const float2*>(smem + L::o_vmeta + b * 1024 + 8 * t);
             const float sc = sz.x * vinfo[b];
             float corr[GROUP];
@@ -837,6 +840,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tc_attention_kernel(Para
                 sts32(prow, enc_pair(xp[0], xp[1 % GROUP]));
             else
                 sts32(prow, enc16(xp[0]) & 0xffffu);
+            if (warp == 4) TR(i, 18);
             RingEntry& re = ring[i & 3];
             if (ki.flags & FL_LAST) {
                 // item done: sum l, l_z over the 128 tokens; (m, l) -> partial, l_z -> correction warps
@@ -872,8 +876,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tc_attention_kernel(Para
                 __threadfence_block();
                 *reinterpret_cast<volatile int*>(&re.tag) = i;
             }
+            if (warp == 4) TR(i, 19);
             fence_async_smem();
             __syncwarp();
+            if (warp == 4) TR(i, 20);
             if (lane == 0) mbar_arrive(b_pready(b));
             if (warp == 4) TR(i, 6);
         }
@@ -1138,13 +1144,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tc_attention_kernel(Para
 // Log-sum-exp merge of a unit's partials (fp chunks + page chunks).  One CTA
 // per unit, 4 warps per query row, each warp over a quarter of the parts.
 template <int GROUP>
-__global__ void __launch_bounds__(GROUP * 128) combine_kernel(Params P) {
-    constexpr int kSub = 4;
-    __shared__ float sm_l[GROUP][kSub];
-    __shared__ float4 sm_acc[GROUP][kSub][32];
-    const int u = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = warp / kSub, sub = warp % kSub;
+__global__ void __launch_bounds__(kMergeWarps * 32) combine_kernel(Params P) {
+    const int u = blockIdx.x / GROUP, g = blockIdx.x - (blockIdx.x / GROUP) * GROUP;
     const KittyCacheDesc& c = P.c;
     const UnitGeom gm = unit_geom(c, u);
     if (gm.n == 0) return;
@@ -1156,74 +1157,15 @@ __global__ void __launch_bounds__(GROUP * 128) combine_kernel(Params P) {
     }
     const int nparts = nfc + nch[0] + nch[1] + nch[2];
     constexpr int kStride = part_stride(GROUP);
-    const float* pb = P.part + (int64_t)u * P.nslot * kStride;
-    auto part_ptr = [&](int i) {
-        int slot;
-        if (i < nfc) slot = i;
-        else if (i < nfc + nch[0]) slot = P.fmax + (i - nfc);
-        else if (i < nfc + nch[0] + nch[1]) slot = P.fmax + P.cmx[0] + (i - nfc - nch[0]);
-        else slot = P.fmax + P.cmx[0] + P.cmx[1] + (i - nfc - nch[0] - nch[1]);
-        return pb + (int64_t)slot * kStride;
+    auto slot_of = [&](int i) {
+        if (i < nfc) return i;
+        if (i < nfc + nch[0]) return P.fmax + (i - nfc);
+        if (i < nfc + nch[0] + nch[1]) return P.fmax + P.cmx[0] + (i - nfc - nch[0]);
+        return P.fmax + P.cmx[0] + P.cmx[1] + (i - nfc - nch[0] - nch[1]);
     };
-    float M = -INFINITY;
-    for (int i = lane; i < nparts; i += 32) M = fmaxf(M, __ldcg(part_ptr(i) + GROUP * D + 2 * g));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float L = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i0 = sub; i0 < nparts; i0 += kSub * 8) {
-        float4 a[8];
-        float w[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int i = i0 + kSub * j;
-            if (i < nparts) {
-                const float* pi = part_ptr(i);
-                a[j] = __ldcg(reinterpret_cast<const float4*>(pi + g * D) + lane);
-                const float mi = __ldcg(pi + GROUP * D + 2 * g);
-                const float li = __ldcg(pi + GROUP * D + 2 * g + 1);
-                w[j] = mi == -INFINITY ? 0.f : ex2(mi - M);
-                L = fmaf(w[j], li, L);
-            } else {
-                a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-                w[j] = 0.f;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            acc.x = fmaf(w[j], a[j].x, acc.x);
-            acc.y = fmaf(w[j], a[j].y, acc.y);
-            acc.z = fmaf(w[j], a[j].z, acc.z);
-            acc.w = fmaf(w[j], a[j].w, acc.w);
-        }
-    }
-    sm_acc[g][sub][lane] = acc;
-    if (lane == 0) sm_l[g][sub] = L;
-    __syncthreads();
-    if (sub == 0) {
-        float4 o = sm_acc[g][0][lane];
-        float Lt = sm_l[g][0];
-#pragma unroll
-        for (int k = 1; k < kSub; ++k) {
-            const float4 x = sm_acc[g][k][lane];
-            o.x += x.x;
-            o.y += x.y;
-            o.z += x.z;
-            o.w += x.w;
-            Lt += sm_l[g][k];
-        }
-        const float inv = 1.f / Lt;
-        const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
-        const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
-        if (P.out_dtype == KITTY_F32) {
-            reinterpret_cast<float4*>(static_cast<float*>(P.out) + row * D)[lane] = make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
-        } else {
-            uint2 v;
-            v.x = f32_to_bf16_bits(o.x * inv) | (f32_to_bf16_bits(o.y * inv) << 16);
-            v.y = f32_to_bf16_bits(o.z * inv) | (f32_to_bf16_bits(o.w * inv) << 16);
-            reinterpret_cast<uint2*>(static_cast<uint16_t*>(P.out) + row * D)[lane] = v;
-        }
-    }
+    const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
+    const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
+    lse_merge_row<GROUP>(P.part + (int64_t)u * P.nslot * kStride, kStride, nparts, slot_of, g, P.out, P.out_dtype, row);
 }
 
 }  // namespace tcattn
@@ -1295,7 +1237,7 @@ static cudaError_t launch_t(const Params& prm, cudaStream_t st) {
     kfn<<<num_sms() * kCtasPerSm, kThreads, sm, st>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    combine_kernel<GROUP><<<prm.units, GROUP * 128, 0, st>>>(prm);
+    combine_kernel<GROUP><<<prm.units * GROUP, kMergeWarps * 32, 0, st>>>(prm);
     return cudaGetLastError();
 }
 
