@@ -3,8 +3,8 @@
 // A unit's work items each leave a partial record (acc[group][d] = sum p v
 // relative to the item's own running max m, then (m, l) per query row, m in
 // the log2 domain).  One CTA of kMergeWarps warps merges one (unit, query row):
-// every warp folds a strided subset of the records with online rescaling
-// (4 records' loads in flight per step), then warp 0 folds the warp states and
+// the weights 2^(m - max) are computed first (thread = part), every warp sums
+// a strided subset of the accumulator rows, and warp 0 adds the warp sums and
 // writes out = acc / l -- the softmax normalisation of cache.py:243-248.
 #pragma once
 
@@ -12,7 +12,7 @@
 
 namespace kitty {
 
-constexpr int kMergeWarps = 16;
+constexpr int kMergeWarps = 8;
 
 __device__ __forceinline__ float merge_ex2(float x) {
     float r;
@@ -21,73 +21,83 @@ __device__ __forceinline__ float merge_ex2(float x) {
 }
 
 // pb: the unit's first record; stride: floats per record; slot_of(i): record
-// index of part i; d = 128 (one float4 per lane).
+// index of part i (nparts <= kMaxParts); d = 128 (one float4 per lane).
+// Thread = part first: record index, (m, l) and the row max, so the weights
+// 2^(m - max) are known before the accumulator rows are read; then every warp
+// streams a strided subset of the rows (address + weight from shared memory,
+// 8 rows' loads in flight).  The index arithmetic per row is a few
+// instructions -- the merge was instruction-bound on it (ncu) before.
+constexpr int kMaxParts = 1024;
 template <int GROUP, class SlotFn>
 __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int nparts, SlotFn slot_of, int g,
                                               void* out, int out_dtype, int64_t row) {
     constexpr int D = 128;
-    __shared__ float s_m[kMergeWarps], s_l[kMergeWarps];
+    constexpr int T = kMergeWarps * 32;
+    __shared__ int s_slot[kMaxParts];
+    __shared__ float s_w[kMaxParts];
+    __shared__ float s_red[kMergeWarps];
     __shared__ float4 s_acc[kMergeWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float M = -INFINITY, L = 0.f;
+    if (nparts > kMaxParts) nparts = kMaxParts;  // host plans keep nslot far below
+    float mloc = -INFINITY;
+    for (int i = threadIdx.x; i < nparts; i += T) {
+        const int sl = slot_of(i);
+        s_slot[i] = sl;
+        const float m = __ldcg(pb + (int64_t)sl * stride + GROUP * D + 2 * g);
+        s_w[i] = m;
+        mloc = fmaxf(mloc, m);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+    if (lane == 0) s_red[warp] = mloc;
+    __syncthreads();
+    float M = s_red[0];
+#pragma unroll
+    for (int w = 1; w < kMergeWarps; ++w) M = fmaxf(M, s_red[w]);
+    float lsum = 0.f;
+    for (int i = threadIdx.x; i < nparts; i += T) {
+        const float m = s_w[i];
+        const float w = m == -INFINITY ? 0.f : merge_ex2(m - M);
+        s_w[i] = w;
+        lsum = fmaf(w, __ldcg(pb + (int64_t)s_slot[i] * stride + GROUP * D + 2 * g + 1), lsum);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    __syncthreads();  // s_red reads done, s_w complete
+    if (lane == 0) s_red[warp] = lsum;
+    const float* rowp = pb + g * D + 4 * lane;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i0 = warp; i0 < nparts; i0 += 4 * kMergeWarps) {
-        float4 a[4];
-        float m[4], l[4];
+    for (int i0 = warp; i0 < nparts; i0 += 8 * kMergeWarps) {
+        float4 a[8];
+        float w[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 8; ++j) {
             const int i = i0 + j * kMergeWarps;
-            if (i < nparts) {
-                const float* p = pb + (int64_t)slot_of(i) * stride;
-                a[j] = __ldcg(reinterpret_cast<const float4*>(p + g * D) + lane);
-                m[j] = __ldcg(p + GROUP * D + 2 * g);
-                l[j] = __ldcg(p + GROUP * D + 2 * g + 1);
-            } else {
-                a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-                m[j] = -INFINITY;
-                l[j] = 0.f;
-            }
+            const bool ok = i < nparts;
+            w[j] = ok ? s_w[i] : 0.f;
+            a[j] = ok ? __ldcg(reinterpret_cast<const float4*>(rowp + (int64_t)s_slot[i] * stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        const float mn = fmaxf(fmaxf(M, fmaxf(m[0], m[1])), fmaxf(m[2], m[3]));
-        if (mn == -INFINITY) continue;
-        const float sc = merge_ex2(M - mn);
-        acc.x *= sc;
-        acc.y *= sc;
-        acc.z *= sc;
-        acc.w *= sc;
-        L *= sc;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float w = merge_ex2(m[j] - mn);
-            acc.x = fmaf(w, a[j].x, acc.x);
-            acc.y = fmaf(w, a[j].y, acc.y);
-            acc.z = fmaf(w, a[j].z, acc.z);
-            acc.w = fmaf(w, a[j].w, acc.w);
-            L = fmaf(w, l[j], L);
+        for (int j = 0; j < 8; ++j) {
+            acc.x = fmaf(w[j], a[j].x, acc.x);
+            acc.y = fmaf(w[j], a[j].y, acc.y);
+            acc.z = fmaf(w[j], a[j].z, acc.z);
+            acc.w = fmaf(w[j], a[j].w, acc.w);
         }
-        M = mn;
     }
     s_acc[warp][lane] = acc;
-    if (lane == 0) {
-        s_m[warp] = M;
-        s_l[warp] = L;
-    }
     __syncthreads();
     if (warp != 0) return;
-    float mt = -INFINITY;
+    float4 o = s_acc[0][lane];
+    float lt = s_red[0];
 #pragma unroll
-    for (int w = 0; w < kMergeWarps; ++w) mt = fmaxf(mt, s_m[w]);
-    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-    float lt = 0.f;
-#pragma unroll
-    for (int w = 0; w < kMergeWarps; ++w) {
-        const float wt = s_m[w] == -INFINITY ? 0.f : merge_ex2(s_m[w] - mt);
+    for (int w = 1; w < kMergeWarps; ++w) {
         const float4 x = s_acc[w][lane];
-        o.x = fmaf(wt, x.x, o.x);
-        o.y = fmaf(wt, x.y, o.y);
-        o.z = fmaf(wt, x.z, o.z);
-        o.w = fmaf(wt, x.w, o.w);
-        lt = fmaf(wt, s_l[w], lt);
+        o.x += x.x;
+        o.y += x.y;
+        o.z += x.z;
+        o.w += x.w;
+        lt += s_red[w];
     }
     const float inv = 1.f / lt;
     if (out_dtype == KITTY_F32) {
