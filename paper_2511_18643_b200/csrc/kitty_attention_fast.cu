@@ -46,6 +46,7 @@ constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
 constexpr int kPtStride = 136;     // f16 per row of the transposed-P buffer
 constexpr int kFpChunk = 32;       // fp tokens per online-softmax step
+constexpr int kMaxTableUnits = 2048;  // units whose lengths the kernel caches in shared memory
 constexpr float kAlpha = 0.12751743074f;  // log2(e) / sqrt(128)
 constexpr uint32_t kMagic = 0x64006400u;  // f16x2 (1024, 1024)
 constexpr uint32_t kOnes = 0x3C003C00u;   // f16x2 (1, 1)
@@ -80,6 +81,7 @@ struct Params {
     int cmx[3];   // chunks per unit bound of each level
     int nslot;    // partial slots per unit: fmax + cmx[0] + cmx[1] + cmx[2]
     int units;
+    uint32_t units_mul, units_shift;  // fast division by units (quotient = (umulhi(n, mul) + n) >> shift)
     int* ctr;   // [0] next item, [1] finished warps
     float* part;
 };
@@ -373,6 +375,27 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     sm.ones[lane + 32] = kOnes;
     __syncwarp();
     const Consts kc;
+    // per-CTA copy of the unit lengths: the queue decode reads them from shared
+    // memory instead of paying a global round trip per work item
+    __shared__ int s_ulen[kMaxTableUnits];
+    const bool len_table = P.units <= kMaxTableUnits;
+    if (len_table) {
+        for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = c.unit_len[i];
+    }
+    __syncthreads();
+    auto geom = [&](int u) {
+        UnitGeom g;
+        g.n = len_table ? s_ulen[u] : c.unit_len[u];
+        const int S = c.cfg.s;
+        const int past = g.n > S ? g.n - S : 0;
+        g.kp = past / G;
+        g.vp = (past - min(c.cfg.r, past)) / G;
+        g.nfp = g.n > S ? S + (past - g.vp * G) : g.n;
+        return g;
+    };
+    auto div_units = [&](int n) {
+        return static_cast<int>((__umulhi(static_cast<uint32_t>(n), P.units_mul) + static_cast<uint32_t>(n)) >> P.units_shift);
+    };
 #ifndef KITTY_TRACE
 #define KITTY_TRACE 0
 #endif
@@ -417,9 +440,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             kind = 0;
             return;
         }
-        const int ch = idx / P.units;
+        const int ch = div_units(idx);
         u = idx - ch * P.units;
-        const UnitGeom gm = unit_geom(c, u);
+        const UnitGeom gm = geom(u);
         if (sect < 0) {
             p0 = ch;
             p1 = 0;
@@ -496,7 +519,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     // or the key q-buffer.  Lane = token for QK, lane = 4 channels for PV.
     // `prefetch` is called once the key slot is free again. ----
     auto process_fp = [&](int u, int fc, auto&& prefetch) {
-        const UnitGeom gm = unit_geom(c, u);
+        const UnitGeom gm = geom(u);
         const int s_len = min(gm.n, S);
         const int c0 = fc * kFpChunk;
         const int cnt = min(kFpChunk, gm.nfp - c0);
@@ -896,7 +919,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             ++p;
             item_done = p == p1;
             if (item_done) {
-                const int slot = page_slot(p0, unit_geom(c, u).vp);
+                const int slot = page_slot(p0, geom(u).vp);
                 float* base = P.part + ((int64_t)u * P.nslot + slot) * part_stride(GROUP);
                 float oacc[8][4];
                 tmem_wait_st();
@@ -1104,6 +1127,13 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     }
     prm.nslot = p.nslot;
     prm.units = p.units;
+    {
+        // fast division by units: q = (umulhi(n, mul) + n) >> shift, n < 2^31
+        uint32_t sh = 0;
+        while ((1u << sh) < static_cast<uint32_t>(p.units)) ++sh;
+        prm.units_shift = sh;
+        prm.units_mul = static_cast<uint32_t>((((1ull << 32) * ((1ull << sh) - static_cast<uint64_t>(p.units))) / p.units) + 1);
+    }
     prm.ctr = static_cast<int*>(ws);
     prm.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ctr_bytes);
     const long long items = (long long)p.units * p.nslot;
