@@ -1093,8 +1093,9 @@ template <int GROUP, int NKH>
 static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     auto kfn = fast_attention_kernel<GROUP, NKH>;
     const size_t sm = sizeof(WarpSmem) * kWarps;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
+    static cudaError_t attr = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  // once per instantiation
+    if (attr != cudaSuccess) return attr;
+    cudaError_t e;
     kfn<<<grid, kWarps * 32, sm, st>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

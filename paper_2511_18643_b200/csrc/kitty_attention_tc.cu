@@ -1232,8 +1232,9 @@ template <int GROUP>
 static cudaError_t launch_t(const Params& prm, cudaStream_t st) {
     auto kfn = tc_attention_kernel<GROUP>;
     const int sm = Smem<GROUP>::kBytes;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e != cudaSuccess) return e;
+    static cudaError_t attr = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);  // once per instantiation
+    if (attr != cudaSuccess) return attr;
+    cudaError_t e;
     kfn<<<num_sms() * kCtasPerSm, kThreads, sm, st>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
