@@ -14,12 +14,6 @@ namespace kitty {
 // [g][d] (row = token), staged in shared memory by the caller.
 // ---------------------------------------------------------------------------
 
-template <typename T>
-__device__ bool tile_all_finite(const T* tile, int n) {
-    int bad = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite(load_elem(tile, i));
-    return __syncthreads_or(bad) == 0;
-}
 
 // pack_key_page (pages.py:81-118) preceded, when `sel` is NULL, by
 // channel_scores + select_boost (cache.py:155-158).  Writes the KTYP body to
@@ -38,7 +32,9 @@ __device__ void pack_key_tile(const T* tile, int g, int d, int d_boost, const in
         // channel_scores (quant.py:64-72): sequential fp64 over tokens, / g
         for (int c = tid; c < d; c += nt) {
             double acc = 0.0;
-            for (int t = 0; t < g; ++t) acc += static_cast<double>(fabsf(load_elem(tile, (int64_t)t * d + c)));
+            const T* col = tile + c;
+#pragma unroll 8
+            for (int t = 0; t < g; ++t) acc += static_cast<double>(fabsf(load_elem(col, t * d)));
             sc.score[c] = acc / static_cast<double>(g);
         }
         __syncthreads();
@@ -55,10 +51,25 @@ __device__ void pack_key_tile(const T* tile, int g, int d, int d_boost, const in
     }
     __syncthreads();
     // high_bits row of each boosted channel: ascending channel order (pages.py:103)
-    for (int c = tid; c < d; c += nt) {
-        int pos = 0;
-        for (int j = 0; j < c; ++j) pos += sc.flag[j];
-        sc.pos[c] = pos;
+    if (d <= nt && d <= 1024) {
+        // ballot prefix: rank of c among the boosted channels below it
+        __shared__ int warp_cnt[32];
+        const int lane = tid & 31, w = tid >> 5;
+        const bool f = tid < d && sc.flag[tid] != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) warp_cnt[w] = __popc(bal);
+        __syncthreads();
+        if (tid < d) {
+            int pos = __popc(bal & ((1u << lane) - 1u));
+            for (int j = 0; j < w; ++j) pos += warp_cnt[j];
+            sc.pos[tid] = pos;
+        }
+    } else {
+        for (int c = tid; c < d; c += nt) {
+            int pos = 0;
+            for (int j = 0; j < c; ++j) pos += sc.flag[j];
+            sc.pos[c] = pos;
+        }
     }
     __syncthreads();
     // per-channel quantization (quant.py:102-116) and 2-bit packing (pages.py:42-45)
@@ -69,20 +80,23 @@ __device__ void pack_key_tile(const T* tile, int g, int d, int d_boost, const in
     uint8_t* s16 = slot_smem + L.scale_off();
     uint8_t* z16 = slot_smem + L.zero_off();
     for (int c = tid; c < d; c += nt) {
-        float mn = load_elem(tile, c), mx = mn;
+        const T* col = tile + c;
+        float mn = load_elem(col, 0), mx = mn;
+#pragma unroll 8
         for (int t = 1; t < g; ++t) {
-            const float v = load_elem(tile, (int64_t)t * d + c);
+            const float v = load_elem(col, t * d);
             mn = fminf(mn, v);
             mx = fmaxf(mx, v);
         }
         const bool boosted = sc.flag[c] != 0;
         const LaneQuant q(mn, mx, boosted ? 15.f : 3.f);
         const int row = sc.pos[c];
+#pragma unroll 2
         for (int b = 0; b < gb; ++b) {
             uint32_t lo = 0, hi = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t code = q.code(load_elem(tile, (int64_t)(4 * b + j) * d + c));
+                const uint32_t code = q.code(load_elem(col, (4 * b + j) * d));
                 lo |= (code & 3u) << (2 * j);
                 hi |= (code >> 2) << (2 * j);
             }
@@ -150,23 +164,38 @@ __device__ void copy_slot_out(const uint8_t* slot_smem, uint8_t* gslot, int byte
     }
 }
 
-// Stage g rows [start, start + g) of a row ring of size `wrap` into smem.
+// Stage g rows [start, start + g) of a row ring of size `wrap` (start < wrap,
+// g <= wrap) into smem, checking every element for non-finite values on the
+// way (pages.py:88-89, 152-153).  Returns true when all are finite.
+__device__ __forceinline__ int bf16x2_nonfinite(uint32_t w) {
+    const uint32_t u = (w & 0x7F807F80u) ^ 0x7F807F80u;  // a zero half = exponent all ones
+    return ((u & 0xFFFFu) == 0u) | ((u >> 16) == 0u);
+}
 template <typename T>
-__device__ void stage_rows(T* tile, const T* base, int start, int wrap, int g, int d) {
+__device__ bool stage_rows(T* tile, const T* base, int start, int wrap, int g, int d) {
+    int bad = 0;
     if (sizeof(T) == 2 && (d % 8) == 0) {
         const int vpr = d / 8;  // uint4 per row
+        const int lg = (vpr & (vpr - 1)) == 0 ? __ffs(vpr) - 1 : -1;
         for (int i = threadIdx.x; i < g * vpr; i += blockDim.x) {
-            const int r = i / vpr, v = i % vpr;
-            const uint4* src = reinterpret_cast<const uint4*>(base + (int64_t)((start + r) % wrap) * d);
-            reinterpret_cast<uint4*>(tile + (int64_t)r * d)[v] = src[v];
+            const int r = lg >= 0 ? (i >> lg) : i / vpr;
+            const int v = i - r * vpr;
+            int row = start + r;
+            if (row >= wrap) row -= wrap;
+            const uint4 x = reinterpret_cast<const uint4*>(base + (int64_t)row * d)[v];
+            reinterpret_cast<uint4*>(tile + (int64_t)r * d)[v] = x;
+            bad |= bf16x2_nonfinite(x.x) | bf16x2_nonfinite(x.y) | bf16x2_nonfinite(x.z) | bf16x2_nonfinite(x.w);
         }
     } else {
         for (int i = threadIdx.x; i < g * d; i += blockDim.x) {
             const int r = i / d, c = i % d;
-            tile[i] = base[(int64_t)((start + r) % wrap) * d + c];
+            int row = start + r;
+            if (row >= wrap) row -= wrap;
+            tile[i] = base[(int64_t)row * d + c];
+            bad |= !isfinite(load_elem(tile, i));
         }
     }
-    __syncthreads();
+    return __syncthreads_or(bad) == 0;
 }
 
 // Shared-memory budget of one pack (tile + slot + scratch), in bytes.
@@ -203,8 +232,7 @@ __global__ void pack_key_pages_kernel(const T* x, int g, int d, int d_boost, con
     uint8_t* slot = smem + off;
     off += ((size_t)max(KeyLayout{d, g, d_boost}.bytes(), ValueLayout{d, g}.bytes()) + 15) & ~size_t(15);
     PackScratch sc = carve_scratch(smem + off, d);
-    stage_rows(tile, x + (int64_t)p * g * d, 0, g, g, d);
-    if (!tile_all_finite(tile, g * d)) {
+    if (!stage_rows(tile, x + (int64_t)p * g * d, 0, g, g, d)) {
         if (threadIdx.x == 0) set_status(status, KITTY_STATUS_NONFINITE);
         return;
     }
@@ -220,8 +248,7 @@ __global__ void pack_value_pages_kernel(const T* x, int g, int d, uint8_t* slots
     const int p = blockIdx.x;
     T* tile = reinterpret_cast<T*>(smem);
     uint8_t* slot = smem + (((size_t)g * d * sizeof(T) + 15) & ~size_t(15));
-    stage_rows(tile, x + (int64_t)p * g * d, 0, g, g, d);
-    if (!tile_all_finite(tile, g * d)) {
+    if (!stage_rows(tile, x + (int64_t)p * g * d, 0, g, g, d)) {
         if (threadIdx.x == 0) set_status(status, KITTY_STATUS_NONFINITE);
         return;
     }
@@ -357,8 +384,7 @@ __device__ void pack_key_into_cache(const KittyCacheDesc& c, int u, int p, const
     uint8_t* slot = smem + off;
     off += ((size_t)max(KeyLayout{k.d, k.g, k.d_boost}.bytes(), ValueLayout{k.d, k.g}.bytes()) + 15) & ~size_t(15);
     PackScratch sc = carve_scratch(smem + off, k.d);
-    stage_rows(tile, base, start, wrap, k.g, k.d);
-    if (!tile_all_finite(tile, k.g * k.d)) {
+    if (!stage_rows(tile, base, start, wrap, k.g, k.d)) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_NONFINITE);
     }
     pack_key_tile(tile, k.g, k.d, k.d_boost, nullptr, slot, sc, nullptr, nullptr);
@@ -375,8 +401,7 @@ __device__ void pack_value_into_cache(const KittyCacheDesc& c, int u, int p, con
     }
     uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
     uint8_t* slot = smem + (((size_t)k.g * k.d * 2 + 15) & ~size_t(15));
-    stage_rows(tile, base, start, wrap, k.g, k.d);
-    if (!tile_all_finite(tile, k.g * k.d)) {
+    if (!stage_rows(tile, base, start, wrap, k.g, k.d)) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_NONFINITE);
     }
     pack_value_tile(tile, k.g, k.d, slot, nullptr, nullptr);
@@ -428,7 +453,12 @@ __global__ void prefill_rows_kernel(KittyCacheDesc c, const uint16_t* keys, cons
     const int kp = past / G;
     const int local = min(k.r, past);
     const int vp = (past - local) / G;
-    for (int t = blockIdx.x; t < P; t += gridDim.x) {
+    // only the tokens that stay full precision: the sink, the key q-buffer
+    // [S + kp G, P) and the value q-buffer + local window [S + vp G, P)
+    const int t_fp = S + vp * G;  // <= S + kp * G
+    const int n_fp = min(P, S) + (P > t_fp ? P - t_fp : 0);
+    for (int i = blockIdx.x; i < n_fp; i += gridDim.x) {
+        const int t = i < min(P, S) ? i : t_fp + (i - min(P, S));
         const uint16_t* kr = keys + ((int64_t)u * P + t) * d;
         const uint16_t* vr = values + ((int64_t)u * P + t) * d;
         if (t < S) {
@@ -599,7 +629,8 @@ cudaError_t launch_prefill(const KittyCacheDesc& c, const uint16_t* keys, const 
     const int past = P > S ? P - S : 0;
     const int kp = past / G;
     const int vp = (past - min(c.cfg.r, past)) / G;
-    const int gx = P > 0 ? min(P, 1024) : 1;
+    const int n_fp = min(P, S) + (P > S + vp * G ? P - (S + vp * G) : 0);
+    const int gx = n_fp > 0 ? min(n_fp, 1024) : 1;
     prefill_rows_kernel<<<dim3(gx, units), 128, 0, st>>>(c, keys, values, P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || kp + vp == 0) return e;
