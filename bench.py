@@ -314,29 +314,8 @@ def run_kitty(args):
 
 
 def _prefill_slice(cache, b0, nb, k, v):
-    """Prefill sequences [b0, b0 + nb) of a layer cache through the C ABI
-    (kitty_prefill on a sub-descriptor that aliases the batch's buffers)."""
-    import ctypes
-
-    import torch
-
-    from paper_2511_18643_b200 import _lib
-    from paper_2511_18643_b200.pages import _stream
-
-    cfg = cache.cfg
-    u0 = b0 * cfg.h_kv
-    d = _lib.KittyCacheDesc()
-    ctypes.memmove(ctypes.byref(d), ctypes.byref(cache.desc), ctypes.sizeof(d))
-    d.num_seqs = nb
-    d.unit_len = cache.unit_len[u0:].data_ptr()
-    d.k_sink = cache.k_sink[u0:].data_ptr()
-    d.v_sink = cache.v_sink[u0:].data_ptr()
-    d.k_qbuf = cache.k_qbuf[u0:].data_ptr()
-    d.v_ring = cache.v_ring[u0:].data_ptr()
-    d.key_block_table = cache.key_block_table[u0:].data_ptr()
-    d.value_block_table = cache.value_block_table[u0:].data_ptr()
-    _lib.check(cache.lib.kitty_prefill(ctypes.byref(d), k.contiguous().data_ptr(), v.contiguous().data_ptr(),
-                                       k.shape[2], _stream()), "prefill")
+    """Prefill sequences [b0, b0 + nb) of a layer cache through the C ABI."""
+    cache.prefill_range(b0, nb, k, v)
 
 
 def _ncu_traffic(config):

@@ -156,21 +156,60 @@ class KittyBatchCache:
             self.lengths[b] += 1
             self._count_events(b, self.lengths[b])
 
-    def prefill(self, keys: torch.Tensor, values: torch.Tensor):
-        """cache.py:125-142 for an empty batch: keys/values [B, h_kv, P, D]."""
+    def prefill(self, keys: torch.Tensor, values: torch.Tensor, lengths=None):
+        """cache.py:125-142 for an empty batch: keys/values [B, h_kv, P, D].
+
+        ``lengths`` (optional, one per sequence, each <= P) makes the batch
+        ragged: sequence b gets the first lengths[b] tokens of its rows, and
+        every later append / attend works on its own length (the device reads
+        the per-unit lengths; pack triggers are per sequence)."""
         if any(self.lengths):
             raise KittyError("prefill requires an empty state")
         cfg = self.cfg
         p = keys.shape[2]
-        if p > self.max_tokens:
-            self.grow(p)
+        if lengths is None:
+            lengths = [p] * self.num_seqs
+        lengths = [int(x) for x in lengths]
+        if len(lengths) != self.num_seqs or min(lengths) < 0 or max(lengths) > p:
+            raise KittyError(f"lengths must be {self.num_seqs} values in [0, {p}]")
+        if max(lengths) > self.max_tokens:
+            self.grow(max(lengths))
         keys = self._rows(keys, (self.num_seqs, cfg.h_kv, p, cfg.d), "keys")
         values = self._rows(values, (self.num_seqs, cfg.h_kv, p, cfg.d), "values")
-        _lib.check(self.lib.kitty_prefill(self._desc_ref, keys.data_ptr(), values.data_ptr(), p, _stream()), "prefill")
-        for b in range(self.num_seqs):
-            for n in range(1, p + 1):
-                self._count_events(b, n)
-            self.lengths[b] = p
+        if all(x == p for x in lengths):
+            _lib.check(self.lib.kitty_prefill(self._desc_ref, keys.data_ptr(), values.data_ptr(), p, _stream()), "prefill")
+        else:
+            for b, n in enumerate(lengths):
+                if n:
+                    self.prefill_range(b, 1, keys[b:b + 1, :, :n], values[b:b + 1, :, :n])
+        for b, n in enumerate(lengths):
+            for i in range(1, n + 1):
+                self._count_events(b, i)
+            self.lengths[b] = n
+
+    def prefill_range(self, b0: int, nb: int, keys: torch.Tensor, values: torch.Tensor):
+        """kitty_prefill of sequences [b0, b0 + nb) through a sub-descriptor that
+        aliases this batch's buffers (keys/values [nb, h_kv, P, D] bf16 on the
+        device).  Does not update the host length mirror."""
+        cfg = self.cfg
+        u0 = b0 * cfg.h_kv
+        d = _lib.KittyCacheDesc()
+        ctypes.memmove(ctypes.byref(d), ctypes.byref(self.desc), ctypes.sizeof(d))
+        d.num_seqs = nb
+        d.unit_len = self.unit_len[u0:].data_ptr()
+        d.k_sink = self.k_sink[u0:].data_ptr()
+        d.v_sink = self.v_sink[u0:].data_ptr()
+        d.k_qbuf = self.k_qbuf[u0:].data_ptr()
+        d.v_ring = self.v_ring[u0:].data_ptr()
+        d.key_block_table = self.key_block_table[u0:].data_ptr()
+        d.value_block_table = self.value_block_table[u0:].data_ptr()
+        # keep the contiguous copies alive until the launch is enqueued: a
+        # temporary freed before its consumer runs can be handed to the next
+        # allocation on the same stream
+        kc, vc = keys.contiguous(), values.contiguous()
+        _lib.check(self.lib.kitty_prefill(ctypes.byref(d), kc.data_ptr(), vc.data_ptr(), keys.shape[2], _stream()),
+                   "prefill")
+        self._keepalive = (kc, vc)
 
     def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.bfloat16) -> torch.Tensor:
         """Step 2 for every sequence: q [B, h_q, D] bf16 -> [B, h_q, D]."""

@@ -274,3 +274,34 @@ def test_decode_loop_matches_oracle(cuda, kernel):
     cache.check()
     assert cache.key_pack_events[0] == oc.key_pack_events
     assert cache.value_pack_events[0] == oc.value_pack_events
+
+
+@pytest.mark.parametrize("group", [4, 8])
+def test_ragged_batch_matches_oracle(cuda, kernel, group):
+    # a ragged batch -- every sequence has its own length,
+    # page count and pack triggers -- through prefill, decode steps and attend
+    rng = np.random.default_rng(11 + group)
+    h_kv, h_q = 2, 2 * group
+    lens = [40, 700, 1337, 2100]
+    b, steps, pmax = len(lens), 3, max(lens)
+    cfg = cuda.KittyConfig(h_kv=h_kv, h_q=h_q)
+    k, v, _ = _c1_like(rng, b, h_kv, h_q, pmax + steps)
+    cache = cuda.KittyBatchCache(cfg, b, pmax + steps + 8)
+    cache.prefill(torch.from_numpy(k[:, :, :pmax]), torch.from_numpy(v[:, :, :pmax]), lengths=lens)
+    ocs = []
+    for bi, n in enumerate(lens):
+        oc = ko.OracleCache(32, 128, 128, 128, h_kv, h_q, 0.125, metadata16=True)
+        oc.prefill(k[bi, :, :n], v[bi, :, :n])
+        ocs.append(oc)
+    for s in range(steps):
+        kn = np.stack([k[bi, :, lens[bi] + s] for bi in range(b)])
+        vn = np.stack([v[bi, :, lens[bi] + s] for bi in range(b)])
+        cache.append(torch.from_numpy(kn), torch.from_numpy(vn))
+        for bi in range(b):
+            ocs[bi].insert_token(kn[bi], vn[bi])
+        q = _bf16(rng.normal(0, 1, (b, h_q, 128)))
+        out = cache.attend(torch.from_numpy(q).cuda()).float().cpu().numpy()
+        cache.check()
+        for bi in range(b):
+            assert cache.lengths[bi] == lens[bi] + s + 1
+            assert np.max(np.abs(out[bi] - ocs[bi].attend(q[bi]))) <= 1e-2, (s, bi)
