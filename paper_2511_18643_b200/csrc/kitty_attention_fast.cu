@@ -40,7 +40,18 @@ constexpr int G = 128;
 // floats per partial record (acc[group][D], then (m, l) per row), padded to 16 B
 __host__ __device__ constexpr int part_stride(int group) { return (group * (D + 2) + 3) & ~3; }
 constexpr int kWarps = 4;         // warps per CTA
-constexpr int kCtasPerSm = 2;      // 8 warps per SM
+#ifndef KITTY_FAST_SINGLE
+#define KITTY_FAST_SINGLE 0
+#endif
+#ifndef KITTY_FAST_CTAS
+#define KITTY_FAST_CTAS 3
+#endif
+// Staging: 2-stage (key, value) page-pair ring per warp at 8 warps / SM, or one
+// key slot + one value slot per warp, each refilled as soon as it is consumed,
+// at 4 * KITTY_FAST_CTAS warps / SM.
+constexpr bool kSingle = KITTY_FAST_SINGLE != 0;
+constexpr int kStages = kSingle ? 1 : 2;
+constexpr int kCtasPerSm = kSingle ? KITTY_FAST_CTAS : 2;
 constexpr int kTmemCols = 64;      // per CTA; per warp (its TMEM lane quarter): [0,32) output accumulators, [32,48) q fragments
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
@@ -55,8 +66,8 @@ constexpr uint32_t kOnes = 0x3C003C00u;   // f16x2 (1, 1)
 // slots; the pair for page i+1 is in flight (cp.async.bulk) while page i is
 // computed.
 struct __align__(128) WarpSmem {
-    uint8_t kbuf[2][kKeySlotMax];  // KTYP key bodies (a free one also stages the fp routine's key page)
-    uint8_t vbuf[2][kValueSlot];   // KTYP value bodies
+    uint8_t kbuf[kStages][kKeySlotMax];  // KTYP key bodies (a free one also stages the fp routine's key page)
+    uint8_t vbuf[kStages][kValueSlot];   // KTYP value bodies
     union {
         uint32_t pt[8][kPtStride / 2];  // P^T as f16x2: rows 0-3 p*s, rows 4-7 p
         struct {
@@ -581,7 +592,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         while (need) {
             const int src = __ffs(need) - 1;
             const int page = __shfl_sync(0xffffffffu, pc / G, src);
-            uint8_t* buf = sm.kbuf[issued & 1];  // <= 1 pair in flight here: this stage is free
+            uint8_t* buf = sm.kbuf[kSingle ? 0 : (issued & 1)];  // <= 1 pair in flight here: this stage is free
             const uint4* gsrc = reinterpret_cast<const uint4*>(
                 c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + page] * kslot);
 #pragma unroll
@@ -866,15 +877,117 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         ofresh = false;
     };
 
+    // single-stage mode: key slot (mbar[0]) and value slot (mbar[1]) refilled separately
+    uint32_t kcon = 0, vcon = 0;
+    auto issue_k = [&](int u_, int p_) {
+        if (lane == 0) {
+            const uint8_t* ks = c.key_pool + (int64_t)c.key_block_table[(int64_t)u_ * c.max_pages + p_] * kslot;
+            mbar_expect_tx(&sm.mbar[0], kslot);
+            bulk_g2s(sm.kbuf[0], ks, kslot, &sm.mbar[0]);
+        }
+        __syncwarp();
+    };
+    auto issue_v = [&](int u_, int p_) {
+        if (lane == 0) {
+            const uint8_t* vs = c.value_pool + (int64_t)c.value_block_table[(int64_t)u_ * c.max_pages + p_] * vslot;
+            mbar_expect_tx(&sm.mbar[1], vslot);
+            bulk_g2s(sm.vbuf[0], vs, vslot, &sm.mbar[1]);
+        }
+        __syncwarp();
+    };
     // ---- work loop -------------------------------------------------------------------
     int kind, u, p0, p1;
     next_item(kind, u, p0, p1);
     int nkind = 0, nu = 0, np0 = 0, np1 = 0;
     if (kind != 0) next_item(nkind, nu, np0, np1);
     bool pending = false;  // the current item's first page pair is already in flight
+    bool kpend = false, vpend = false;  // single-stage: next item's first key / value page in flight
     int p = p0;
 #pragma unroll 1
-    while (kind != 0) {
+    while (kSingle && kind != 0) {
+        bool item_done;
+        if (kind == 1) {
+            if (nkind == 2 && !vpend) {  // the value slot is idle during an fp item
+                issue_v(nu, np0);
+                vpend = true;
+            }
+            process_fp(u, p0, [&]() {
+                if (nkind == 2 && !kpend) {
+                    issue_k(nu, np0);
+                    kpend = true;
+                }
+            });
+            item_done = true;
+        } else {
+            if (p == p0) {
+                if (!kpend) issue_k(u, p0);
+                if (!vpend) issue_v(u, p0);
+                kpend = vpend = false;
+                load_unit(u);
+                om[0] = om[1] = -INFINITY;
+                ol[0] = ol[1] = 0.f;
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) ob[c4][0] = ob[c4][1] = 0.f;
+                ofresh = true;
+            }
+            const bool more = p + 1 < p1;
+            const bool chain = !more && nkind == 2;
+            mbar_wait(&sm.mbar[0], kcon & 1);
+            ++kcon;
+            qk_page(0);
+            __syncwarp();
+            if (more) issue_k(u, p + 1);
+            if (chain) {
+                issue_k(nu, np0);
+                kpend = true;
+            }
+            mbar_wait(&sm.mbar[1], vcon & 1);
+            ++vcon;
+            pv_page(0);
+            __syncwarp();
+            if (more) issue_v(u, p + 1);
+            if (chain) {
+                issue_v(nu, np0);
+                vpend = true;
+            }
+            ++p;
+            item_done = p == p1;
+            if (item_done) {
+                const int slot = page_slot(p0, geom(u).vp);
+                float* base = P.part + ((int64_t)u * P.nslot + slot) * part_stride(GROUP);
+                float oacc[8][4];
+                tmem_wait_st();
+                tmem_ld32(taddr, oacc);
+                if (tig < 2) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int g = 2 * tig + j;
+                        if (g < GROUP) {
+#pragma unroll
+                            for (int m = 0; m < 8; ++m)
+                                *reinterpret_cast<float2*>(base + g * D + 16 * gid + 2 * m) =
+                                    make_float2(oacc[m][j] + ob[(m & 1) ? 2 : 0][j],
+                                                oacc[m][2 + j] + ob[(m & 1) ? 3 : 1][j]);
+                            if (gid == 0) {
+                                base[GROUP * D + 2 * g] = om[j];
+                                base[GROUP * D + 2 * g + 1] = ol[j];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (item_done) {
+            kind = nkind;
+            u = nu;
+            p0 = np0;
+            p1 = np1;
+            p = p0;
+            if (kind != 0) next_item(nkind, nu, np0, np1);
+        }
+    }
+#pragma unroll 1
+    while (!kSingle && kind != 0) {
         bool item_done;
         if (kind == 1) {
             const long long tf0 = trace ? gtimer() : 0;
