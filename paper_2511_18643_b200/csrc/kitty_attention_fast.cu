@@ -320,12 +320,14 @@ struct UnitGeom {
 };
 
 // Pages of a unit are scheduled in three levels of decreasing chunk size:
-// [0, vp/2) in chunks of cs[0], [vp/2, 4vp/5) in cs[1], [4vp/5, vp) in 1-page
-// chunks; the queue serves level 0 (interleaved with the fp chunks) first, so
-// it drains in small pieces and no SM idles behind a long item.
-// level boundaries as per-mille of vp (tuning knobs, set once by the host plan)
-__constant__ int c_lvl[2] = {500, 800};
-static int h_lvl[2] = {500, 800};
+// [0, 0.8 vp) in chunks of cs[0] (<= 8 pages), [0.8 vp, 0.94 vp) in cs[0] / 2,
+// the rest page by page; the queue serves the fp chunks, then level 0, 1, 2,
+// so it drains in small pieces and no SM idles behind a long item (swept on
+// B200 with tools/sweep_sched.sh: 148 -> 133 us per C2 layer with the fp
+// chunks moved first).  Level boundaries are per-mille of vp (tuning knobs,
+// set once by the host plan; KITTY_SCHED overrides them for sweeps).
+__constant__ int c_lvl[2] = {800, 940};
+static int h_lvl[2] = {800, 940};
 __host__ __device__ __forceinline__ int level_begin(int lv, int vp) {
 #ifdef __CUDA_ARCH__
     const int* lvl = c_lvl;
@@ -428,19 +430,21 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         return i;
     };
     // item -> (kind, unit, a, b); kind 0 = end, 1 = fp chunk a, 2 = pages [a, b), 3 = empty.
-    // Queue: fp chunks interleaved with level-0 page chunks (latency-bound fp
-    // work overlaps tensor-core work), then level-1 chunks, then level-2.
+    // Queue: all fp chunks first (latency-bound CUDA-core work, one wave across
+    // every warp while the first page loads are in flight; measured 148 -> 140 us
+    // per C2 layer against interleaving them with level 0), then level-0, level-1
+    // and level-2 page chunks.
     const int nf = P.units * P.fmax, nq0 = P.units * P.cmx[0];
     const int nq1 = P.units * P.cmx[1], nq2 = P.units * P.cmx[2];
     const int n2 = 2 * min(nf, nq0);
     auto decode = [&](int it, int& kind, int& u, int& p0, int& p1) {
         int sect, idx;  // -1 fp, 0..2 page level
-        if (it < n2) {
-            sect = (it & 1) ? 0 : -1;
-            idx = it >> 1;
+        if (it < nf) {  // the fp chunks first: latency-bound, they overlap on all warps at once
+            sect = -1;
+            idx = it;
         } else if (it < nf + nq0) {
-            sect = nf > nq0 ? -1 : 0;
-            idx = it - n2 + min(nf, nq0);
+            sect = 0;
+            idx = it - nf;
         } else if (it < nf + nq0 + nq1) {
             sect = 1;
             idx = it - nf - nq0;
@@ -1168,7 +1172,7 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     const int maxp = past / G + 1;
     const long long pages = (long long)p.units * maxp;
     const long long warps = (long long)num_sms() * kCtasPerSm * kWarps;
-    static int ppc_max = 8, cs1_div = 4, inited = 0;
+    static int ppc_max = 8, cs1_div = 2, inited = 0;
     if (!inited) {
         inited = 1;
         if (const char* e = getenv("KITTY_SCHED")) {  // experiments: "l1,l2,ppc_max,cs1_div"
