@@ -30,6 +30,7 @@
 
 #include "kitty_attention.cuh"
 #include "kitty_combine.cuh"
+#include "kitty_fp.cuh"
 #include "kitty_codec.cuh"
 
 namespace kitty {
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     // every warp while the first page loads are in flight; measured 148 -> 140 us
     // per C2 layer against interleaving them with level 0), then level-0, level-1
     // and level-2 page chunks.
-    const int nf = P.units * P.fmax, nq0 = P.units * P.cmx[0];
+    const int nf = 0, nq0 = P.units * P.cmx[0];  // fp chunks run in fp_tokens_kernel
     const int nq1 = P.units * P.cmx[1], nq2 = P.units * P.cmx[2];
     const int n2 = 2 * min(nf, nq0);
     auto decode = [&](int it, int& kind, int& u, int& p0, int& p1) {
@@ -526,170 +527,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
         tmem_wait_st();
         tmem_st16(taddr + 32, qa);
-    };
-
-    // ---- one chunk of <= 32 full-precision tokens of a unit: the sink and the
-    // value q-buffer + local (cache.py:196-208); keys of those tokens come from
-    // the key sink, a key page (Alg. 1 from a shared-memory copy of the page)
-    // or the key q-buffer.  Lane = token for QK, lane = 4 channels for PV.
-    // `prefetch` is called once the key slot is free again. ----
-    auto process_fp = [&](int u, int fc, auto&& prefetch) {
-        const UnitGeom gm = geom(u);
-        const int s_len = min(gm.n, S);
-        const int c0 = fc * kFpChunk;
-        const int cnt = min(kFpChunk, gm.nfp - c0);
-        const int vbase = S + gm.vp * G;  // first value-fp token past the sink
-        auto token_of = [&](int j) { return j < s_len ? j : vbase + (j - s_len); };
-        // q * alpha (f32) into shared memory
-#pragma unroll
-        for (int g = 0; g < GROUP; ++g) {
-            const uint2 w = __ldg(reinterpret_cast<const uint2*>(q_row(u, g)) + lane);
-            sm.u.fp.qf[g][2 * lane] = __floats2half2_rn(__uint_as_float(w.x << 16) * kAlpha,
-                                                        __uint_as_float(w.x & 0xffff0000u) * kAlpha);
-            sm.u.fp.qf[g][2 * lane + 1] = __floats2half2_rn(__uint_as_float(w.y << 16) * kAlpha,
-                                                            __uint_as_float(w.y & 0xffff0000u) * kAlpha);
-        }
-        __syncwarp();
-        const bool valid = lane < cnt;
-        const int t = token_of(c0 + (valid ? lane : 0));
-        const int pc = t - S;
-        const bool in_page = t >= S && pc < gm.kp * G;
-        float lg[4] = {0.f, 0.f, 0.f, 0.f};
-        if (!in_page) {
-            const uint16_t* krow = t < S ? c.k_sink + ((int64_t)u * S + t) * D
-                                         : c.k_qbuf + ((int64_t)u * G + pc % G) * D;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint4 w[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) w[i] = reinterpret_cast<const uint4*>(krow)[8 * half + i];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int d0 = 8 * (8 * half + i);
-                    const float k8[8] = {__uint_as_float(w[i].x << 16), __uint_as_float(w[i].x & 0xffff0000u),
-                                         __uint_as_float(w[i].y << 16), __uint_as_float(w[i].y & 0xffff0000u),
-                                         __uint_as_float(w[i].z << 16), __uint_as_float(w[i].z & 0xffff0000u),
-                                         __uint_as_float(w[i].w << 16), __uint_as_float(w[i].w & 0xffff0000u)};
-#pragma unroll
-                    for (int g = 0; g < GROUP; ++g) {
-                        const uint4 qh = *reinterpret_cast<const uint4*>(&sm.u.fp.qf[g][d0 / 2]);
-                        const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&qh.x));
-                        const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&qh.y));
-                        const float2 q45 = __half22float2(*reinterpret_cast<const __half2*>(&qh.z));
-                        const float2 q67 = __half22float2(*reinterpret_cast<const __half2*>(&qh.w));
-                        const float4 qa_ = make_float4(q01.x, q01.y, q23.x, q23.y);
-                        const float4 qb_ = make_float4(q45.x, q45.y, q67.x, q67.y);
-                        lg[g] = fmaf(qa_.x, k8[0], lg[g]);
-                        lg[g] = fmaf(qa_.y, k8[1], lg[g]);
-                        lg[g] = fmaf(qa_.z, k8[2], lg[g]);
-                        lg[g] = fmaf(qa_.w, k8[3], lg[g]);
-                        lg[g] = fmaf(qb_.x, k8[4], lg[g]);
-                        lg[g] = fmaf(qb_.y, k8[5], lg[g]);
-                        lg[g] = fmaf(qb_.z, k8[6], lg[g]);
-                        lg[g] = fmaf(qb_.w, k8[7], lg[g]);
-                    }
-                }
-            }
-        }
-        // keys that sit in key pages: stage each such page in the (idle) key slot
-        unsigned need = __ballot_sync(0xffffffffu, valid && in_page);
-        while (need) {
-            const int src = __ffs(need) - 1;
-            const int page = __shfl_sync(0xffffffffu, pc / G, src);
-            uint8_t* buf = sm.kbuf[kSingle ? 0 : (issued & 1)];  // <= 1 pair in flight here: this stage is free
-            const uint4* gsrc = reinterpret_cast<const uint4*>(
-                c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + page] * kslot);
-#pragma unroll
-            for (int i0 = 0; i0 < 12; i0 += 6) {
-                uint4 tmp[6];
-#pragma unroll
-                for (int i = 0; i < 6; ++i)
-                    if (lane + 32 * (i0 + i) < kslot / 16) tmp[i] = gsrc[lane + 32 * (i0 + i)];
-#pragma unroll
-                for (int i = 0; i < 6; ++i)
-                    if (lane + 32 * (i0 + i) < kslot / 16) reinterpret_cast<uint4*>(buf)[lane + 32 * (i0 + i)] = tmp[i];
-            }
-            __syncwarp();
-            const bool mine = valid && in_page && pc / G == page;
-            if (mine) {
-                const int tl = pc % G, sh = 2 * (tl & 3), byte = tl >> 2;
-                const uint8_t* hb = buf + D * G / 4;
-                const uint8_t* ib = buf + D * G / 4 + d_boost * G / 4;
-#pragma unroll 4
-                for (int d = 0; d < D; ++d) {
-                    uint32_t code = (buf[d * (G / 4) + byte] >> sh) & 3u;
-                    const uint32_t r = ib[d];
-                    if (r != kSentinel) code |= ((hb[r * (G / 4) + byte] >> sh) & 3u) << 2;
-                    const float s_ = half_bits_to_f32(ld_u16(buf + scale_off + 2 * d));
-                    const float z_ = half_bits_to_f32(ld_u16(buf + zero_off + 2 * d));
-                    const float kv = fmaf(static_cast<float>(code), s_, z_);
-#pragma unroll
-                    for (int g = 0; g < GROUP; ++g) {
-                        const __half2 qq = sm.u.fp.qf[g][d >> 1];
-                        lg[g] = fmaf((d & 1) ? __high2float(qq) : __low2float(qq), kv, lg[g]);
-                    }
-                }
-            }
-            __syncwarp();
-            need &= ~__ballot_sync(0xffffffffu, mine);
-        }
-        prefetch();  // key slot is free: start the next page item's loads
-        // softmax of the chunk (log2 domain)
-        float m[4], l[4];
-#pragma unroll
-        for (int g = 0; g < GROUP; ++g) {
-            const float x = valid ? lg[g] : -INFINITY;
-            float mc = x;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
-            const float p = valid ? ex2(x - mc) : 0.f;
-            float ps = p;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-            m[g] = mc;
-            l[g] = ps;
-            sm.u.fp.ps[g][lane] = p;
-        }
-        __syncwarp();
-        // P V over the chunk: lane owns channels 4 lane .. 4 lane + 3
-        float acc[4][4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
-        const uint16_t* vsink = c.v_sink + (int64_t)u * S * D;
-        const uint16_t* vr = c.v_ring + (int64_t)u * W * D;
-#pragma unroll 1
-        for (int j0 = 0; j0 < cnt; j0 += 16) {
-            uint2 vv[16];
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-                const int tt = token_of(c0 + min(j0 + jj, cnt - 1));
-                const uint16_t* vrow = tt < S ? vsink + (int64_t)tt * D : vr + (int64_t)((tt - S) % W) * D;
-                vv[jj] = reinterpret_cast<const uint2*>(vrow)[lane];
-            }
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-                const float v0 = __uint_as_float(vv[jj].x << 16), v1 = __uint_as_float(vv[jj].x & 0xffff0000u);
-                const float v2 = __uint_as_float(vv[jj].y << 16), v3 = __uint_as_float(vv[jj].y & 0xffff0000u);
-#pragma unroll
-                for (int g = 0; g < GROUP; ++g) {
-                    const float pg = (j0 + jj < cnt) ? sm.u.fp.ps[g][j0 + jj] : 0.f;
-                    acc[g][0] = fmaf(pg, v0, acc[g][0]);
-                    acc[g][1] = fmaf(pg, v1, acc[g][1]);
-                    acc[g][2] = fmaf(pg, v2, acc[g][2]);
-                    acc[g][3] = fmaf(pg, v3, acc[g][3]);
-                }
-            }
-        }
-        __syncwarp();
-        float* base = P.part + ((int64_t)u * P.nslot + fc) * part_stride(GROUP);
-#pragma unroll
-        for (int g = 0; g < GROUP; ++g) {
-            reinterpret_cast<float4*>(base + g * D)[lane] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
-            if (lane == 0) {
-                base[GROUP * D + 2 * g] = m[g];
-                base[GROUP * D + 2 * g + 1] = l[g];
-            }
-        }
     };
 
     // ---- quantized pages: QK^T on the key slot, then P V on the value slot ----
@@ -910,19 +747,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll 1
     while (kSingle && kind != 0) {
         bool item_done;
-        if (kind == 1) {
-            if (nkind == 2 && !vpend) {  // the value slot is idle during an fp item
-                issue_v(nu, np0);
-                vpend = true;
-            }
-            process_fp(u, p0, [&]() {
-                if (nkind == 2 && !kpend) {
-                    issue_k(nu, np0);
-                    kpend = true;
-                }
-            });
-            item_done = true;
-        } else {
+        {
             if (p == p0) {
                 if (!kpend) issue_k(u, p0);
                 if (!vpend) issue_v(u, p0);
@@ -993,18 +818,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll 1
     while (!kSingle && kind != 0) {
         bool item_done;
-        if (kind == 1) {
-            const long long tf0 = trace ? gtimer() : 0;
-            ++tr_nfp;
-            process_fp(u, p0, [&]() {
-                if (nkind == 2 && !pending) {
-                    issue(nu, np0);
-                    pending = true;
-                }
-            });
-            if (trace) tr_fp += gtimer() - tf0;
-            item_done = true;
-        } else {
+        {
             if (p == p0) {
                 if (!pending) issue(u, p0);
                 pending = false;
@@ -1110,6 +924,19 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 // K5: log-sum-exp merge of a unit's partials (fp chunks + page chunks).  One
 // CTA per unit, 4 warps per query row, each warp over a quarter of the parts;
 // loads are independent so the merge is one or two L2 round trips deep.
+// The full-precision tokens: one 128-thread CTA per 32-token chunk
+// (kitty_fp.cuh), run as its own launch before the page kernel so neither
+// code path's register allocation or instruction footprint burdens the other.
+template <int GROUP>
+__global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
+    extern __shared__ __align__(128) uint8_t fsm[];
+    const int it = blockIdx.x;
+    const int fc = it / P.units, u = it - fc * P.units;
+    const fptok::Geom gm = fptok::geom(P.c, u);
+    if (gm.n == 0 || fc * kFpChunk >= gm.nfp) return;
+    fptok::chunk_cta<GROUP>(P.c, P.q, P.part, P.nslot, part_stride(GROUP), fsm, u, fc);
+}
+
 template <int GROUP>
 __global__ void __launch_bounds__(kMergeWarps * 32) combine_parts_kernel(Params P) {
     const int u = blockIdx.x / GROUP, g = blockIdx.x - (blockIdx.x / GROUP) * GROUP;
@@ -1212,7 +1039,15 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     const size_t sm = sizeof(WarpSmem) * kWarps;
     static cudaError_t attr = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  // once per instantiation
     if (attr != cudaSuccess) return attr;
+    // the fp-token chunks first (their own launch), then the pages, then the merge
     cudaError_t e;
+    {
+        const int nfp_items = prm.units * prm.fmax;
+        const int fsm = fptok::cta_scratch_bytes<GROUP>();
+        fp_tokens_kernel<GROUP><<<nfp_items, 128, fsm, st>>>(prm);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     kfn<<<grid, kWarps * 32, sm, st>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

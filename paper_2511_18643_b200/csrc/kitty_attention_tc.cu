@@ -36,6 +36,7 @@
 // a unit's partials (log-sum-exp) and writes the bf16 / f32 output.
 #include "kitty_attention.cuh"
 #include "kitty_combine.cuh"
+#include "kitty_fp.cuh"
 #include "kitty_codec.cuh"
 
 namespace kitty {
@@ -90,7 +91,7 @@ struct Smem {
     static constexpr int o_vmeta = o_bp + 2 * 128 * NB;          // [2][128] float2 (s, z)
     static constexpr int o_zx = o_vmeta + 2 * 128 * 8;            // [2][4 warps][8] partial sum_d q alpha z_d
     static constexpr int o_fp = o_zx + 2 * 4 * 8 * 4;             // per fp warp scratch
-    static constexpr int kFpBytes = kKeySlotMax + GROUP * D * 2 + GROUP * kFpChunk * 4;
+    static constexpr int kFpBytes = fptok::scratch_bytes<GROUP>();
     static constexpr int kFpAl = (kFpBytes + 127) / 128 * 128;
     static constexpr int o_ring4 = o_fp + kFpWarps * kFpAl;      // RingEntry[4]
     static constexpr int o_kinfo = o_ring4 + 4 * sizeof(RingEntry);
@@ -316,150 +317,6 @@ __device__ __forceinline__ UnitGeom unit_geom(const KittyCacheDesc& c, int u) {
 // serves level 0 of every unit first, so it drains in small pieces.
 __host__ __device__ __forceinline__ int level_begin(int lv, int vp) {
     return lv == 0 ? 0 : (lv == 1 ? (vp * 3) / 5 : (lv == 2 ? (vp * 9) / 10 : vp));
-}
-
-// ---- the full-precision tokens of a unit (CUDA cores), one 32-token chunk ----------
-// Tokens: sink, then the value q-buffer + local window (cache.py:196-208); the
-// keys of those tokens come from the key sink, a key page (dequantised from a
-// shared-memory copy, Alg. 1) or the key q-buffer.  Lane = token for QK, lane
-// = 4 channels for PV.
-template <int GROUP>
-__device__ void fp_chunk(const Params& P, uint8_t* scratch, int u, int fc, int lane) {
-    const KittyCacheDesc& c = P.c;
-    const int S = c.cfg.s, W = c.cfg.r + c.cfg.g, d_boost = c.cfg.d_boost;
-    const int kslot = static_cast<int>(c.key_slot_bytes);
-    const int scale_off = D * G / 4 + d_boost * G / 4 + D, zero_off = scale_off + 2 * D;
-    uint8_t* kbuf = scratch;
-    __half2* qf = reinterpret_cast<__half2*>(scratch + kKeySlotMax);           // [GROUP][D/2]
-    float* ps = reinterpret_cast<float*>(scratch + kKeySlotMax + GROUP * D * 2);  // [GROUP][32]
-    const UnitGeom gm = unit_geom(c, u);
-    const int s_len = min(gm.n, S);
-    const int c0 = fc * kFpChunk;
-    const int cnt = min(kFpChunk, gm.nfp - c0);
-    const int vbase = S + gm.vp * G;
-    auto token_of = [&](int j) { return j < s_len ? j : vbase + (j - s_len); };
-    const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
-    const uint16_t* qbase = P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP) * D;
-#pragma unroll
-    for (int g = 0; g < GROUP; ++g) {
-        const uint2 w = __ldg(reinterpret_cast<const uint2*>(qbase + g * D) + lane);
-        qf[g * (D / 2) + 2 * lane] = __floats2half2_rn(__uint_as_float(w.x << 16) * kAlpha, __uint_as_float(w.x & 0xffff0000u) * kAlpha);
-        qf[g * (D / 2) + 2 * lane + 1] = __floats2half2_rn(__uint_as_float(w.y << 16) * kAlpha, __uint_as_float(w.y & 0xffff0000u) * kAlpha);
-    }
-    __syncwarp();
-    const bool valid = lane < cnt;
-    const int t = token_of(c0 + (valid ? lane : 0));
-    const int pc = t - S;
-    const bool in_page = t >= S && pc < gm.kp * G;
-    float lg[GROUP];
-#pragma unroll
-    for (int g = 0; g < GROUP; ++g) lg[g] = 0.f;
-    if (!in_page) {
-        const uint16_t* krow = t < S ? c.k_sink + ((int64_t)u * S + t) * D : c.k_qbuf + ((int64_t)u * G + pc % G) * D;
-#pragma unroll 2
-        for (int i = 0; i < 16; ++i) {
-            const uint4 w = reinterpret_cast<const uint4*>(krow)[i];
-            const float k8[8] = {__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u),
-                                 __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u),
-                                 __uint_as_float(w.z << 16), __uint_as_float(w.z & 0xffff0000u),
-                                 __uint_as_float(w.w << 16), __uint_as_float(w.w & 0xffff0000u)};
-#pragma unroll
-            for (int g = 0; g < GROUP; ++g) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 qq = __half22float2(qf[g * (D / 2) + 4 * i + e]);
-                    lg[g] = fmaf(qq.x, k8[2 * e], lg[g]);
-                    lg[g] = fmaf(qq.y, k8[2 * e + 1], lg[g]);
-                }
-            }
-        }
-    }
-    // keys that sit in key pages: stage each such page in the warp's key buffer
-    unsigned need = __ballot_sync(0xffffffffu, valid && in_page);
-    while (need) {
-        const int src = __ffs(need) - 1;
-        const int page = __shfl_sync(0xffffffffu, pc / G, src);
-        const uint4* gsrc = reinterpret_cast<const uint4*>(c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + page] * kslot);
-        for (int i = lane; i < kslot / 16; i += 32) reinterpret_cast<uint4*>(kbuf)[i] = gsrc[i];
-        __syncwarp();
-        const bool mine = valid && in_page && pc / G == page;
-        if (mine) {
-            const int tl = pc % G, sh = 2 * (tl & 3), byte = tl >> 2;
-            const uint8_t* hb = kbuf + D * G / 4;
-            const uint8_t* ib = kbuf + D * G / 4 + d_boost * G / 4;
-#pragma unroll 4
-            for (int d = 0; d < D; ++d) {
-                uint32_t code = (kbuf[d * (G / 4) + byte] >> sh) & 3u;
-                const uint32_t r = ib[d];
-                if (r != kSentinel) code |= ((hb[r * (G / 4) + byte] >> sh) & 3u) << 2;
-                const float s_ = half_bits_to_f32(ld_u16(kbuf + scale_off + 2 * d));
-                const float z_ = half_bits_to_f32(ld_u16(kbuf + zero_off + 2 * d));
-                const float kv = fmaf(static_cast<float>(code), s_, z_);
-#pragma unroll
-                for (int g = 0; g < GROUP; ++g) {
-                    const __half2 qq = qf[g * (D / 2) + (d >> 1)];
-                    lg[g] = fmaf((d & 1) ? __high2float(qq) : __low2float(qq), kv, lg[g]);
-                }
-            }
-        }
-        __syncwarp();
-        need &= ~__ballot_sync(0xffffffffu, mine);
-    }
-    float m[GROUP], l[GROUP];
-#pragma unroll
-    for (int g = 0; g < GROUP; ++g) {
-        const float x = valid ? lg[g] : -INFINITY;
-        float mc = x;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
-        const float p = valid ? ex2(x - mc) : 0.f;
-        float s = p;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        m[g] = mc;
-        l[g] = s;
-        ps[g * kFpChunk + lane] = p;
-    }
-    __syncwarp();
-    float acc[GROUP][4];
-#pragma unroll
-    for (int g = 0; g < GROUP; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
-    const uint16_t* vsink = c.v_sink + (int64_t)u * S * D;
-    const uint16_t* vr = c.v_ring + (int64_t)u * W * D;
-#pragma unroll 1
-    for (int j0 = 0; j0 < cnt; j0 += 8) {
-        uint2 vv[8];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-            const int tt = token_of(c0 + min(j0 + jj, cnt - 1));
-            const uint16_t* vrow = tt < S ? vsink + (int64_t)tt * D : vr + (int64_t)((tt - S) % W) * D;
-            vv[jj] = reinterpret_cast<const uint2*>(vrow)[lane];
-        }
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-            const float v0 = __uint_as_float(vv[jj].x << 16), v1 = __uint_as_float(vv[jj].x & 0xffff0000u);
-            const float v2 = __uint_as_float(vv[jj].y << 16), v3 = __uint_as_float(vv[jj].y & 0xffff0000u);
-#pragma unroll
-            for (int g = 0; g < GROUP; ++g) {
-                const float pg = (j0 + jj < cnt) ? ps[g * kFpChunk + j0 + jj] : 0.f;
-                acc[g][0] = fmaf(pg, v0, acc[g][0]);
-                acc[g][1] = fmaf(pg, v1, acc[g][1]);
-                acc[g][2] = fmaf(pg, v2, acc[g][2]);
-                acc[g][3] = fmaf(pg, v3, acc[g][3]);
-            }
-        }
-    }
-    __syncwarp();
-    float* base = P.part + ((int64_t)u * P.nslot + fc) * part_stride(GROUP);
-#pragma unroll
-    for (int g = 0; g < GROUP; ++g) {
-        reinterpret_cast<float4*>(base + g * D)[lane] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
-        if (lane == 0) {
-            base[GROUP * D + 2 * g] = m[g];
-            base[GROUP * D + 2 * g + 1] = l[g];
-        }
-    }
-    __syncwarp();
 }
 
 // ---- the kernel --------------------------------------------------------------------
@@ -1119,7 +976,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tc_attention_kernel(Para
             const int fc = it / P.units, u = it - fc * P.units;
             const UnitGeom gm = unit_geom(c, u);
             if (gm.n == 0 || fc * kFpChunk >= gm.nfp) continue;
-            fp_chunk<GROUP>(P, scratch, u, fc, lane);
+            fptok::chunk<GROUP>(P.c, P.q, P.part, P.nslot, part_stride(GROUP), scratch, u, fc, lane);
         }
     }
 
