@@ -203,13 +203,13 @@ class KittyBatchCache:
         d.v_ring = self.v_ring[u0:].data_ptr()
         d.key_block_table = self.key_block_table[u0:].data_ptr()
         d.value_block_table = self.value_block_table[u0:].data_ptr()
-        # keep the contiguous copies alive until the launch is enqueued: a
-        # temporary freed before its consumer runs can be handed to the next
-        # allocation on the same stream
+        # both contiguous copies must be alive when the launch is enqueued: a
+        # temporary freed before its consumer is enqueued can be handed to the
+        # next allocation on the same stream (after the enqueue, stream order
+        # makes reuse safe)
         kc, vc = keys.contiguous(), values.contiguous()
         _lib.check(self.lib.kitty_prefill(ctypes.byref(d), kc.data_ptr(), vc.data_ptr(), keys.shape[2], _stream()),
                    "prefill")
-        self._keepalive = (kc, vc)
 
     def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.bfloat16) -> torch.Tensor:
         """Step 2 for every sequence: q [B, h_q, D] bf16 -> [B, h_q, D]."""
