@@ -226,8 +226,8 @@ cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, 
                                     cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
     if (units == 0) return cudaSuccess;
-    // mma.sync kernel for GQA groups <= 4 (fastest measured); the
-    // tcgen05 kernel for group 8 and when selected
+    // mma.sync kernel (fastest measured); the tcgen05 kernel when
+    // selected (kitty_debug_select_attention)
     if (fast_attention_supported(c) && !(g_attention_impl == 1 && tc_attention_supported(c)))
         return launch_fast_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
     if (tc_attention_supported(c)) return launch_tc_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);

@@ -70,7 +70,7 @@ struct __align__(128) WarpSmem {
     uint8_t kbuf[kStages][kKeySlotMax];  // KTYP key bodies (a free one also stages the fp routine's key page)
     uint8_t vbuf[kStages][kValueSlot];   // KTYP value bodies
     union {
-        uint32_t pt[8][kPtStride / 2];  // P^T as f16x2: rows 0-3 p*s, rows 4-7 p
+        uint32_t pt[16][kPtStride / 2];  // P^T as f16x2: p*s per query, then p (rows 4-7 / 8-15 for group 4 / 8)
         struct {
             __half2 qf[4][D / 2];    // q * alpha (f16) for the fp routine
             float ps[4][kFpChunk];   // fp routine probabilities
@@ -366,7 +366,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     const int scale_off = D * G / 4 + d_boost * G / 4 + D;  // KTYP key scales
     const int zero_off = scale_off + 2 * D;
     const int hkv = c.cfg.h_kv;
-    const bool main_col = gid < 4;
+    // group <= 4: B columns 0-3 are the queries, 4-7 auxiliary (unscaled q / p);
+    // group 8: all eight are queries and the auxiliary sums take a second MMA
+    constexpr bool kFull = GROUP == 8;
+    const bool main_col = kFull || gid < 4;
     const bool row0 = gid == 0;
 
     __shared__ uint32_t tmem_base_sh;
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         if (u == cur_unit) return;
         cur_unit = u;
         q_cur = q_row(u, 0);
-        const int col = gid & 3;
+        const int col = kFull ? gid : (gid & 3);
         const uint16_t* qg = q_row(u, col < GROUP ? col : 0);
         uint32_t qa[8][2];
 #pragma unroll
@@ -549,7 +552,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
             __syncwarp();
         }
-        float aux[4];
+        float aux[4], aux2[4];
         // aux lanes (B columns 4-7) read their "scale" from a ones buffer
         const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
         uint32_t qa[8][2];
@@ -569,13 +572,15 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             if (ks == 0) {
                 mma_codes<true>(kc, acc, w0, w1, w2, w3, b0, b1);
                 mma16816_z(aux, kOnes, z0, kOnes, z1, b0, b1);
+                if (kFull) mma16816_z(aux2, kOnes, z0, kOnes, z1, qa[ks][0], qa[ks][1]);
             } else {
                 mma_codes(kc, acc, w0, w1, w2, w3, b0, b1);
                 mma16816(aux, kOnes, z0, kOnes, z1, b0, b1);
+                if (kFull) mma16816(aux2, kOnes, z0, kOnes, z1, qa[ks][0], qa[ks][1]);
             }
         }
         if (NKH > 0) {
-            const int col = gid & 3;
+            const int col = kFull ? gid : (gid & 3);
             const uint16_t* qg = q_cur + (col < GROUP ? col : 0) * D;
 #pragma unroll
             for (int hk = 0; hk < NKH; ++hk) {
@@ -601,8 +606,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         // Row weights: even tiles hold codes 0 / 1 of a byte (w 256 / 4), odd tiles 2 / 3 (w 16 / 64).
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const float sumB = __shfl_sync(0xffffffffu, aux[j], tig & 1);
-            const float cst = __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
+            const float sumB = __shfl_sync(0xffffffffu, aux[j], kFull ? tig : (tig & 1));
+            const float cst = kFull ? __shfl_sync(0xffffffffu, aux2[2 + j], tig)
+                                    : __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
             bw[0][j] = cst - 4.f * sumB;    // w 256
             bw[1][j] = cst - 256.f * sumB;  // w 4
             bw[2][j] = cst - 64.f * sumB;   // w 16
@@ -647,17 +653,17 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const uint32_t sv = lds32(vscale + 2 * tok);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                if (tig < 2) {
+                if (kFull || tig < 2) {
                     const int g = 2 * tig + j;
                     const int w = 8 * gid + (m ^ gid);  // XOR swizzle: conflict-free stores and loads
                     sm.u.pt[g][w] = hmul2(pu[m][j], sv);
-                    sm.u.pt[4 + g][w] = pu[m][j];
+                    sm.u.pt[(kFull ? 8 : 4) + g][w] = pu[m][j];
                 }
             }
         }
         __syncwarp();
         float pacc[8][4];
-        float vaux[4];
+        float vaux[4], vaux2[4];
         const uint8_t* vzero = vscale + 2 * G;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
@@ -675,12 +681,20 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 mma_codes(kc, pacc, w0, w1, w2, w3, b0, b1);
                 mma16816(vaux, kOnes, z0, kOnes, z1, b0, b1);
             }
+            if (kFull) {  // the unscaled p (rows 8-15 of P^T): sum p and sum p z
+                const uint32_t c0u = sm.u.pt[8 + gid][8 * ks + (tig ^ ks)];
+                const uint32_t c1u = sm.u.pt[8 + gid][8 * ks + ((tig + 4) ^ ks)];
+                if (ks == 0)
+                    mma16816_z(vaux2, kOnes, z0, kOnes, z1, c0u, c1u);
+                else
+                    mma16816(vaux2, kOnes, z0, kOnes, z1, c0u, c1u);
+            }
         }
         // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z).
         // Row constants (zero points, the 1024 offset) accumulate per column in
         // ob[weight class] and are added at the flush; the accumulators are only
         // rescaled when a running max of a real column moved (warp vote).
-        const bool real0 = tig < 2 && 2 * tig < GROUP, real1 = tig < 2 && 2 * tig + 1 < GROUP;
+        const bool real0 = kFull || (tig < 2 && 2 * tig < GROUP), real1 = kFull || (tig < 2 && 2 * tig + 1 < GROUP);
         const bool rescale = __any_sync(0xffffffffu, (real0 && corr[0] != 1.f) || (real1 && corr[1] != 1.f));
         float oacc[8][4];
         if (ofresh) {
@@ -692,9 +706,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const float sBv = __shfl_sync(0xffffffffu, vaux[j], tig & 1);
-            const float lp = __shfl_sync(0xffffffffu, vaux[j], 2 + (tig & 1));
-            const float zz = __shfl_sync(0xffffffffu, vaux[2 + j], 2 + (tig & 1));
+            const float sBv = __shfl_sync(0xffffffffu, vaux[j], kFull ? tig : (tig & 1));
+            const float lp = kFull ? __shfl_sync(0xffffffffu, vaux2[j], tig) : __shfl_sync(0xffffffffu, vaux[j], 2 + (tig & 1));
+            const float zz = kFull ? __shfl_sync(0xffffffffu, vaux2[2 + j], tig)
+                                   : __shfl_sync(0xffffffffu, vaux[2 + j], 2 + (tig & 1));
             ol[j] = fmaf(ol[j], corr[j], lp);
             ob[0][j] = fmaf(ob[0][j], corr[j], zz - 4.f * sBv);
             ob[1][j] = fmaf(ob[1][j], corr[j], zz - 256.f * sBv);
@@ -787,7 +802,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 float oacc[8][4];
                 tmem_wait_st();
                 tmem_ld32(taddr, oacc);
-                if (tig < 2) {
+                if (kFull || tig < 2) {
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         const int g = 2 * tig + j;
@@ -855,7 +870,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
                 float oacc[8][4];
                 tmem_wait_st();
                 tmem_ld32(taddr, oacc);
-                if (tig < 2) {
+                if (kFull || tig < 2) {
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         const int g = 2 * tig + j;
@@ -982,7 +997,7 @@ static int num_sms() {
 bool fast_attention_supported(const KittyCacheDesc& c) {
     const int group = c.cfg.h_q / c.cfg.h_kv;
     return c.cfg.d == D && c.cfg.g == G && c.cfg.key_bits == 2 && c.cfg.value_bits == 2 &&
-           (group == 1 || group == 2 || group == 4) && c.cfg.d_boost <= 32 &&
+           (group == 1 || group == 2 || group == 4 || group == 8) && c.cfg.d_boost <= 32 &&
            c.key_slot_bytes <= kKeySlotMax && c.value_slot_bytes == 4608;
 }
 
@@ -1097,7 +1112,8 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     switch (p.group) {
         case 1: return launch_g<1>(prm, nkh, grid, st);
         case 2: return launch_g<2>(prm, nkh, grid, st);
-        default: return launch_g<4>(prm, nkh, grid, st);
+        case 4: return launch_g<4>(prm, nkh, grid, st);
+        default: return launch_g<8>(prm, nkh, grid, st);
     }
 }
 

@@ -49,9 +49,9 @@ class DecodeStep:
         return self.num_layers * (1 + self.attention_launches())
 
     def attention_launches(self) -> int:
-        # mma.sync path (groups <= 4): fp-token chunks + pages + split-KV merge;
-        # tcgen05 path (group 8): one kernel (fp tokens on dedicated warps) + merge
-        return 3 if self.cfg.group_size <= 4 else 2
+        # mma.sync path (default): fp-token chunks + pages + split-KV merge;
+        # the tcgen05 path (kitty_debug_select_attention) launches 2
+        return 3
 
     def fast_path(self) -> bool:
         c = self.cfg

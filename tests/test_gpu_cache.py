@@ -222,8 +222,8 @@ def _c1_like(rng, b, h_kv, h_q, n, d=128):
 
 @pytest.fixture(params=["default", "tc"])
 def kernel(request, cuda):
-    """Both decode-attention kernels: the default dispatch (mma.sync kernel for
-    GQA groups <= 4, tcgen05 for group 8) and the tcgen05 kernel everywhere."""
+    """Both decode-attention kernels: the default dispatch (mma.sync kernel,
+    GQA groups 1-8) and the tcgen05 kernel everywhere."""
     cuda.select_attention_kernel(request.param)
     yield request.param
     cuda.select_attention_kernel("default")
