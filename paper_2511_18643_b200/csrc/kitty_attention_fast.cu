@@ -321,14 +321,13 @@ struct UnitGeom {
 };
 
 // Pages of a unit are scheduled in three levels of decreasing chunk size:
-// [0, 0.8 vp) in chunks of cs[0] (<= 8 pages), [0.8 vp, 0.94 vp) in cs[0] / 2,
-// the rest page by page; the queue serves the fp chunks, then level 0, 1, 2,
-// so it drains in small pieces and no SM idles behind a long item (swept on
-// B200 with tools/sweep_sched.sh: 148 -> 133 us per C2 layer with the fp
-// chunks moved first).  Level boundaries are per-mille of vp (tuning knobs,
+// [0, 0.85 vp) in chunks of cs[0] (<= 8 pages), [0.85 vp, 0.95 vp) in cs[0] / 4,
+// the rest page by page; the queue serves level 0, 1, 2, so it drains in small
+// pieces and no SM idles behind a long item (swept on B200 with
+// tools/sweep_sched.sh).  Level boundaries are per-mille of vp (tuning knobs,
 // set once by the host plan; KITTY_SCHED overrides them for sweeps).
-__constant__ int c_lvl[2] = {800, 940};
-static int h_lvl[2] = {800, 940};
+__constant__ int c_lvl[2] = {850, 950};
+static int h_lvl[2] = {850, 950};
 __host__ __device__ __forceinline__ int level_begin(int lv, int vp) {
 #ifdef __CUDA_ARCH__
     const int* lvl = c_lvl;
@@ -1014,7 +1013,7 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     const int maxp = past / G + 1;
     const long long pages = (long long)p.units * maxp;
     const long long warps = (long long)num_sms() * kCtasPerSm * kWarps;
-    static int ppc_max = 8, cs1_div = 2, inited = 0;
+    static int ppc_max = 8, cs1_div = 4, inited = 0;
     if (!inited) {
         inited = 1;
         if (const char* e = getenv("KITTY_SCHED")) {  // experiments: "l1,l2,ppc_max,cs1_div"
