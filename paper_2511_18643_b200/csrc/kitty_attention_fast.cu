@@ -65,16 +65,14 @@ constexpr uint32_t kOnes = 0x3C003C00u;   // f16x2 (1, 1)
 
 // Per-warp shared memory (23 KB): a 2-stage ring of (key page, value page)
 // slots; the pair for page i+1 is in flight (cp.async.bulk) while page i is
-// computed.
-struct __align__(128) WarpSmem {
-    uint8_t kbuf[kStages][kKeySlotMax];  // KTYP key bodies (a free one also stages the fp routine's key page)
+// computed.  Sized so that two page CTAs leave room on the SM for one fp-token
+// CTA (the programmatic dependent grid) from the start.
+template <int PT_ROWS>
+struct __align__(128) WarpSmemT {
+    uint8_t kbuf[kStages][kKeySlotMax];  // KTYP key bodies
     uint8_t vbuf[kStages][kValueSlot];   // KTYP value bodies
-    union {
-        uint32_t pt[16][kPtStride / 2];  // P^T as f16x2: p*s per query, then p (rows 4-7 / 8-15 for group 4 / 8)
-        struct {
-            __half2 qf[4][D / 2];    // q * alpha (f16) for the fp routine
-            float ps[4][kFpChunk];   // fp routine probabilities
-        } fp;
+    struct {
+        uint32_t pt[PT_ROWS][kPtStride / 2];  // P^T as f16x2: p*s per query, then p (rows 4-7 / 8-15 for group 4 / 8)
     } u;
     uint32_t ones[64];            // f16x2 (1, 1): scale operand of the aux B columns
     uint8_t inv[32];              // boosted channel of high_bits row j
@@ -356,6 +354,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
+    using WarpSmem = WarpSmemT<GROUP == 8 ? 16 : 8>;
     WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
     const KittyCacheDesc& c = P.c;
     const int S = c.cfg.s, W = c.cfg.r + c.cfg.g;
@@ -391,9 +390,14 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     sm.ones[lane + 32] = kOnes;
     __syncwarp();
     const Consts kc;
+    // launched as a programmatic dependent of the preceding kernel (the append):
+    // the prologue above overlaps its tail; nothing of the cache is read before this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the fp-token grid (our programmatic dependent) may be scheduled from now on
+    asm volatile("griddepcontrol.launch_dependents;");
     // per-CTA copy of the unit lengths: the queue decode reads them from shared
     // memory instead of paying a global round trip per work item
-    __shared__ int s_ulen[kMaxTableUnits];
+    int* s_ulen = reinterpret_cast<int*>(smem_raw + sizeof(WarpSmem) * kWarps);  // dynamic, units entries
     const bool len_table = P.units <= kMaxTableUnits;
     if (len_table) {
         for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = c.unit_len[i];
@@ -947,12 +951,15 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
     const int it = blockIdx.x;
     const int fc = it / P.units, u = it - fc * P.units;
     const fptok::Geom gm = fptok::geom(P.c, u);
-    if (gm.n == 0 || fc * kFpChunk >= gm.nfp) return;
-    fptok::chunk_cta<GROUP>(P.c, P.q, P.part, P.nslot, part_stride(GROUP), fsm, u, fc);
+    asm volatile("griddepcontrol.launch_dependents;");  // the merge may pre-launch
+    if (gm.n > 0 && fc * kFpChunk < gm.nfp) fptok::chunk_tc<GROUP>(P.c, P.q, P.part, P.nslot, part_stride(GROUP), fsm, u, fc);
+    // launched as a programmatic dependent of the page grid: finish only after it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 template <int GROUP>
 __global__ void __launch_bounds__(kMergeWarps * 32) combine_parts_kernel(Params P) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the fp grid
     const int u = blockIdx.x / GROUP, g = blockIdx.x - (blockIdx.x / GROUP) * GROUP;
     const KittyCacheDesc& c = P.c;
     const UnitGeom gm = unit_geom(c, u);
@@ -1047,26 +1054,61 @@ size_t fast_attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
     return p.ctr_bytes + p.part_bytes;
 }
 
+// programmatic dependent launch per edge, a bit mask (A/B knob KITTY_PDL):
+// 1 = page grid behind the preceding kernel, 2 = fp grid behind the page grid,
+// 4 = merge grid behind the fp grid
+static const int g_pdl = [] {
+    const char* e = std::getenv("KITTY_PDL");
+    return e ? std::atoi(e) : 3;
+}();
+
 template <int GROUP, int NKH>
 static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     auto kfn = fast_attention_kernel<GROUP, NKH>;
-    const size_t sm = sizeof(WarpSmem) * kWarps;
-    static cudaError_t attr = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  // once per instantiation
+    const size_t sm = sizeof(WarpSmemT<GROUP == 8 ? 16 : 8>) * kWarps + (prm.units <= kMaxTableUnits ? 4 * prm.units : 0);
+    static cudaError_t attr = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)(sizeof(WarpSmemT<GROUP == 8 ? 16 : 8>) * kWarps + 4 * kMaxTableUnits));  // once per instantiation
     if (attr != cudaSuccess) return attr;
-    // the fp-token chunks first (their own launch), then the pages, then the merge
+    // the pages first; the fp-token chunks as a programmatic dependent of the
+    // page grid, so their CTAs backfill SMs as persistent page CTAs retire (the
+    // fp grid waits on the page grid only before it exits); then the merge
     cudaError_t e;
+    cudaLaunchAttribute at[3];
+    for (int i = 0; i < 3; ++i) {
+        at[i].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[i].val.programmaticStreamSerializationAllowed = (g_pdl >> i) & 1;
+    }
     {
-        const int nfp_items = prm.units * prm.fmax;
-        const int fsm = fptok::cta_scratch_bytes<GROUP>();
-        fp_tokens_kernel<GROUP><<<nfp_items, 128, fsm, st>>>(prm);
-        e = cudaGetLastError();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kWarps * 32);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cfg.attrs = at + 0;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kfn, prm);
         if (e != cudaSuccess) return e;
     }
-    kfn<<<grid, kWarps * 32, sm, st>>>(prm);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    combine_parts_kernel<GROUP><<<prm.units * GROUP, kMergeWarps * 32, 0, st>>>(prm);
-    return cudaGetLastError();
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(prm.units * prm.fmax);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = fptok::tc_scratch_bytes<GROUP>();
+        cfg.stream = st;
+        cfg.attrs = at + 1;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, fp_tokens_kernel<GROUP>, prm);
+        if (e != cudaSuccess) return e;
+    }
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(prm.units * GROUP);
+        cfg.blockDim = dim3(kMergeWarps * 32);
+        cfg.stream = st;
+        cfg.attrs = at + 2;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP>, prm);
+    }
 }
 
 template <int GROUP>

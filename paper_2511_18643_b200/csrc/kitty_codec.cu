@@ -413,6 +413,9 @@ __device__ void pack_value_into_cache(const KittyCacheDesc& c, int u, int p, con
 // of maybe_pack (cache.py:144-178) on this unit's own counts.
 __global__ void append_kernel(KittyCacheDesc c, const uint16_t* k_new, const uint16_t* v_new) {
     extern __shared__ __align__(16) uint8_t smem[];
+    // the attention grid that follows may run its prologue now (it waits on us
+    // with griddepcontrol.wait before reading the cache)
+    asm volatile("griddepcontrol.launch_dependents;");
     const KittyConfigC& k = c.cfg;
     const int u = blockIdx.x;
     const int d = k.d, S = k.s, G = k.g, W = k.r + k.g;

@@ -448,3 +448,272 @@ __device__ void chunk_cta(const KittyCacheDesc& c, const uint16_t* q, float* par
 
 }  // namespace fptok
 }  // namespace kitty
+
+namespace kitty {
+namespace fptok {
+
+// ---- tensor-core version: the chunk's key and value rows staged as exact f16
+// tiles (bf16 -> f16 is exact for these magnitudes), QK and PV on
+// mma.sync.m16n8k16 with ldmatrix operands.  One 128-thread CTA per chunk. ----
+constexpr int kRowH = D + 8;  // f16 per staged row (272 B: conflict-free ldmatrix)
+
+template <int GROUP>
+__host__ __device__ constexpr int tc_scratch_bytes() {
+    return kKeySlotMax + 2 * kChunk * kRowH * 2 + 2 * kChunk * 8 * 4 + 8 * kChunk * 2 + 64;
+}
+
+__device__ __forceinline__ uint32_t f2h2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// 8 bf16 -> 8 f16 (exact for |x| in the f16 range)
+__device__ __forceinline__ uint4 bf16x8_to_f16x8(uint4 w) {
+    uint4 o;
+    o.x = f2h2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u));
+    o.y = f2h2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u));
+    o.z = f2h2(__uint_as_float(w.z << 16), __uint_as_float(w.z & 0xffff0000u));
+    o.w = f2h2(__uint_as_float(w.w << 16), __uint_as_float(w.w & 0xffff0000u));
+    return o;
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void hmma(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                     uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// the key page arrives by 1-D TMA on one mbarrier (one phase per page)
+__device__ __forceinline__ void page_fetch(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint64_t* bar) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void page_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "PW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra PW_%=;\n}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+        "r"(phase)
+        : "memory");
+}
+
+template <int GROUP>
+__device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part, int nslot, int stride,
+                         uint8_t* scratch, int u, int fc) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int S = c.cfg.s, W = c.cfg.r + c.cfg.g, d_boost = c.cfg.d_boost;
+    const int kslot = static_cast<int>(c.key_slot_bytes);
+    const int scale_off = D * G / 4 + d_boost * G / 4 + D, zero_off = scale_off + 2 * D;
+    uint8_t* kbuf = scratch;
+    uint16_t* kt = reinterpret_cast<uint16_t*>(scratch + kKeySlotMax);   // [32][kRowH] f16 keys
+    uint16_t* vt = kt + kChunk * kRowH;                                   // [32][kRowH] f16 values
+    float* lgs = reinterpret_cast<float*>(vt + kChunk * kRowH);           // [2][32][8] logit halves
+    uint16_t* pT = reinterpret_cast<uint16_t*>(lgs + 2 * kChunk * 8);      // [8][32] f16 probabilities
+    uint64_t* bar = reinterpret_cast<uint64_t*>(pT + 8 * kChunk);
+    const Geom gm = geom(c, u);
+    const int s_len = min(gm.n, S);
+    const int c0 = fc * kChunk;
+    const int cnt = min(kChunk, gm.nfp - c0);
+    const int vbase = S + gm.vp * G;
+    auto token_of = [&](int j) { return j < s_len ? j : vbase + (j - s_len); };
+    const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
+    const uint16_t* qbase = q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP) * D;
+    // key pages the chunk's tokens sit in (the local window): [pg_lo, pg_hi]
+    const int first_t = token_of(c0), last_t = token_of(c0 + cnt - 1);
+    const int fpc = first_t - S, lpc = last_t - S;
+    const bool fp_ = first_t >= S && fpc < gm.kp * G, lp_ = last_t >= S && lpc < gm.kp * G;
+    const int pg_lo = fp_ ? fpc / G : (lp_ ? gm.kp - 1 : 1);
+    const int pg_hi = lp_ ? lpc / G : (fp_ ? gm.kp - 1 : 0);
+    auto page_src = [&](int page) { return c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + page] * kslot; };
+    // ---- issue every global load first: the page (TMA), the rows, q ----
+    if (tid == 0 && pg_lo <= pg_hi) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        page_fetch(kbuf, page_src(pg_lo), kslot, bar);
+    }
+    const int tk = tid >> 2, qq = tid & 3;
+    const int tt = token_of(c0 + min(tk, cnt - 1));
+    const int pct = tt - S;
+    const bool paged = tt >= S && pct < gm.kp * G;
+    uint4 kw[4], vw[4];
+    {
+        const uint16_t* krow = tt < S ? c.k_sink + ((int64_t)u * S + tt) * D : c.k_qbuf + ((int64_t)u * G + (pct % G)) * D;
+        const uint16_t* vrow = tt < S ? c.v_sink + ((int64_t)u * S + tt) * D : c.v_ring + ((int64_t)u * W + (pct % W)) * D;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (!paged) kw[i] = __ldg(reinterpret_cast<const uint4*>(krow + 32 * qq) + i);
+            vw[i] = __ldg(reinterpret_cast<const uint4*>(vrow + 32 * qq) + i);
+        }
+    }
+    // QK split: warp w -> tokens 16 (w & 1) .., k-steps 4 (w >> 1) .. + 3
+    const int mrow = warp & 1, khalf = warp >> 1;
+    uint32_t qw[8];
+    {
+        const uint16_t* qg = qbase + (gid < GROUP ? gid : 0) * D;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int ch = 16 * (4 * khalf + k) + 2 * tig;
+            qw[2 * k] = __ldg(reinterpret_cast<const uint32_t*>(qg + ch));
+            qw[2 * k + 1] = __ldg(reinterpret_cast<const uint32_t*>(qg + ch + 8));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (!paged) reinterpret_cast<uint4*>(kt + tk * kRowH + 32 * qq)[i] = bf16x8_to_f16x8(kw[i]);
+        reinterpret_cast<uint4*>(vt + tk * kRowH + 32 * qq)[i] = bf16x8_to_f16x8(vw[i]);
+    }
+    // keys that sit in key pages: dequantise into the tile.  thread = (channel
+    // pair cp, token half th); the half's codes come from one shifted 64-bit
+    // window of each channel's code row (16 tokens = 32 bits)
+    if (pg_lo <= pg_hi) {
+        const int cp = tid & 63, th = tid >> 6, d0 = 2 * cp;
+        // chunk token j >= s_len - c0 sits at cache position pct = pbase + j
+        const int jpost = max(0, s_len - c0), pbase = vbase - S + c0 - s_len;
+        for (int page = pg_lo; page <= pg_hi; ++page) {
+            if (page > pg_lo) {
+                __syncthreads();  // kbuf reuse
+                if (tid == 0) page_fetch(kbuf, page_src(page), kslot, bar);
+            }
+            if (tid == 0) page_wait(bar, (page - pg_lo) & 1);
+            __syncthreads();
+            // this half's tokens on this page: j in [jlo, jhi]
+            const int lo_pc = page * G, hi_pc = min(page * G + G, gm.kp * G) - 1;
+            const int jlo = max(max(16 * th, jpost), lo_pc - pbase);
+            const int jhi = min(min(16 * th + 15, cnt - 1), hi_pc - pbase);
+            if (jlo > jhi) continue;
+            const int w = pbase + jlo - lo_pc;  // page-local token of jlo
+            const int word = w >> 4, off = w & 15;
+            const uint32_t sc2 = *reinterpret_cast<const uint32_t*>(kbuf + scale_off + 2 * d0);
+            const uint32_t zr2 = *reinterpret_cast<const uint32_t*>(kbuf + zero_off + 2 * d0);
+            const uint16_t ix2 = *reinterpret_cast<const uint16_t*>(kbuf + D * G / 4 + d_boost * G / 4 + d0);
+            float sc[2], zr[2];
+            uint32_t lo[2], hi[2];
+#pragma unroll
+            for (int k2 = 0; k2 < 2; ++k2) {
+                sc[k2] = half_bits_to_f32(static_cast<uint16_t>(sc2 >> (16 * k2)));
+                zr[k2] = half_bits_to_f32(static_cast<uint16_t>(zr2 >> (16 * k2)));
+                const uint32_t* row = reinterpret_cast<const uint32_t*>(kbuf + (d0 + k2) * (G / 4)) + word;
+                lo[k2] = static_cast<uint32_t>(((static_cast<uint64_t>(row[1]) << 32) | row[0]) >> (2 * off));
+                const uint32_t r = (ix2 >> (8 * k2)) & 0xffu;
+                hi[k2] = 0u;
+                if (r != kSentinel) {
+                    const uint32_t* hrow = reinterpret_cast<const uint32_t*>(kbuf + D * G / 4 + r * (G / 4)) + word;
+                    hi[k2] = static_cast<uint32_t>(((static_cast<uint64_t>(hrow[1]) << 32) | hrow[0]) >> (2 * off));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (jlo + i <= jhi) {
+                    float kv[2];
+#pragma unroll
+                    for (int k2 = 0; k2 < 2; ++k2) {
+                        const uint32_t code = ((lo[k2] >> (2 * i)) & 3u) | (((hi[k2] >> (2 * i)) & 3u) << 2);
+                        // Alg. 1: code * scale + zero (the value the reference attends to)
+                        kv[k2] = __fadd_rn(__fmul_rn(__uint_as_float(code | 0x4b000000u) - 8388608.f, sc[k2]), zr[k2]);
+                    }
+                    *reinterpret_cast<uint32_t*>(kt + (jlo + i) * kRowH + d0) = f2h2(kv[0], kv[1]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t kt_s = static_cast<uint32_t>(__cvta_generic_to_shared(kt));
+    const uint32_t vt_s = static_cast<uint32_t>(__cvta_generic_to_shared(vt));
+    // ---- QK: N = 8 query columns (q alpha as f16 B fragments) ----
+    {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        const int i4 = lane >> 3, r8 = lane & 7;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t w0 = qw[2 * k], w1 = qw[2 * k + 1];
+            const uint32_t b0 = gid < GROUP ? f2h2(__uint_as_float(w0 << 16) * kAlpha, __uint_as_float(w0 & 0xffff0000u) * kAlpha) : 0u;
+            const uint32_t b1 = gid < GROUP ? f2h2(__uint_as_float(w1 << 16) * kAlpha, __uint_as_float(w1 & 0xffff0000u) * kAlpha) : 0u;
+            uint32_t a0, a1, a2, a3;
+            const int row = 16 * mrow + r8 + 8 * (i4 & 1), cc = 16 * (4 * khalf + k) + 8 * (i4 >> 1);
+            ldsm_x4(kt_s + 2 * (row * kRowH + cc), a0, a1, a2, a3);
+            hmma(acc, a0, a1, a2, a3, b0, b1);
+        }
+        // acc: rows (tokens) 16 mrow + gid / + 8, columns 2 tig, 2 tig + 1
+        float* lg = lgs + khalf * kChunk * 8;
+        *reinterpret_cast<float2*>(lg + (16 * mrow + gid) * 8 + 2 * tig) = make_float2(acc[0], acc[1]);
+        *reinterpret_cast<float2*>(lg + (16 * mrow + 8 + gid) * 8 + 2 * tig) = make_float2(acc[2], acc[3]);
+    }
+    __syncthreads();
+    // ---- softmax of the chunk, one warp per query (two passes for group 8) ----
+    const bool valid = lane < cnt;
+#pragma unroll
+    for (int pass = 0; pass < (GROUP + 3) / 4; ++pass) {
+        const int g = 4 * pass + warp;
+        if (g < GROUP) {
+            const float x = valid ? lgs[lane * 8 + g] + lgs[kChunk * 8 + lane * 8 + g] : -INFINITY;
+            float mc = x;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+            const float p = valid ? ex2f(x - mc) : 0.f;
+            float s = p;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            pT[g * kChunk + lane] = __half_as_ushort(__float2half_rn(p));
+            if (lane == 0) {
+                float* base = part + ((int64_t)u * nslot + fc) * stride;
+                base[GROUP * D + 2 * g] = mc;
+                base[GROUP * D + 2 * g + 1] = s;
+            }
+        } else if (g < 8) {
+            pT[g * kChunk + lane] = 0;
+        }
+    }
+    __syncthreads();
+    // ---- PV: warp w -> channels 32 w .. 32 w + 31 (two M tiles), K = 32 tokens ----
+    {
+        float acc[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+        const int i4 = lane >> 3, r8 = lane & 7;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            // B = P [token][query]: b0 = (tokens 16 ks + 2 tig, + 1; query gid)
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(pT + gid * kChunk + 16 * ks + 2 * tig);
+            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(pT + gid * kChunk + 16 * ks + 8 + 2 * tig);
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                // A = V^T [channel][token] via transposed 8x8 loads of V [token][channel]
+                const int tok = 16 * ks + r8 + 8 * (i4 >> 1), chn = 32 * warp + 16 * mt + 8 * (i4 & 1);
+                ldsm_x4_t(vt_s + 2 * (tok * kRowH + chn), a0, a1, a2, a3);
+                hmma(acc[mt], a0, a1, a2, a3, b0, b1);
+            }
+        }
+        float* base = part + ((int64_t)u * nslot + fc) * stride;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            const int ch = 32 * warp + 16 * mt + gid;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int g = 2 * tig + j;
+                if (g < GROUP) {
+                    base[g * D + ch] = acc[mt][j];
+                    base[g * D + ch + 8] = acc[mt][2 + j];
+                }
+            }
+        }
+    }
+}
+
+}  // namespace fptok
+}  // namespace kitty

@@ -25,9 +25,9 @@ def line_map(obj, func):
             continue
         if not inside:
             continue
-        g = re.search(r'line (\d+)', ln) if "//##" in ln else None
+        g = re.search(r'File "([^"]+)", line (\d+)', ln) if "//##" in ln else None
         if g:
-            cur = int(g.group(1))
+            cur = (os.path.basename(g.group(1)), int(g.group(2)))
             continue
         a = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if a and cur is not None:
@@ -50,7 +50,7 @@ def main(rep, obj, func, *roles):
         addr = int(r[0], 16)
         base = addr if base is None else base
         off = addr - base
-        line = lm.get(off, -1)
+        line = lm.get(off, ("?", -1))
         per_line[line][0] += int(r[idx["Warp Stall Sampling (All Samples)"]] or 0)
         per_line[line][1] += int(r[idx["Instructions Executed"]] or 0)
     tot_s = sum(v[0] for v in per_line.values())
@@ -62,7 +62,7 @@ def main(rep, obj, func, *roles):
         spans.append((name, a, b))
     agg = defaultdict(lambda: [0, 0])
     for line, (s, n) in per_line.items():
-        name = next((nm for nm, a, b in spans if a <= line <= b), "other")
+        name = next((nm for nm, a, b in spans if a <= line[1] <= b), "other")
         agg[name][0] += s
         agg[name][1] += n
     print(f"{'role':12s} {'stall samples':>14s} {'%':>6s} {'warp-instr':>12s} {'%':>6s}")
@@ -70,7 +70,7 @@ def main(rep, obj, func, *roles):
         print(f"{name:12s} {s:14d} {100 * s / max(tot_s, 1):6.1f} {n:12d} {100 * n / max(tot_i, 1):6.1f}")
     print("\ntop lines by samples:")
     for line, (s, n) in sorted(per_line.items(), key=lambda kv: -kv[1][0])[:40]:
-        print(f"  line {line:5d}  samples {s:8d} ({100 * s / max(tot_s, 1):5.1f}%)  instr {n:10d}")
+        print(f"  {line[0]}:{line[1]:<5d}  samples {s:8d} ({100 * s / max(tot_s, 1):5.1f}%)  instr {n:10d}")
 
 
 if __name__ == "__main__":
