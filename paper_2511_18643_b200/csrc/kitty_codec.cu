@@ -5,7 +5,10 @@
 // sum in token order (quant.py:72); the quantizer uses IEEE float32 division
 // and round-half-even (quant.py:112-114); dequantisation is multiply-then-add
 // with no FMA contraction (quant.py:120, pages.py:143); f16 metadata is RNE.
+#include <cstdlib>
+
 #include "kitty_codec.cuh"
+#include "kitty_pack_fast.cuh"
 
 namespace kitty {
 
@@ -88,6 +91,20 @@ __device__ void pack_key_tile(const T* tile, int g, int d, int d_boost, const in
             mn = fminf(mn, v);
             mx = fmaxf(mx, v);
         }
+        if (mn == 0.f || mx == 0.f) {
+            // a zero min / max carries the sign of the channel's last zero:
+            // np.minimum.reduce / np.maximum.reduce keep the later operand of a tie
+            float z = 0.f;
+            for (int t = g - 1; t >= 0; --t) {
+                const float v = load_elem(col, t * d);
+                if (v == 0.f) {
+                    z = v;
+                    break;
+                }
+            }
+            mn = mn == 0.f ? z : mn;
+            mx = mx == 0.f ? z : mx;
+        }
         const bool boosted = sc.flag[c] != 0;
         const LaneQuant q(mn, mx, boosted ? 15.f : 3.f);
         const int row = sc.pos[c];
@@ -136,6 +153,18 @@ __device__ void pack_value_tile(const T* tile, int g, int d, uint8_t* slot_smem,
         for (int o = 16; o > 0; o >>= 1) {
             mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (mn == 0.f || mx == 0.f) {  // warp-uniform: the sign of the row's last zero
+            int best = -1;
+            for (int c = lane; c < d; c += 32) {
+                const float v = load_elem(row, c);
+                if (v == 0.f) best = (c << 1) | (signbit(v) ? 1 : 0);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+            const float z = (best & 1) ? -0.f : 0.f;
+            mn = mn == 0.f ? z : mn;
+            mx = mx == 0.f ? z : mx;
         }
         const LaneQuant q(mn, mx, 3.f);
         for (int b = lane; b < db; b += 32) {
@@ -492,6 +521,32 @@ __global__ void prefill_pack_kernel(KittyCacheDesc c, const uint16_t* keys, cons
     }
 }
 
+// The same pages for d = g = 128 (kitty_pack_fast.cuh): 64 threads, one page
+// per CTA, the page's rows by TMA, bytes straight to the slot.
+__global__ void __launch_bounds__(fastpack::kThreads) prefill_pack_fast_kernel(KittyCacheDesc c, const uint16_t* keys,
+                                                                              const uint16_t* values, int P, int kp,
+                                                                              int vp) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    fastpack::Smem& s = *reinterpret_cast<fastpack::Smem*>(smem);
+    const KittyConfigC& k = c.cfg;
+    const int u = blockIdx.y, y = blockIdx.x;
+    const bool is_key = y < kp;
+    const int p = is_key ? y : y - kp;
+    if (!is_key && p >= vp) return;
+    if (p >= c.max_pages) {
+        if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+        return;
+    }
+    const int64_t row0 = (int64_t)u * P + k.s + (int64_t)p * fastpack::kG;
+    if (is_key) {
+        uint8_t* slot = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes;
+        fastpack::key_page(s, keys + row0 * fastpack::kD, k.d_boost, slot, c.status);
+    } else {
+        uint8_t* slot = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes;
+        fastpack::value_page(s, values + row0 * fastpack::kD, slot, c.status);
+    }
+}
+
 // flatten_keys / flatten_values (cache.py:210-215) of one unit.
 __global__ void flatten_kernel(KittyCacheDesc c, int u, int n, float* keys_out, float* values_out) {
     const KittyConfigC& k = c.cfg;
@@ -624,6 +679,12 @@ cudaError_t launch_append(const KittyCacheDesc& c, const uint16_t* k_new, const 
     return cudaGetLastError();
 }
 
+// KITTY_FAST_PACK=0 keeps prefill on the generic packer (A/B and parity knob)
+static const int g_fast_pack = [] {
+    const char* e = std::getenv("KITTY_FAST_PACK");
+    return e ? std::atoi(e) : 1;
+}();
+
 cudaError_t launch_prefill(const KittyCacheDesc& c, const uint16_t* keys, const uint16_t* values,
                            int P, cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
@@ -637,6 +698,14 @@ cudaError_t launch_prefill(const KittyCacheDesc& c, const uint16_t* keys, const 
     prefill_rows_kernel<<<dim3(gx, units), 128, 0, st>>>(c, keys, values, P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || kp + vp == 0) return e;
+    if (c.cfg.d == fastpack::kD && G == fastpack::kG && g_fast_pack) {
+        const int sm = static_cast<int>(sizeof(fastpack::Smem));
+        static cudaError_t attr =
+            cudaFuncSetAttribute(prefill_pack_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        if (attr != cudaSuccess) return attr;
+        prefill_pack_fast_kernel<<<dim3(kp + vp, units), fastpack::kThreads, sm, st>>>(c, keys, values, P, kp, vp);
+        return cudaGetLastError();
+    }
     const size_t sm = pack_smem_bytes(G, c.cfg.d, c.cfg.d_boost, 2);
     cudaFuncSetAttribute(prefill_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     prefill_pack_kernel<<<dim3(kp + vp, units), 128, sm, st>>>(c, keys, values, P, kp, vp);

@@ -83,15 +83,94 @@ def test_prefill_equals_fold_of_inserts(cuda, n):
         assert np.array_equal(bulk.flatten_values(h), stepped.flatten_values(h))
 
 
-def test_prefill_default_shape_matches_reference(cuda, golden):
-    kw, n = _golden_cfg(golden, 3)
+@pytest.mark.parametrize("ci", [3, 4])
+def test_prefill_default_shape_matches_reference(cuda, golden, ci):
+    # d = g = 128: the bulk packer (kitty_pack_fast.cuh) against the reference's bytes
+    kw, n = _golden_cfg(golden, ci)
     cfg = cuda.KittyConfig(**kw)
     st = cuda.KittyCacheState(cfg, max_tokens=n)
-    st.prefill(golden["cache3_keys"], golden["cache3_values"])
+    st.prefill(golden[f"cache{ci}_keys"], golden[f"cache{ci}_values"])
     for h in range(cfg.h_kv):
         kb_, vb_ = st.export_pages(h)
-        assert [a[11:] for a in kb_] == [b.tobytes() for b in golden[f"cache3_h{h}_kpages"]]
-        assert [a[11:] for a in vb_] == [b.tobytes() for b in golden[f"cache3_h{h}_vpages"]]
+        assert [a[11:] for a in kb_] == [b.tobytes() for b in golden[f"cache{ci}_h{h}_kpages"]]
+        assert [a[11:] for a in vb_] == [b.tobytes() for b in golden[f"cache{ci}_h{h}_vpages"]]
+
+
+@pytest.mark.parametrize("frac", [0.0, 0.125, 0.25])
+def test_bulk_packer_matches_append_packer(cuda, frac):
+    # the d = g = 128 bulk packer (prefill) and the per-page packer behind
+    # insert_token must write the same bytes, on adversarial pages: constant
+    # channels / rows (scale 0), tied channel scores, quotients at exact
+    # half-integers (round-half-even), signed zeros, outliers, tiny values
+    cfg = cuda.KittyConfig(s=4, r=128, g=128, d=128, h_kv=2, h_q=4, boost_fraction=frac)
+    rng = np.random.default_rng(77)
+    n = 4 + 3 * 128 + 128 + 9
+    k = rng.normal(0, 1, (2, n, 128)).astype(np.float32)
+    v = rng.normal(0, 1, (2, n, 128)).astype(np.float32)
+    k[:, :, 3] = 0.75                                   # constant channel
+    k[:, :, 9] = k[:, :, 10]                            # tied scores
+    k[:, :, 20] = rng.integers(0, 7, (2, n))            # integer grid: (x - mn) / 2 hits .5
+    k[:, :, 21] = rng.choice([-0.0, 0.0], (2, n))       # signed zeros only
+    k[:, ::37, 30] = 300.0                              # outliers
+    k[:, :, 40] *= 1e-30                                # tiny magnitudes
+    v[:, 50, :] = -1.25                                 # constant row
+    v[:, 60, :] = rng.integers(0, 7, 128)               # half-integer quotients per row
+    v[:, 70, ::2] = -0.0
+    k, v = _bf16(k), _bf16(v)
+    bulk = cuda.KittyCacheState(cfg, max_tokens=n)
+    bulk.prefill(k, v)
+    stepped = cuda.KittyCacheState(cfg, max_tokens=n)
+    for t in range(n):
+        stepped.insert_token(k[:, t], v[:, t])
+    for h in range(2):
+        kb_, vb_ = bulk.export_pages(h)
+        ks_, vs_ = stepped.export_pages(h)
+        assert len(kb_) == 4 and len(vb_) == 3
+        assert kb_ == ks_
+        assert vb_ == vs_
+    # and against the oracle's packer (pages.py:81-118, 146-162)
+    for p in range(4):
+        rows = k[0, 4 + 128 * p: 4 + 128 * (p + 1)]
+        kp = ko.pack_key_page(rows, ko.select_boost(ko.channel_scores(rows), frac))
+        assert bulk.export_pages(0)[0][p][11:] == ko.key_page_body(kp)
+
+
+@pytest.mark.parametrize("d,g", [(8, 8), (128, 128)])
+def test_signed_zero_zero_points(cuda, d, g):
+    # a lane whose min / max is zero stores the sign of its last zero, as
+    # np.minimum.reduce does (quant.py:109); both packers, append and bulk
+    cfg = cuda.KittyConfig(s=2, r=g, g=g, d=d, h_kv=1, h_q=1, boost_fraction=0.25)
+    rng = np.random.default_rng(11)
+    n = 2 + 3 * g + 1
+    k = rng.choice(np.array([0.0, -0.0, 0.5, 1.0], np.float32), (1, n, d))
+    v = rng.choice(np.array([0.0, -0.0, 0.25, -1.0], np.float32), (1, n, d))
+    k[0, :, 1] = rng.choice(np.array([0.0, -0.0], np.float32), n)
+    v[0, 7, :] = rng.choice(np.array([0.0, -0.0], np.float32), d)
+    oc = ko.OracleCache(2, g, g, d, 1, 1, 0.25, metadata16=True)
+    oc.prefill(k[0], v[0])
+    for bulk in (True, False):
+        st = cuda.KittyCacheState(cfg, max_tokens=n)
+        if bulk:
+            st.prefill(k, v)
+        else:
+            for t in range(n):
+                st.insert_token(k[:, t], v[:, t])
+        kb_, vb_ = st.export_pages(0)
+        assert [a[11:] for a in kb_] == [ko.key_page_body(p) for p in oc.heads[0]["kpages"]]
+        assert [a[11:] for a in vb_] == [ko.value_page_body(p) for p in oc.heads[0]["vpages"]]
+
+
+def test_bulk_packer_flags_nonfinite(cuda):
+    cfg = cuda.KittyConfig(s=4, r=128, g=128, d=128, h_kv=1, h_q=1)
+    n = 4 + 2 * 128 + 128
+    rng = np.random.default_rng(5)
+    for where in ("key", "value"):
+        k = _bf16(rng.normal(0, 1, (1, n, 128)))
+        v = _bf16(rng.normal(0, 1, (1, n, 128)))
+        (k if where == "key" else v)[0, 10, 5] = np.nan if where == "key" else np.inf
+        st = cuda.KittyCacheState(cfg, max_tokens=n)
+        with pytest.raises(cuda.KittyError):
+            st.prefill(k, v)
 
 
 def test_attend_after_every_step_boundary_sweep(cuda):
