@@ -461,15 +461,45 @@ __global__ void append_kernel(KittyCacheDesc c, const uint16_t* k_new, const uin
         copy_row_bf16(kq + (int64_t)(pc % G) * d, kr, d);
         copy_row_bf16(vring + (int64_t)(pc % W) * d, vr, d);
     }
-    __syncthreads();
     const int n = t + 1;
     const int past = n > S ? n - S : 0;
-    if (past > 0 && past % G == 0) pack_key_into_cache(c, u, past / G - 1, kq, 0, G, smem);
     const int vtot = past > k.r ? past - k.r : 0;  // tokens that left the local window
-    if (vtot > 0 && vtot % G == 0) {
-        const int p = vtot / G - 1;
+    const bool kpack = past > 0 && past % G == 0, vpack = vtot > 0 && vtot % G == 0;
+    if (d == fastpack::kD && G == fastpack::kG && (kpack || vpack)) {
+        // the bulk packer's routines: the page rows arrive by TMA (async proxy),
+        // so the row this CTA just stored must be visible to it first
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();
-        pack_value_into_cache(c, u, p, vring, (p * G) % W, W, smem);
+        fastpack::Smem& s = *reinterpret_cast<fastpack::Smem*>(smem);
+        if (kpack) {
+            const int p = past / G - 1;
+            if (p >= c.max_pages) {
+                if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+            } else {
+                fastpack::key_page(s, kq, 0, G, k.d_boost,
+                                   c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes,
+                                   c.status);
+            }
+            __syncthreads();
+        }
+        if (vpack) {
+            const int p = vtot / G - 1;
+            if (p >= c.max_pages) {
+                if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+            } else {
+                fastpack::value_page(s, vring, (p * G) % W, W,
+                                     c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes,
+                                     c.status);
+            }
+        }
+    } else {
+        __syncthreads();
+        if (kpack) pack_key_into_cache(c, u, past / G - 1, kq, 0, G, smem);
+        if (vpack) {
+            const int p = vtot / G - 1;
+            __syncthreads();
+            pack_value_into_cache(c, u, p, vring, (p * G) % W, W, smem);
+        }
     }
     if (threadIdx.x == 0) c.unit_len[u] = n;
 }
@@ -540,10 +570,10 @@ __global__ void __launch_bounds__(fastpack::kThreads) prefill_pack_fast_kernel(K
     const int64_t row0 = (int64_t)u * P + k.s + (int64_t)p * fastpack::kG;
     if (is_key) {
         uint8_t* slot = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes;
-        fastpack::key_page(s, keys + row0 * fastpack::kD, k.d_boost, slot, c.status);
+        fastpack::key_page(s, keys + row0 * fastpack::kD, 0, fastpack::kG, k.d_boost, slot, c.status);
     } else {
         uint8_t* slot = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes;
-        fastpack::value_page(s, values + row0 * fastpack::kD, slot, c.status);
+        fastpack::value_page(s, values + row0 * fastpack::kD, 0, fastpack::kG, slot, c.status);
     }
 }
 
@@ -673,9 +703,10 @@ cudaError_t launch_append(const KittyCacheDesc& c, const uint16_t* k_new, const 
                           cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
     if (units == 0) return cudaSuccess;
-    const size_t sm = pack_smem_bytes(c.cfg.g, c.cfg.d, c.cfg.d_boost, 2);
+    size_t sm = pack_smem_bytes(c.cfg.g, c.cfg.d, c.cfg.d_boost, 2);
+    if (c.cfg.d == fastpack::kD && c.cfg.g == fastpack::kG && sm < sizeof(fastpack::Smem)) sm = sizeof(fastpack::Smem);
     cudaFuncSetAttribute(append_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    append_kernel<<<units, 128, sm, st>>>(c, k_new, v_new);
+    append_kernel<<<units, fastpack::kThreads, sm, st>>>(c, k_new, v_new);
     return cudaGetLastError();
 }
 

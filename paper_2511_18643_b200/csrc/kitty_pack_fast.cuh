@@ -32,7 +32,7 @@ struct Smem {
     double score[kD];
     uint8_t row[kD];             // boost row of each channel, kSentinel if not boosted
     float lim[kD][2];            // per-channel (min, max) from pass 1
-    unsigned long long bar;
+    unsigned long long bar[2];   // key page, value page (an append may pack both)
 };
 
 __device__ __forceinline__ uint32_t bmin2(uint32_t a, uint32_t b) {
@@ -93,24 +93,34 @@ __device__ __forceinline__ void split_nibbles(uint32_t x, uint32_t& lo, uint32_t
     hi = (h | (h >> 8)) & 0x0000ffffu;
 }
 
-__device__ __forceinline__ void fetch_tile(Smem& s, const uint16_t* src) {
+// The page's kG rows, rows [start, start + kG) of a ring of `wrap` rows at
+// `base` (prefill: wrap >= start + kG, one copy; the value ring of an
+// append may wrap, two copies), into s.tile by 1-D TMA on barrier `which`.
+__device__ __forceinline__ void fetch_tile(Smem& s, const uint16_t* base, int start, int wrap, int which) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&s.bar[which]));
     if (threadIdx.x == 0) {
-        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&s.bar));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kG * kD * 2) : "memory");
+        const int n1 = min(kG, wrap - start);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 static_cast<uint32_t>(__cvta_generic_to_shared(s.tile))),
-            "l"(src), "r"(kG * kD * 2), "r"(b)
+            "l"(base + (int64_t)start * kD), "r"(n1 * kD * 2), "r"(b)
             : "memory");
+        if (n1 < kG)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    static_cast<uint32_t>(__cvta_generic_to_shared(s.tile + n1 * (kD / 2)))),
+                "l"(base), "r"((kG - n1) * kD * 2), "r"(b)
+                : "memory");
     }
     __syncthreads();
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "FT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-        "@!p bra FT_%=;\n}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s.bar)))
+        "@!p bra FT_%=;\n}" ::"r"(b)
         : "memory");
 }
 
@@ -180,11 +190,12 @@ __device__ __noinline__ float last_zero_key(const uint32_t* tile, int tp, int co
     return 0.f;
 }
 
-// pack_key_page (pages.py:81-118) of the page whose rows start at `src`.
-__device__ void key_page(Smem& s, const uint16_t* src, int d_boost, uint8_t* gslot, uint32_t* status) {
+// pack_key_page (pages.py:81-118) of the page of rows [start, start + kG) of the ring at `base`.
+__device__ void key_page(Smem& s, const uint16_t* base, int start, int wrap, int d_boost, uint8_t* gslot,
+                         uint32_t* status) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tp = tid & 63, half = tid >> 6;
-    fetch_tile(s, src);
+    fetch_tile(s, base, start, wrap, 0);
     bool bad = false;
     if (half == 0) {
         // pass 1: bf16x2 min / max and the fp64 scores of channels 2 tp, 2 tp + 1
@@ -309,9 +320,9 @@ __device__ __noinline__ uint2 slow_value_codes(const uint32_t* tile, int r, int 
 // pack_value_page (pages.py:146-162): per-token quantisation.  Four lanes per
 // token row (32 channels each, 16-byte chunks read in a row-rotated order so a
 // warp's 8 rows hit distinct banks), 32 rows per pass.
-__device__ void value_page(Smem& s, const uint16_t* src, uint8_t* gslot, uint32_t* status) {
+__device__ void value_page(Smem& s, const uint16_t* base, int start, int wrap, uint8_t* gslot, uint32_t* status) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    fetch_tile(s, src);
+    fetch_tile(s, base, start, wrap, 1);
     const ValueLayout L{kD, kG};
     const int q = lane & 3;
     bool bad = false;

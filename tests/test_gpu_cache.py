@@ -98,8 +98,9 @@ def test_prefill_default_shape_matches_reference(cuda, golden, ci):
 
 @pytest.mark.parametrize("frac", [0.0, 0.125, 0.25])
 def test_bulk_packer_matches_append_packer(cuda, frac):
-    # the d = g = 128 bulk packer (prefill) and the per-page packer behind
-    # insert_token must write the same bytes, on adversarial pages: constant
+    # prefill and insert_token (both on the kitty_pack_fast.cuh routines at
+    # d = g = 128, the value ring wrapping) must write the oracle's bytes on
+    # adversarial pages: constant
     # channels / rows (scale 0), tied channel scores, quotients at exact
     # half-integers (round-half-even), signed zeros, outliers, tiny values
     cfg = cuda.KittyConfig(s=4, r=128, g=128, d=128, h_kv=2, h_q=4, boost_fraction=frac)
@@ -129,10 +130,12 @@ def test_bulk_packer_matches_append_packer(cuda, frac):
         assert kb_ == ks_
         assert vb_ == vs_
     # and against the oracle's packer (pages.py:81-118, 146-162)
-    for p in range(4):
-        rows = k[0, 4 + 128 * p: 4 + 128 * (p + 1)]
-        kp = ko.pack_key_page(rows, ko.select_boost(ko.channel_scores(rows), frac))
-        assert bulk.export_pages(0)[0][p][11:] == ko.key_page_body(kp)
+    oc = ko.OracleCache(4, 128, 128, 128, 2, 4, frac, metadata16=True)
+    oc.prefill(k, v)
+    for h in range(2):
+        kb_, vb_ = bulk.export_pages(h)
+        assert [a[11:] for a in kb_] == [ko.key_page_body(p) for p in oc.heads[h]["kpages"]]
+        assert [a[11:] for a in vb_] == [ko.value_page_body(p) for p in oc.heads[h]["vpages"]]
 
 
 @pytest.mark.parametrize("d,g", [(8, 8), (128, 128)])
