@@ -959,10 +959,12 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
 
 template <int GROUP>
 __global__ void __launch_bounds__(kMergeWarps * 32) combine_parts_kernel(Params P) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the fp grid
     const int u = blockIdx.x / GROUP, g = blockIdx.x - (blockIdx.x / GROUP) * GROUP;
     const KittyCacheDesc& c = P.c;
+    // the unit's part list depends only on its length (written by the append,
+    // before the page grid): computed before waiting on the fp grid
     const UnitGeom gm = unit_geom(c, u);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the fp grid (KITTY_PDL bit 2)
     if (gm.n == 0) return;
     const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
     int nch[3];

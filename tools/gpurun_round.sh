@@ -17,6 +17,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:fast
     -o gpurun_out/prof_attn -f python bench.py --steps 1 --warmup 3 --layers 4 --no-cpu-baseline --no-graph > gpurun_out/ncu_full.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fp_tokens|combine" -s 4 -c 2 \
     -o gpurun_out/prof_aux -f python bench.py --steps 1 --warmup 3 --layers 4 --no-cpu-baseline --no-graph > gpurun_out/ncu_aux.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_pack_fast -c 1 \
+    -o gpurun_out/prof_pack -f python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_pack.txt 2>&1
 tail -n 2 gpurun_out/smoke.txt gpurun_out/pytest_gpu.txt
 for f in bench_c2 bench_c1 bench_c3 bench_c4 bench_c5_b32 bench_c2_tc bench_ref; do python -c "
 import json,sys
