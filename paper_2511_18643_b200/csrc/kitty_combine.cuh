@@ -35,6 +35,7 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
     constexpr int T = kMergeWarps * 32;
     __shared__ int s_slot[kMaxParts];
     __shared__ float s_w[kMaxParts];
+    __shared__ float s_l[kMaxParts];
     __shared__ float s_red[kMergeWarps];
     __shared__ float4 s_acc[kMergeWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -43,8 +44,10 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
     for (int i = threadIdx.x; i < nparts; i += T) {
         const int sl = slot_of(i);
         s_slot[i] = sl;
-        const float m = __ldcg(pb + (int64_t)sl * stride + GROUP * D + 2 * g);
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(pb + (int64_t)sl * stride + GROUP * D + 2 * g));
+        const float m = ml.x;
         s_w[i] = m;
+        s_l[i] = ml.y;  // (m, l) in one load: no second round trip for l
         mloc = fmaxf(mloc, m);
     }
 #pragma unroll
@@ -59,7 +62,7 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
         const float m = s_w[i];
         const float w = m == -INFINITY ? 0.f : merge_ex2(m - M);
         s_w[i] = w;
-        lsum = fmaf(w, __ldcg(pb + (int64_t)s_slot[i] * stride + GROUP * D + 2 * g + 1), lsum);
+        lsum = fmaf(w, s_l[i], lsum);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
