@@ -665,7 +665,29 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             }
         }
         __syncwarp();
-        float pacc[8][4];
+        // the output accumulators (TMEM-parked, unweighted: a row's weight class
+        // is the same on every page, so it is applied once at the flush) are
+        // rescaled first when a real column's running max moved (warp vote),
+        // then the P V MMAs accumulate straight into them
+        const bool real0 = kFull || (tig < 2 && 2 * tig < GROUP), real1 = kFull || (tig < 2 && 2 * tig + 1 < GROUP);
+        const bool rescale = __any_sync(0xffffffffu, (real0 && corr[0] != 1.f) || (real1 && corr[1] != 1.f));
+        float oacc[8][4];
+        if (ofresh) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) oacc[m][0] = oacc[m][1] = oacc[m][2] = oacc[m][3] = 0.f;
+        } else {
+            tmem_wait_st();
+            tmem_ld32(taddr, oacc);
+            if (rescale) {
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    oacc[m][0] *= corr[0];
+                    oacc[m][2] *= corr[0];
+                    oacc[m][1] *= corr[1];
+                    oacc[m][3] *= corr[1];
+                }
+            }
+        }
         float vaux[4], vaux2[4];
         const uint8_t* vzero = vscale + 2 * G;
 #pragma unroll
@@ -677,13 +699,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const uint32_t w2 = vw[8 * (t0 + 8) + gid], w3 = vw[8 * (t0 + 9) + gid];
             const uint32_t z0 = lds32(vzero + 2 * t0);
             const uint32_t z1 = lds32(vzero + 2 * (t0 + 8));
-            if (ks == 0) {
-                mma_codes<true>(kc, pacc, w0, w1, w2, w3, b0, b1);
+            mma_codes(kc, oacc, w0, w1, w2, w3, b0, b1);
+            if (ks == 0)
                 mma16816_z(vaux, kOnes, z0, kOnes, z1, b0, b1);
-            } else {
-                mma_codes(kc, pacc, w0, w1, w2, w3, b0, b1);
+            else
                 mma16816(vaux, kOnes, z0, kOnes, z1, b0, b1);
-            }
             if (kFull) {  // the unscaled p (rows 8-15 of P^T): sum p and sum p z
                 const uint32_t c0u = sm.u.pt[8 + gid][8 * ks + (tig ^ ks)];
                 const uint32_t c1u = sm.u.pt[8 + gid][8 * ks + ((tig + 4) ^ ks)];
@@ -695,18 +715,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         }
         // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z).
         // Row constants (zero points, the 1024 offset) accumulate per column in
-        // ob[weight class] and are added at the flush; the accumulators are only
-        // rescaled when a running max of a real column moved (warp vote).
-        const bool real0 = kFull || (tig < 2 && 2 * tig < GROUP), real1 = kFull || (tig < 2 && 2 * tig + 1 < GROUP);
-        const bool rescale = __any_sync(0xffffffffu, (real0 && corr[0] != 1.f) || (real1 && corr[1] != 1.f));
-        float oacc[8][4];
-        if (ofresh) {
-#pragma unroll
-            for (int m = 0; m < 8; ++m) oacc[m][0] = oacc[m][1] = oacc[m][2] = oacc[m][3] = 0.f;
-        } else {
-            tmem_wait_st();
-            tmem_ld32(taddr, oacc);
-        }
+        // ob[weight class] and are added at the flush.
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const float sBv = __shfl_sync(0xffffffffu, vaux[j], kFull ? tig : (tig & 1));
@@ -718,18 +727,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             ob[1][j] = fmaf(ob[1][j], corr[j], zz - 256.f * sBv);
             ob[2][j] = fmaf(ob[2][j], corr[j], zz - 64.f * sBv);
             ob[3][j] = fmaf(ob[3][j], corr[j], zz - 16.f * sBv);
-            if (rescale) {
-#pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    oacc[m][j] *= corr[j];
-                    oacc[m][2 + j] *= corr[j];
-                }
-            }
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                oacc[m][j] = fmaf(pacc[m][j], (m & 1) ? 1.f / 16.f : 1.f / 256.f, oacc[m][j]);
-                oacc[m][2 + j] = fmaf(pacc[m][2 + j], (m & 1) ? 1.f / 64.f : 1.f / 4.f, oacc[m][2 + j]);
-            }
             om[j] = mnew[j];
         }
         tmem_st32(taddr, oacc);
@@ -813,8 +810,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
                             for (int m = 0; m < 8; ++m)
                                 *reinterpret_cast<float2*>(base + g * D + 16 * gid + 2 * m) =
-                                    make_float2(oacc[m][j] + ob[(m & 1) ? 2 : 0][j],
-                                                oacc[m][2 + j] + ob[(m & 1) ? 3 : 1][j]);
+                                    make_float2(fmaf(oacc[m][j], (m & 1) ? 1.f / 16.f : 1.f / 256.f, ob[(m & 1) ? 2 : 0][j]),
+                                                fmaf(oacc[m][2 + j], (m & 1) ? 1.f / 64.f : 1.f / 4.f, ob[(m & 1) ? 3 : 1][j]));
                             if (gid == 0) {
                                 base[GROUP * D + 2 * g] = om[j];
                                 base[GROUP * D + 2 * g + 1] = ol[j];
@@ -881,8 +878,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
 #pragma unroll
                             for (int m = 0; m < 8; ++m)
                                 *reinterpret_cast<float2*>(base + g * D + 16 * gid + 2 * m) =
-                                    make_float2(oacc[m][j] + ob[(m & 1) ? 2 : 0][j],
-                                                oacc[m][2 + j] + ob[(m & 1) ? 3 : 1][j]);
+                                    make_float2(fmaf(oacc[m][j], (m & 1) ? 1.f / 16.f : 1.f / 256.f, ob[(m & 1) ? 2 : 0][j]),
+                                                fmaf(oacc[m][2 + j], (m & 1) ? 1.f / 64.f : 1.f / 4.f, ob[(m & 1) ? 3 : 1][j]));
                             if (gid == 0) {
                                 base[GROUP * D + 2 * g] = om[j];
                                 base[GROUP * D + 2 * g + 1] = ol[j];
