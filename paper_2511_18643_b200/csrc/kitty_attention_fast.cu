@@ -47,12 +47,19 @@ constexpr int kWarps = 4;         // warps per CTA
 #ifndef KITTY_FAST_CTAS
 #define KITTY_FAST_CTAS 3
 #endif
-// Staging: 2-stage (key, value) page-pair ring per warp at 8 warps / SM, or one
-// key slot + one value slot per warp, each refilled as soon as it is consumed,
-// at 4 * KITTY_FAST_CTAS warps / SM.
+#ifndef KITTY_FAST_HALF
+#define KITTY_FAST_HALF 0
+#endif
+// Staging: 2-stage (key, value) page-pair ring per warp at 8 warps / SM; or
+// (KITTY_FAST_HALF) two key slots + one value slot per warp at 12 warps / SM,
+// the next value page loaded while the next key page's QK runs; or one key
+// slot + one value slot per warp, each refilled as soon as it is consumed, at
+// 4 * KITTY_FAST_CTAS warps / SM.
 constexpr bool kSingle = KITTY_FAST_SINGLE != 0;
-constexpr int kStages = kSingle ? 1 : 2;
-constexpr int kCtasPerSm = kSingle ? KITTY_FAST_CTAS : 2;
+constexpr bool kHalf = !kSingle && KITTY_FAST_HALF != 0;
+constexpr int kStages = kSingle ? 1 : 2;  // key slots per warp
+constexpr int kVStages = (kSingle || kHalf) ? 1 : 2;
+constexpr int kCtasPerSm = kSingle ? KITTY_FAST_CTAS : (kHalf ? 3 : 2);
 constexpr int kTmemCols = 64;      // per CTA; per warp (its TMEM lane quarter): [0,32) output accumulators, [32,48) q fragments
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
@@ -63,21 +70,26 @@ constexpr float kAlpha = 0.12751743074f;  // log2(e) / sqrt(128)
 constexpr uint32_t kMagic = 0x64006400u;  // f16x2 (1024, 1024)
 constexpr uint32_t kOnes = 0x3C003C00u;   // f16x2 (1, 1)
 
-// Per-warp shared memory (23 KB): a 2-stage ring of (key page, value page)
-// slots; the pair for page i+1 is in flight (cp.async.bulk) while page i is
-// computed.  Sized so that two page CTAs leave room on the SM for one fp-token
-// CTA (the programmatic dependent grid) from the start.
+// Per-warp shared memory: this fixed part, then the page slots -- kStages key
+// slots and kVStages value slots, sized by the cache's slot bytes at launch
+// (warp_bytes), so that a 5 248-byte key page costs no more than that.
 template <int PT_ROWS>
-struct __align__(128) WarpSmemT {
-    uint8_t kbuf[kStages][kKeySlotMax];  // KTYP key bodies
-    uint8_t vbuf[kStages][kValueSlot];   // KTYP value bodies
+struct __align__(16) WarpFixedT {
     struct {
         uint32_t pt[PT_ROWS][kPtStride / 2];  // P^T as f16x2: p*s per query, then p (rows 4-7 / 8-15 for group 4 / 8)
     } u;
     uint32_t ones[64];            // f16x2 (1, 1): scale operand of the aux B columns
     uint8_t inv[32];              // boosted channel of high_bits row j
-    unsigned long long mbar[2];   // one per stage
+    unsigned long long mbar[3];   // 2-stage: one per stage; single / half: key slot(s), value slot
 };
+template <int GROUP>
+__host__ __device__ constexpr int warp_fixed_bytes() {
+    return static_cast<int>((sizeof(WarpFixedT<GROUP == 8 ? 16 : 8>) + 127) & ~size_t(127));
+}
+template <int GROUP>
+__host__ __device__ inline int warp_smem_bytes(int kslot, int vslot) {
+    return (warp_fixed_bytes<GROUP>() + kStages * kslot + kVStages * vslot + 127) & ~127;
+}
 
 struct Params {
     KittyCacheDesc c;
@@ -354,8 +366,12 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    using WarpSmem = WarpSmemT<GROUP == 8 ? 16 : 8>;
-    WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+    using WarpFixed = WarpFixedT<GROUP == 8 ? 16 : 8>;
+    const int wbytes = warp_smem_bytes<GROUP>(static_cast<int>(P.c.key_slot_bytes), static_cast<int>(P.c.value_slot_bytes));
+    uint8_t* wbase = smem_raw + warp * wbytes;
+    WarpFixed& sm = *reinterpret_cast<WarpFixed*>(wbase);
+    uint8_t* const kslots = wbase + warp_fixed_bytes<GROUP>();
+    uint8_t* const vslots = kslots + kStages * static_cast<int>(P.c.key_slot_bytes);
     const KittyCacheDesc& c = P.c;
     const int S = c.cfg.s, W = c.cfg.r + c.cfg.g;
     const int d_boost = c.cfg.d_boost;
@@ -379,6 +395,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     if (lane == 0) {
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
+        mbar_init(&sm.mbar[2], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     asm volatile("griddepcontrol.launch_dependents;");
     // per-CTA copy of the unit lengths: the queue decode reads them from shared
     // memory instead of paying a global round trip per work item
-    int* s_ulen = reinterpret_cast<int*>(smem_raw + sizeof(WarpSmem) * kWarps);  // dynamic, units entries
+    int* s_ulen = reinterpret_cast<int*>(smem_raw + wbytes * kWarps);  // dynamic, units entries
     const bool len_table = P.units <= kMaxTableUnits;
     if (len_table) {
         for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = c.unit_len[i];
@@ -501,8 +518,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             const uint8_t* ks = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * kslot;
             const uint8_t* vs = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * vslot;
             mbar_expect_tx(&sm.mbar[st], kslot + vslot);
-            bulk_g2s(sm.kbuf[st], ks, kslot, &sm.mbar[st]);
-            bulk_g2s(sm.vbuf[st], vs, vslot, &sm.mbar[st]);
+            bulk_g2s(kslots + st * kslot, ks, kslot, &sm.mbar[st]);
+            bulk_g2s(vslots + st * vslot, vs, vslot, &sm.mbar[st]);
         }
         __syncwarp();
         ++issued;
@@ -543,7 +560,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     float mnew[2], corr[2], bw[4][2];
 
     auto qk_page = [&](int st) {
-        const uint8_t* kp = sm.kbuf[st];
+        const uint8_t* kp = kslots + st * kslot;
         const uint32_t* kw = reinterpret_cast<const uint32_t*>(kp);
         // boosted rows -> channels (inverse of boost_idx)
         if (NKH > 0) {
@@ -646,7 +663,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     };
 
     auto pv_page = [&](int st) {
-        const uint8_t* vp = sm.vbuf[st];
+        const uint8_t* vp = vslots + st * vslot;
         const uint32_t* vw = reinterpret_cast<const uint32_t*>(vp);
         const uint8_t* vscale = vp + G * D / 4;
         // P^T -> shared (rows 0-3: p * s_token, rows 4-7: p), tokens 16 gid + 2m (+1)
@@ -739,7 +756,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         if (lane == 0) {
             const uint8_t* ks = c.key_pool + (int64_t)c.key_block_table[(int64_t)u_ * c.max_pages + p_] * kslot;
             mbar_expect_tx(&sm.mbar[0], kslot);
-            bulk_g2s(sm.kbuf[0], ks, kslot, &sm.mbar[0]);
+            bulk_g2s(kslots, ks, kslot, &sm.mbar[0]);
         }
         __syncwarp();
     };
@@ -747,7 +764,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
         if (lane == 0) {
             const uint8_t* vs = c.value_pool + (int64_t)c.value_block_table[(int64_t)u_ * c.max_pages + p_] * vslot;
             mbar_expect_tx(&sm.mbar[1], vslot);
-            bulk_g2s(sm.vbuf[0], vs, vslot, &sm.mbar[1]);
+            bulk_g2s(vslots, vs, vslot, &sm.mbar[1]);
         }
         __syncwarp();
     };
@@ -830,8 +847,101 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             if (kind != 0) next_item(nkind, nu, np0, np1);
         }
     }
+    // half mode: key slots ring on mbar[0..1] (kiss / kcon), the value slot on mbar[2]
+    uint32_t kiss = 0;
+    auto issue_kh = [&](int u_, int p_) {
+        const int ks_ = kiss & 1;
+        if (lane == 0) {
+            const uint8_t* src = c.key_pool + (int64_t)c.key_block_table[(int64_t)u_ * c.max_pages + p_] * kslot;
+            mbar_expect_tx(&sm.mbar[ks_], kslot);
+            bulk_g2s(kslots + ks_ * kslot, src, kslot, &sm.mbar[ks_]);
+        }
+        __syncwarp();
+        ++kiss;
+    };
+    auto issue_vh = [&](int u_, int p_) {
+        if (lane == 0) {
+            const uint8_t* src = c.value_pool + (int64_t)c.value_block_table[(int64_t)u_ * c.max_pages + p_] * vslot;
+            mbar_expect_tx(&sm.mbar[2], vslot);
+            bulk_g2s(vslots, src, vslot, &sm.mbar[2]);
+        }
+        __syncwarp();
+    };
 #pragma unroll 1
-    while (!kSingle && kind != 0) {
+    while (kHalf && kind != 0) {
+        bool item_done;
+        {
+            if (p == p0) {
+                if (!kpend) issue_kh(u, p0);
+                if (!vpend) issue_vh(u, p0);
+                kpend = vpend = false;
+                load_unit(u);
+                om[0] = om[1] = -INFINITY;
+                ol[0] = ol[1] = 0.f;
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) ob[c4][0] = ob[c4][1] = 0.f;
+                ofresh = true;
+            }
+            // the next key page into the other key slot right away; the next
+            // value page once this one is consumed (it lands during the next QK)
+            const bool more = p + 1 < p1;
+            const bool chain = !more && nkind == 2;
+            if (more) issue_kh(u, p + 1);
+            if (chain) {
+                issue_kh(nu, np0);
+                kpend = true;
+            }
+            const int ks_ = kcon & 1;
+            mbar_wait(&sm.mbar[ks_], (kcon >> 1) & 1);
+            ++kcon;
+            qk_page(ks_);
+            mbar_wait(&sm.mbar[2], vcon & 1);
+            ++vcon;
+            pv_page(0);
+            __syncwarp();
+            if (more) issue_vh(u, p + 1);
+            if (chain) {
+                issue_vh(nu, np0);
+                vpend = true;
+            }
+            ++p;
+            item_done = p == p1;
+            if (item_done) {
+                const int slot = page_slot(p0, geom(u).vp);
+                float* base = P.part + ((int64_t)u * P.nslot + slot) * part_stride(GROUP);
+                float oacc[8][4];
+                tmem_wait_st();
+                tmem_ld32(taddr, oacc);
+                if (kFull || tig < 2) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int g = 2 * tig + j;
+                        if (g < GROUP) {
+#pragma unroll
+                            for (int m = 0; m < 8; ++m)
+                                *reinterpret_cast<float2*>(base + g * D + 16 * gid + 2 * m) =
+                                    make_float2(fmaf(oacc[m][j], (m & 1) ? 1.f / 16.f : 1.f / 256.f, ob[(m & 1) ? 2 : 0][j]),
+                                                fmaf(oacc[m][2 + j], (m & 1) ? 1.f / 64.f : 1.f / 4.f, ob[(m & 1) ? 3 : 1][j]));
+                            if (gid == 0) {
+                                base[GROUP * D + 2 * g] = om[j];
+                                base[GROUP * D + 2 * g + 1] = ol[j];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (item_done) {
+            kind = nkind;
+            u = nu;
+            p0 = np0;
+            p1 = np1;
+            p = p0;
+            if (kind != 0) next_item(nkind, nu, np0, np1);
+        }
+    }
+#pragma unroll 1
+    while (!kSingle && !kHalf && kind != 0) {
         bool item_done;
         {
             if (p == p0) {
@@ -1064,10 +1174,28 @@ static const int g_pdl = [] {
 template <int GROUP, int NKH>
 static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     auto kfn = fast_attention_kernel<GROUP, NKH>;
-    const size_t sm = sizeof(WarpSmemT<GROUP == 8 ? 16 : 8>) * kWarps + (prm.units <= kMaxTableUnits ? 4 * prm.units : 0);
+    const size_t sm = (size_t)warp_smem_bytes<GROUP>((int)prm.c.key_slot_bytes, (int)prm.c.value_slot_bytes) * kWarps +
+                      (prm.units <= kMaxTableUnits ? 4 * prm.units : 0);
     static cudaError_t attr = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)(sizeof(WarpSmemT<GROUP == 8 ? 16 : 8>) * kWarps + 4 * kMaxTableUnits));  // once per instantiation
+                                                   (int)(warp_smem_bytes<GROUP>(kKeySlotMax, kValueSlot) * kWarps +
+                                                         4 * kMaxTableUnits));  // once per instantiation
     if (attr != cudaSuccess) return attr;
+    static cudaError_t carve =
+        cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    if (carve != cudaSuccess) return carve;
+    // persistent grid: kCtasPerSm CTAs per SM must be co-resident (their shared
+    // memory, the 1 KB per-CTA reservation and the static part fit the SM), else
+    // one fewer per SM.  (cudaOccupancyMaxActiveBlocksPerMultiprocessor reports
+    // 1 for this kernel on B200 at any shared-memory size, so it is not used.)
+    static int smpm = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        return v;
+    }();
+    int per_sm = kCtasPerSm;
+    while (per_sm > 1 && (size_t)per_sm * (sm + 128 + 1024) > (size_t)smpm) --per_sm;
+    if (grid > num_sms() * per_sm) grid = num_sms() * per_sm;
     // the pages first; the fp-token chunks as a programmatic dependent of the
     // page grid, so their CTAs backfill SMs as persistent page CTAs retire (the
     // fp grid waits on the page grid only before it exits); then the merge
