@@ -59,7 +59,10 @@ constexpr bool kSingle = KITTY_FAST_SINGLE != 0;
 constexpr bool kHalf = !kSingle && KITTY_FAST_HALF != 0;
 constexpr int kStages = kSingle ? 1 : 2;  // key slots per warp
 constexpr int kVStages = (kSingle || kHalf) ? 1 : 2;
-constexpr int kCtasPerSm = kSingle ? KITTY_FAST_CTAS : (kHalf ? 3 : 2);
+#ifndef KITTY_HALF_CTAS
+#define KITTY_HALF_CTAS 3
+#endif
+constexpr int kCtasPerSm = kSingle ? KITTY_FAST_CTAS : (kHalf ? KITTY_HALF_CTAS : 2);
 constexpr int kTmemCols = 64;      // per CTA; per warp (its TMEM lane quarter): [0,32) output accumulators, [32,48) q fragments
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
@@ -336,13 +339,16 @@ struct UnitGeom {
 // pieces and no SM idles behind a long item (swept on B200 with
 // tools/sweep_sched.sh).  Level boundaries are per-mille of vp (tuning knobs,
 // set once by the host plan; KITTY_SCHED overrides them for sweeps).
-__constant__ int c_lvl[2] = {850, 950};
-static int h_lvl[2] = {850, 950};
+// Units of >= 512 pages (128K-token contexts) take the second pair: their
+// tails are long enough that a larger level 0 wins (C4 45.9 -> 44.0 us per
+// layer; C2 / C3, 254 / 62 pages per unit, keep 850 / 950).
+__constant__ int c_lvl[4] = {850, 950, 880, 960};
+static int h_lvl[4] = {850, 950, 880, 960};
 __host__ __device__ __forceinline__ int level_begin(int lv, int vp) {
 #ifdef __CUDA_ARCH__
-    const int* lvl = c_lvl;
+    const int* lvl = c_lvl + (vp >= 512 ? 2 : 0);
 #else
-    const int* lvl = h_lvl;
+    const int* lvl = h_lvl + (vp >= 512 ? 2 : 0);
 #endif
     return lv == 0 ? 0 : (lv == 1 ? (vp * lvl[0]) / 1000 : (lv == 2 ? (vp * lvl[1]) / 1000 : vp));
 }
@@ -1134,6 +1140,8 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
         inited = 1;
         if (const char* e = getenv("KITTY_SCHED")) {  // experiments: "l1,l2,ppc_max,cs1_div"
             sscanf(e, "%d,%d,%d,%d", &h_lvl[0], &h_lvl[1], &ppc_max, &cs1_div);
+            h_lvl[2] = h_lvl[0];  // a sweep sets one pair for every unit length
+            h_lvl[3] = h_lvl[1];
             cudaMemcpyToSymbol(c_lvl, h_lvl, sizeof(h_lvl));
         }
     }
@@ -1144,8 +1152,15 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     p.cs[0] = ppc;
     p.cs[1] = ppc / cs1_div > 1 ? ppc / cs1_div : 1;
     p.cs[2] = 1;
+    // chunk bound per level over every unit length up to maxp: level sizes grow
+    // with vp within one split rule (+2 absorbs the floor rounding), and the
+    // rule switches at 512 pages, so both sides of the switch are evaluated
     for (int lv = 0; lv < 3; ++lv) {
-        const int n = level_begin(lv + 1, maxp) - level_begin(lv, maxp) + 2;
+        int n = level_begin(lv + 1, maxp) - level_begin(lv, maxp) + 2;
+        if (maxp >= 512) {
+            const int n2 = level_begin(lv + 1, 511) - level_begin(lv, 511) + 2;
+            n = n2 > n ? n2 : n;
+        }
         p.cmx[lv] = (n + p.cs[lv] - 1) / p.cs[lv];
     }
     const int nfp_max = min(max_tokens, c.cfg.s + c.cfg.r + c.cfg.g - 1);

@@ -359,6 +359,31 @@ def test_decode_loop_matches_oracle(cuda, kernel):
 
 
 @pytest.mark.parametrize("group", [4, 8])
+def test_long_units_on_both_schedule_rules(cuda, group):
+    # units of >= 512 pages take the other level split (kitty_attention_fast.cu
+    # level_begin): a ragged batch straddling the switch (70 000 / 65 000 /
+    # 20 000 tokens = 546 / 507 / 155 pages), attention against dense fp32
+    # attention over the cache's own dequantised rows (flatten, a15)
+    rng = np.random.default_rng(3 + group)
+    h_kv, h_q = 1, group
+    lens = [70000, 65000, 20000]
+    cfg = cuda.KittyConfig(h_kv=h_kv, h_q=h_q)
+    k = torch.randn(len(lens), h_kv, max(lens), 128).bfloat16()
+    v = torch.randn(len(lens), h_kv, max(lens), 128).bfloat16()
+    cache = cuda.KittyBatchCache(cfg, len(lens), max(lens) + 8)
+    cache.prefill(k, v, lengths=lens)
+    q = torch.randn(len(lens), h_q, 128).bfloat16()
+    out = cache.attend(q.cuda()).float().cpu().numpy()
+    cache.check()
+    for bi in range(len(lens)):
+        kf, vf = (t.double() for t in cache.flatten(bi, 0))
+        logits = (q[bi].double().cuda() @ kf.T) / np.sqrt(128.0)
+        p = torch.softmax(logits, dim=-1)
+        ref = (p @ vf).float().cpu().numpy()
+        assert np.max(np.abs(out[bi] - ref)) <= 1e-2, bi
+
+
+@pytest.mark.parametrize("group", [4, 8])
 def test_ragged_batch_matches_oracle(cuda, kernel, group):
     # a ragged batch -- every sequence has its own length,
     # page count and pack triggers -- through prefill, decode steps and attend
