@@ -257,6 +257,10 @@ def run_kitty(args):
     e2.record()
     cp.wait_stream(main)
 
+    # tiny steps (C1: 12 KB in) are host-bound: staging and events cost more than
+    # the copies they hide, so those copy straight through on the compute stream
+    pipelined = step.input_bytes() > (1 << 20)
+
     def h2d(i):
         with torch.cuda.stream(cp):
             if i >= 2:
@@ -265,8 +269,15 @@ def run_kitty(args):
                 dst.copy_(src, non_blocking=True)
             in_ready[i % 2].record(cp)
 
-    h2d(0)
-    for i in range(e_steps):
+    if not pipelined:
+        for i in range(e_steps):
+            step.k_in.copy_(host_k[i], non_blocking=True)
+            step.v_in.copy_(host_v[i], non_blocking=True)
+            step.q_in.copy_(host_q[i], non_blocking=True)
+            step.step()
+            host_out[i].copy_(step.out, non_blocking=True)
+    h2d(0) if pipelined else None
+    for i in range(e_steps if pipelined else 0):
         if i + 1 < e_steps:
             h2d(i + 1)
         main.wait_event(in_ready[i % 2])
@@ -332,7 +343,8 @@ def run_kitty(args):
             "value": round(e2e_tps, 2), "unit": "tokens/s",
             "h2d_bytes_per_step": step.input_bytes(), "d2h_bytes_per_step": step.output_bytes(),
             "steps": e_steps,
-            "copies": "pinned host <-> device every step, pipelined on a copy stream (step i+1 H2D and step i D2H overlap compute)",
+            "copies": ("pinned host <-> device every step, pipelined on a copy stream (step i+1 H2D and step i D2H overlap compute)"
+                       if pipelined else "pinned host <-> device every step, on the compute stream"),
         },
         "gpu_launches": launches,
         "clocks": clk,

@@ -7,6 +7,9 @@ timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/p
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c2.txt 2>&1
 timeout 600 python bench.py --config c1 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c1.txt 2>&1
 timeout 600 python bench.py --config c3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.txt 2>&1
+for b in 0 0.0625 0.25; do  # BASELINE C3 boost fractions (0.125 is bench_c3)
+  timeout 600 python bench.py --config c3 --boost $b --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3_b$b.txt 2>&1
+done
 timeout 900 python bench.py --config c5 --batch 32 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5_b32.txt 2>&1
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --kernel tc > gpurun_out/bench_c2_tc.txt 2>&1
 timeout 600 python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4.txt 2>&1
@@ -20,7 +23,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fp_
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_pack_fast -c 1 \
     -o gpurun_out/prof_pack -f python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_pack.txt 2>&1
 tail -n 2 gpurun_out/smoke.txt gpurun_out/pytest_gpu.txt
-for f in bench_c2 bench_c1 bench_c3 bench_c4 bench_c5_b32 bench_c2_tc bench_ref; do python -c "
+for f in bench_c2 bench_c1 bench_c3 bench_c3_b0 bench_c3_b0.0625 bench_c3_b0.25 bench_c4 bench_c5_b32 bench_c2_tc bench_ref; do python -c "
 import json,sys
 try:
     d=json.loads(open('gpurun_out/$f.txt').read().strip().splitlines()[-1]); r=d.get('roofline',{})
