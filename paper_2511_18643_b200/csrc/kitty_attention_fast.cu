@@ -1070,8 +1070,10 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-template <int GROUP>
-__global__ void __launch_bounds__(kMergeWarps * 32) combine_parts_kernel(Params P) {
+// WARPS warps merge one (unit, query row): 8 for long part lists, 2 when a
+// unit has <= 32 partial slots (short contexts: many small CTAs, one wave)
+template <int GROUP, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
     const int u = blockIdx.x / GROUP, g = blockIdx.x - (blockIdx.x / GROUP) * GROUP;
     const KittyCacheDesc& c = P.c;
     // the unit's part list depends only on its length (written by the append,
@@ -1095,7 +1097,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) combine_parts_kernel(Params 
     };
     const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
     const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
-    lse_merge_row<GROUP>(P.part + (int64_t)u * P.nslot * kStride, kStride, nparts, slot_of, g, P.out, P.out_dtype, row);
+    lse_merge_row<GROUP, decltype(slot_of), WARPS>(P.part + (int64_t)u * P.nslot * kStride, kStride, nparts, slot_of, g,
+                                                  P.out, P.out_dtype, row);
 }
 
 }  // namespace fastattn
@@ -1245,11 +1248,15 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(prm.units * GROUP);
-        cfg.blockDim = dim3(kMergeWarps * 32);
         cfg.stream = st;
         cfg.attrs = at + 2;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP>, prm);
+        if (prm.nslot <= 32) {
+            cfg.blockDim = dim3(2 * 32);
+            return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 2>, prm);
+        }
+        cfg.blockDim = dim3(kMergeWarps * 32);
+        return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, kMergeWarps>, prm);
     }
 }
 

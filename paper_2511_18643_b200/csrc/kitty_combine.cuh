@@ -28,16 +28,17 @@ __device__ __forceinline__ float merge_ex2(float x) {
 // 8 rows' loads in flight).  The index arithmetic per row is a few
 // instructions -- the merge was instruction-bound on it (ncu) before.
 constexpr int kMaxParts = 1024;
-template <int GROUP, class SlotFn>
+template <int GROUP, class SlotFn, int WARPS = kMergeWarps>
 __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int nparts, SlotFn slot_of, int g,
                                               void* out, int out_dtype, int64_t row) {
     constexpr int D = 128;
-    constexpr int T = kMergeWarps * 32;
+    constexpr int T = WARPS * 32;
+    constexpr int F = WARPS < 4 ? 16 : 8;  // accumulator rows in flight per warp
     __shared__ int s_slot[kMaxParts];
     __shared__ float s_w[kMaxParts];
     __shared__ float s_l[kMaxParts];
-    __shared__ float s_red[kMergeWarps];
-    __shared__ float4 s_acc[kMergeWarps][32];
+    __shared__ float s_red[WARPS];
+    __shared__ float4 s_acc[WARPS][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (nparts > kMaxParts) nparts = kMaxParts;  // host plans keep nslot far below
     float mloc = -INFINITY;
@@ -56,7 +57,7 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
     __syncthreads();
     float M = s_red[0];
 #pragma unroll
-    for (int w = 1; w < kMergeWarps; ++w) M = fmaxf(M, s_red[w]);
+    for (int w = 1; w < WARPS; ++w) M = fmaxf(M, s_red[w]);
     float lsum = 0.f;
     for (int i = threadIdx.x; i < nparts; i += T) {
         const float m = s_w[i];
@@ -70,18 +71,18 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
     if (lane == 0) s_red[warp] = lsum;
     const float* rowp = pb + g * D + 4 * lane;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i0 = warp; i0 < nparts; i0 += 8 * kMergeWarps) {
-        float4 a[8];
-        float w[8];
+    for (int i0 = warp; i0 < nparts; i0 += F * WARPS) {
+        float4 a[F];
+        float w[F];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int i = i0 + j * kMergeWarps;
+        for (int j = 0; j < F; ++j) {
+            const int i = i0 + j * WARPS;
             const bool ok = i < nparts;
             w[j] = ok ? s_w[i] : 0.f;
             a[j] = ok ? __ldcg(reinterpret_cast<const float4*>(rowp + (int64_t)s_slot[i] * stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < F; ++j) {
             acc.x = fmaf(w[j], a[j].x, acc.x);
             acc.y = fmaf(w[j], a[j].y, acc.y);
             acc.z = fmaf(w[j], a[j].z, acc.z);
@@ -94,7 +95,7 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
     float4 o = s_acc[0][lane];
     float lt = s_red[0];
 #pragma unroll
-    for (int w = 1; w < kMergeWarps; ++w) {
+    for (int w = 1; w < WARPS; ++w) {
         const float4 x = s_acc[w][lane];
         o.x += x.x;
         o.y += x.y;
