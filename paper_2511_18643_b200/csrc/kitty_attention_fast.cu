@@ -1239,7 +1239,7 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(prm.units * prm.fmax);
         cfg.blockDim = dim3(128);
-        cfg.dynamicSmemBytes = fptok::tc_scratch_bytes<GROUP>();
+        cfg.dynamicSmemBytes = fptok::tc_scratch_bytes((int)prm.c.key_slot_bytes);
         cfg.stream = st;
         cfg.attrs = at + 1;
         cfg.numAttrs = 1;

@@ -457,10 +457,12 @@ namespace fptok {
 // mma.sync.m16n8k16 with ldmatrix operands.  One 128-thread CTA per chunk. ----
 constexpr int kRowH = D + 8;  // f16 per staged row (272 B: conflict-free ldmatrix)
 
-template <int GROUP>
-__host__ __device__ constexpr int tc_scratch_bytes() {
-    return kKeySlotMax + 2 * kChunk * kRowH * 2 + 2 * kChunk * 8 * 4 + 8 * kChunk * 2 + 64;
-}
+// Scratch of one chunk CTA: the key page (key_slot_bytes, 16-aligned; the
+// logits and P^T reuse it once the page is dequantised), the f16 key and
+// value tiles and the page barrier -- ~22 KB at d_boost 16, so two chunk CTAs
+// fit beside the page kernel's two CTAs on an SM.
+__host__ __device__ inline int tc_kbuf_bytes(int kslot) { return (kslot + 127) & ~127; }
+__host__ __device__ inline int tc_scratch_bytes(int kslot) { return tc_kbuf_bytes(kslot) + 2 * kChunk * kRowH * 2 + 64; }
 
 __device__ __forceinline__ uint32_t f2h2(float lo, float hi) {
     uint32_t r;
@@ -520,11 +522,13 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
     const int kslot = static_cast<int>(c.key_slot_bytes);
     const int scale_off = D * G / 4 + d_boost * G / 4 + D, zero_off = scale_off + 2 * D;
     uint8_t* kbuf = scratch;
-    uint16_t* kt = reinterpret_cast<uint16_t*>(scratch + kKeySlotMax);   // [32][kRowH] f16 keys
-    uint16_t* vt = kt + kChunk * kRowH;                                   // [32][kRowH] f16 values
-    float* lgs = reinterpret_cast<float*>(vt + kChunk * kRowH);           // [2][32][8] logit halves
-    uint16_t* pT = reinterpret_cast<uint16_t*>(lgs + 2 * kChunk * 8);      // [8][32] f16 probabilities
-    uint64_t* bar = reinterpret_cast<uint64_t*>(pT + 8 * kChunk);
+    uint16_t* kt = reinterpret_cast<uint16_t*>(scratch + tc_kbuf_bytes(kslot));  // [32][kRowH] f16 keys
+    uint16_t* vt = kt + kChunk * kRowH;                                          // [32][kRowH] f16 values
+    uint64_t* bar = reinterpret_cast<uint64_t*>(vt + kChunk * kRowH);
+    // after the dequantisation (a __syncthreads) the key page is dead: logits
+    // and P^T live in its bytes (2.5 KB <= the slot)
+    float* lgs = reinterpret_cast<float*>(kbuf);                   // [2][32][8] logit halves
+    uint16_t* pT = reinterpret_cast<uint16_t*>(lgs + 2 * kChunk * 8);  // [8][32] f16 probabilities
     const Geom gm = geom(c, u);
     const int s_len = min(gm.n, S);
     const int c0 = fc * kChunk;
