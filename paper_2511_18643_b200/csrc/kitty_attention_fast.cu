@@ -1072,7 +1072,8 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
 
 // WARPS warps merge one (unit, query row): 2 when a unit has <= 32 partial
 // slots (short contexts: many small CTAs, one wave); 4 when 8-warp CTAs would
-// need more than one wave and a unit has <= 128 slots; else 8
+// need more than one wave and a unit has <= 128 slots; 16 above 128 slots
+// (long contexts); else 8
 template <int GROUP, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
     const int u = blockIdx.x / GROUP, g = blockIdx.x - (blockIdx.x / GROUP) * GROUP;
@@ -1260,6 +1261,10 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
         if (prm.nslot <= 128 && (long long)prm.units * GROUP * kMergeWarps > 48LL * num_sms()) {
             cfg.blockDim = dim3(4 * 32);
             return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 4>, prm);
+        }
+        if (prm.nslot > 128) {  // long contexts: few rows, hundreds of parts each
+            cfg.blockDim = dim3(16 * 32);
+            return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 16>, prm);
         }
         cfg.blockDim = dim3(kMergeWarps * 32);
         return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, kMergeWarps>, prm);

@@ -33,7 +33,7 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
                                               void* out, int out_dtype, int64_t row) {
     constexpr int D = 128;
     constexpr int T = WARPS * 32;
-    constexpr int F = WARPS < 8 ? 16 : 8;  // accumulator rows in flight per warp
+    constexpr int F = WARPS == 8 ? 8 : 16;  // accumulator rows in flight per warp
     __shared__ int s_slot[kMaxParts];
     __shared__ float s_w[kMaxParts];
     __shared__ float s_l[kMaxParts];

@@ -1,4 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; tail -1 gpurun_out/pytest_gpu.txt
-bash tools/ab.sh exp/libMw5.so exp/libFpSm.so --config c3 | tail -4
-bash tools/ab.sh exp/libMw5.so exp/libFpSm.so | tail -2
-bash tools/ab.sh exp/libMw5.so exp/libFpSm.so --config c5 --batch 32 | tail -2
+bash tools/ab.sh exp/libFpSm.so exp/libMw16.so --config c4 | tail -4
