@@ -104,6 +104,7 @@ struct Params {
     int fmax;   // fp-token chunk items per unit (grid bound)
     int cs[3];    // page-chunk size of schedule level 0 / 1 / 2
     int cmx[3];   // chunks per unit bound of each level
+    int lvl[4];   // level 1 / 2 starts in per mille of vp: units < 512 pages, >= 512 pages
     int nslot;    // partial slots per unit: fmax + cmx[0] + cmx[1] + cmx[2]
     int units;
     uint32_t units_mul, units_shift;  // fast division by units (quotient = (umulhi(n, mul) + n) >> shift)
@@ -339,17 +340,13 @@ struct UnitGeom {
 // pieces and no SM idles behind a long item (swept on B200 with
 // tools/sweep_sched.sh).  Level boundaries are per-mille of vp (tuning knobs,
 // set once by the host plan; KITTY_SCHED overrides them for sweeps).
-// Units of >= 512 pages (128K-token contexts) take the second pair: their
-// tails are long enough that a larger level 0 wins (C4 45.9 -> 44.0 us per
-// layer; C2 / C3, 254 / 62 pages per unit, keep 850 / 950).
-__constant__ int c_lvl[4] = {850, 950, 880, 960};
+// Level starts per mille of vp, one pair for units below 512 pages and one
+// from 512 pages on (128K-token contexts have tails long enough that a larger
+// level 0 wins: C4 45.9 -> 44.0 us per layer).  The host plan passes them per
+// launch (Params::lvl), after quantising level 0 to whole rounds of the warps.
 static int h_lvl[4] = {850, 950, 880, 960};
-__host__ __device__ __forceinline__ int level_begin(int lv, int vp) {
-#ifdef __CUDA_ARCH__
-    const int* lvl = c_lvl + (vp >= 512 ? 2 : 0);
-#else
-    const int* lvl = h_lvl + (vp >= 512 ? 2 : 0);
-#endif
+__host__ __device__ __forceinline__ int level_begin(int lv, int vp, const int* lvl4) {
+    const int* lvl = lvl4 + (vp >= 512 ? 2 : 0);
     return lv == 0 ? 0 : (lv == 1 ? (vp * lvl[0]) / 1000 : (lv == 2 ? (vp * lvl[1]) / 1000 : vp));
 }
 
@@ -493,7 +490,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
             p1 = 0;
             kind = (gm.n > 0 && ch * kFpChunk < gm.nfp) ? 1 : 3;
         } else {
-            const int lb = level_begin(sect, gm.vp), le = level_begin(sect + 1, gm.vp);
+            const int lb = level_begin(sect, gm.vp, P.lvl), le = level_begin(sect + 1, gm.vp, P.lvl);
             p0 = lb + ch * P.cs[sect];
             p1 = min(le, p0 + P.cs[sect]);
             kind = (p0 < p1 && gm.n > 0) ? 2 : 3;
@@ -501,13 +498,13 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     };
     // partial slot of the page chunk starting at p0, and the chunk count of a unit
     auto page_slot = [&](int p0_, int vp) {
-        const int lv = p0_ < level_begin(1, vp) ? 0 : (p0_ < level_begin(2, vp) ? 1 : 2);
-        int slot = P.fmax + (p0_ - level_begin(lv, vp)) / P.cs[lv];
+        const int lv = p0_ < level_begin(1, vp, P.lvl) ? 0 : (p0_ < level_begin(2, vp, P.lvl) ? 1 : 2);
+        int slot = P.fmax + (p0_ - level_begin(lv, vp, P.lvl)) / P.cs[lv];
         for (int l = 0; l < lv; ++l) slot += P.cmx[l];
         return slot;
     };
     auto page_chunks = [&](int lv, int vp) {
-        const int n = level_begin(lv + 1, vp) - level_begin(lv, vp);
+        const int n = level_begin(lv + 1, vp, P.lvl) - level_begin(lv, vp, P.lvl);
         return (n + P.cs[lv] - 1) / P.cs[lv];
     };
     auto next_item = [&](int& kind, int& u, int& p0, int& p1) {
@@ -1086,7 +1083,7 @@ __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
     const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
     int nch[3];
     for (int lv = 0; lv < 3; ++lv) {
-        const int n = level_begin(lv + 1, gm.vp) - level_begin(lv, gm.vp);
+        const int n = level_begin(lv + 1, gm.vp, P.lvl) - level_begin(lv, gm.vp, P.lvl);
         nch[lv] = (n + P.cs[lv] - 1) / P.cs[lv];
     }
     const int nparts = nfc + nch[0] + nch[1] + nch[2];
@@ -1128,7 +1125,7 @@ bool fast_attention_supported(const KittyCacheDesc& c) {
 }
 
 struct FastPlan {
-    int ppc, cmax, fmax, units, group, cs[3], cmx[3], nslot;
+    int ppc, cmax, fmax, units, group, cs[3], cmx[3], lvl[4], nslot;
     size_t ctr_bytes, part_bytes;
 };
 
@@ -1147,7 +1144,6 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
             sscanf(e, "%d,%d,%d,%d", &h_lvl[0], &h_lvl[1], &ppc_max, &cs1_div);
             h_lvl[2] = h_lvl[0];  // a sweep sets one pair for every unit length
             h_lvl[3] = h_lvl[1];
-            cudaMemcpyToSymbol(c_lvl, h_lvl, sizeof(h_lvl));
         }
     }
     int ppc = static_cast<int>(pages / (2 * warps));
@@ -1157,13 +1153,33 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     p.cs[0] = ppc;
     p.cs[1] = ppc / cs1_div > 1 ? ppc / cs1_div : 1;
     p.cs[2] = 1;
+    // Level 0 in whole rounds: its items (ppc pages each, for units at the
+    // longest length) are pulled round by round by the `warps` warps; when
+    // there are only 1-2 whole rounds and the last would be nearly empty
+    // (< 35 %), a few warps would start one more long item -- a large share of
+    // a warp's work -- as everyone else runs out, so level 0 shrinks to the
+    // whole rounds (C4: 2.03 rounds; with 3+ rounds, C3 / C5, the cut costs
+    // more than the tail it removes).
+    for (int i = 0; i < 4; ++i) p.lvl[i] = h_lvl[i];
+    {
+        const int past_m = max_tokens > c.cfg.s ? max_tokens - c.cfg.s : 0;
+        const int vpm = (past_m - min(c.cfg.r, past_m)) / G;
+        const int rule = vpm >= 512 ? 2 : 0;
+        const int l0 = (vpm * p.lvl[rule]) / 1000;
+        const long long items0 = (long long)p.units * ((l0 + ppc - 1) / ppc);
+        const long long rounds = items0 / warps, rest = items0 - rounds * warps;
+        if (vpm > 0 && rounds >= 1 && rounds < 3 && rest * 100 < 35 * warps) {
+            const int l0n = static_cast<int>((rounds * warps) / p.units) * ppc;
+            if (l0n > 0 && l0n < l0) p.lvl[rule] = static_cast<int>((long long)l0n * 1000 / vpm);
+        }
+    }
     // chunk bound per level over every unit length up to maxp: level sizes grow
     // with vp within one split rule (+2 absorbs the floor rounding), and the
     // rule switches at 512 pages, so both sides of the switch are evaluated
     for (int lv = 0; lv < 3; ++lv) {
-        int n = level_begin(lv + 1, maxp) - level_begin(lv, maxp) + 2;
+        int n = level_begin(lv + 1, maxp, p.lvl) - level_begin(lv, maxp, p.lvl) + 2;
         if (maxp >= 512) {
-            const int n2 = level_begin(lv + 1, 511) - level_begin(lv, 511) + 2;
+            const int n2 = level_begin(lv + 1, 511, p.lvl) - level_begin(lv, 511, p.lvl) + 2;
             n = n2 > n ? n2 : n;
         }
         p.cmx[lv] = (n + p.cs[lv] - 1) / p.cs[lv];
@@ -1294,6 +1310,7 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
         prm.cs[lv] = p.cs[lv];
         prm.cmx[lv] = p.cmx[lv];
     }
+    for (int i = 0; i < 4; ++i) prm.lvl[i] = p.lvl[i];
     prm.nslot = p.nslot;
     prm.units = p.units;
     {

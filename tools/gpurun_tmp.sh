@@ -1,4 +1,3 @@
-for c in c2 c3 c4; do for m in 3 7 3 7; do
-KITTY_PDL=$m KITTY_B200_LIB=exp/libCur.so timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > /tmp/ab.txt 2>&1
-python -c "import json; d=json.loads(open('/tmp/ab.txt').read().strip().splitlines()[-1]); print('$c pdl=$m', d['value'], d['roofline']['avg_launch_ms'])"
-done; done
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; tail -1 gpurun_out/pytest_gpu.txt
+bash tools/ab.sh exp/libCur.so exp/libWave2.so --config c4 | tail -4
+bash tools/ab.sh exp/libCur.so exp/libWave2.so --config c3 | tail -2
