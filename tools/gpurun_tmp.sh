@@ -1,5 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; tail -1 gpurun_out/pytest_gpu.txt
-bash tools/ab.sh exp/libWave2.so exp/libMpre.so | tail -4
-bash tools/ab.sh exp/libWave2.so exp/libMpre.so --config c3 | tail -2
-bash tools/ab.sh exp/libWave2.so exp/libMpre.so --config c4 | tail -2
-bash tools/ab.sh exp/libWave2.so exp/libMpre.so --config c5 --batch 32 | tail -2
+rm -f gpurun_out/sweep.txt
+SCHEDS="880,960,8,4 800,950,8,4 750,930,8,4 700,900,8,4 650,900,8,4 600,880,8,4" bash tools/sweep_sched.sh --config c4
