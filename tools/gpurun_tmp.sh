@@ -1,2 +1,1 @@
-rm -f gpurun_out/sweep.txt
-SCHEDS="880,960,8,4 800,950,8,4 750,930,8,4 700,900,8,4 650,900,8,4 600,880,8,4" bash tools/sweep_sched.sh --config c4
+timeout 900 python -m pytest tests/test_gpu_knobs.py -m gpu -q -p no:cacheprovider 2>&1 | tail -15
