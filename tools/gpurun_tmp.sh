@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_knobs.py -m gpu -q -p no:cacheprovider 2>&1 | tail -15
+bash tools/ab.sh exp/libWave2.so exp/libF16.so | tail -4
+bash tools/ab.sh exp/libWave2.so exp/libF16.so --config c4 | tail -2
