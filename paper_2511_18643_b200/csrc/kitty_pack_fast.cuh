@@ -23,7 +23,7 @@ namespace kitty {
 namespace fastpack {
 
 constexpr int kD = 128, kG = 128;
-constexpr int kThreads = 128;  // keys: pass 1 on warps 0-1 (channel pairs), pass 2 on all four (token halves)
+constexpr int kThreads = 128;  // keys: thread = (channel pair, half); pass 1 scores one channel each, pass 2 a token half
 constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
 constexpr uint32_t kMagicBits = 0x4B400000u;
 
@@ -196,22 +196,26 @@ __device__ void key_page(Smem& s, const uint16_t* base, int start, int wrap, int
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tp = tid & 63, half = tid >> 6;
     fetch_tile(s, base, start, wrap, 0);
-    bool bad = false;
+    // pass 1: the fp64 score of channel 2 tp + half (each chain sequential in
+    // token order, quant.py:72), and on warps 0-1 the bf16x2 min / max of both
+    // channels of the pair
+    uint32_t mn2 = s.tile[tp], mx2 = mn2;
+    double a = 0.0;
     if (half == 0) {
-        // pass 1: bf16x2 min / max and the fp64 scores of channels 2 tp, 2 tp + 1
-        uint32_t mn2 = s.tile[tp], mx2 = mn2;
-        double a0 = 0.0, a1 = 0.0;
 #pragma unroll 8
         for (int t = 0; t < kG; ++t) {
             const uint32_t w = s.tile[t * 64 + tp];
             mn2 = bmin2(mn2, w);
             mx2 = bmax2(mx2, w);
-            a0 += static_cast<double>(fabsf(lo_f(w)));
-            a1 += static_cast<double>(fabsf(hi_f(w)));
+            a += static_cast<double>(fabsf(lo_f(w)));
         }
-        s.score[2 * tp] = a0 / static_cast<double>(kG);
-        s.score[2 * tp + 1] = a1 / static_cast<double>(kG);
-        bad = !(fabs(a0) < INFINITY) || !(fabs(a1) < INFINITY);
+    } else {
+#pragma unroll 8
+        for (int t = 0; t < kG; ++t) a += static_cast<double>(fabsf(hi_f(s.tile[t * 64 + tp])));
+    }
+    s.score[2 * tp + half] = a / static_cast<double>(kG);
+    const bool bad = !(fabs(a) < INFINITY);
+    if (half == 0) {
         float mn0 = lo_f(mn2), mx0 = lo_f(mx2), mn1 = hi_f(mn2), mx1 = hi_f(mx2);
         if (mn0 == 0.f || mx0 == 0.f) {
             const float z = last_zero_key(s.tile, tp, 0);
