@@ -358,6 +358,34 @@ def test_decode_loop_matches_oracle(cuda, kernel):
     assert cache.value_pack_events[0] == oc.value_pack_events
 
 
+def test_merge_width_tiers(cuda):
+    # the split-KV merge picks its CTA width from the partial-slot count and
+    # the grid size (kitty_attention_fast.cu launch_t): 64 sequences x 8 KV
+    # heads at group 2 and ~16K tokens give 1 024 (unit, row) CTAs with 33-128
+    # slots each -> the 4-warp tier; sampled units against dense attention
+    # over the cache's own dequantised rows
+    torch.manual_seed(7)
+    B, h_kv, h_q = 64, 8, 16
+    lens = [16000 + 37 * (b % 9) for b in range(B)]
+    cfg = cuda.KittyConfig(h_kv=h_kv, h_q=h_q)
+    cache = cuda.KittyBatchCache(cfg, B, max(lens) + 8)
+    k = torch.randn(B, h_kv, max(lens), 128, device="cuda").bfloat16()
+    v = torch.randn(B, h_kv, max(lens), 128, device="cuda").bfloat16()
+    cache.prefill(k, v, lengths=lens)
+    del k, v
+    q = torch.randn(B, h_q, 128).bfloat16()
+    out = cache.attend(q.cuda()).float().cpu().numpy()
+    cache.check()
+    g = h_q // h_kv
+    for b in (0, 21, 63):
+        for h in (0, 5):
+            kf, vf = (t.double() for t in cache.flatten(b, h))
+            qq = q[b, h * g:(h + 1) * g].double().cuda()
+            p = torch.softmax((qq @ kf.T) / np.sqrt(128.0), dim=-1)
+            ref = (p @ vf).float().cpu().numpy()
+            assert np.max(np.abs(out[b, h * g:(h + 1) * g] - ref)) <= 1e-2, (b, h)
+
+
 @pytest.mark.parametrize("group", [4, 8])
 def test_long_units_on_both_schedule_rules(cuda, group):
     # units of >= 512 pages take the other level split (kitty_attention_fast.cu

@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "bulk_packer or prefill or signed_zero or golden or knobs" 2>&1 | tail -1
-for L in exp/libWave2.so exp/libPk.so; do KITTY_B200_LIB=$L timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:prefill_pack_fast -c 3 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | grep duration | awk -v l=$L '{print l, $NF}'; done
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "merge_width or long_units" 2>&1 | tail -3
