@@ -40,7 +40,10 @@ constexpr int D = 128;
 constexpr int G = 128;
 // floats per partial record (acc[group][D], then (m, l) per row), padded to 16 B
 __host__ __device__ constexpr int part_stride(int group) { return (group * (D + 2) + 3) & ~3; }
-constexpr int kWarps = 4;         // warps per CTA
+#ifndef KITTY_FAST_WARPS
+#define KITTY_FAST_WARPS 4
+#endif
+constexpr int kWarps = KITTY_FAST_WARPS;  // warps per CTA (a fifth warp shares lane quarter 0 at TMEM column 64)
 #ifndef KITTY_FAST_SINGLE
 #define KITTY_FAST_SINGLE 0
 #endif
@@ -63,7 +66,7 @@ constexpr int kVStages = (kSingle || kHalf) ? 1 : 2;
 #define KITTY_HALF_CTAS 3
 #endif
 constexpr int kCtasPerSm = kSingle ? KITTY_FAST_CTAS : (kHalf ? KITTY_HALF_CTAS : 2);
-constexpr int kTmemCols = 64;      // per CTA; per warp (its TMEM lane quarter): [0,32) output accumulators, [32,48) q fragments
+constexpr int kTmemCols = kWarps > 4 ? 128 : 64;  // per CTA; per warp (its TMEM lane quarter, + 64 columns for warps 4-7): [0,32) output accumulators, [32,48) q fragments
 constexpr int kKeySlotMax = 5760;  // d_boost = 32
 constexpr int kValueSlot = 4608;
 constexpr int kPtStride = 136;     // f16 per row of the transposed-P buffer
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t taddr = tmem_base_sh + (static_cast<uint32_t>(32 * warp) << 16);
+    const uint32_t taddr = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + 64u * (warp >> 2);
     sm.inv[lane] = 0;
     sm.ones[lane] = kOnes;
     sm.ones[lane + 32] = kOnes;
