@@ -6,11 +6,11 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c2.txt 2>&1
 timeout 600 python bench.py --config c1 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c1.txt 2>&1
-timeout 600 python bench.py --config c3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.txt 2>&1
+timeout 600 python bench.py --config c3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.txt 2>&1
 for b in 0 0.0625 0.25; do  # BASELINE C3 boost fractions (0.125 is bench_c3)
-  timeout 600 python bench.py --config c3 --boost $b --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3_b$b.txt 2>&1
+  timeout 600 python bench.py --config c3 --boost $b --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3_b$b.txt 2>&1
 done
-timeout 900 python bench.py --config c5 --batch 32 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5_b32.txt 2>&1
+timeout 900 python bench.py --config c5 --batch 32 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5_b32.txt 2>&1
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --kernel tc > gpurun_out/bench_c2_tc.txt 2>&1
 timeout 600 python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4.txt 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.txt 2>&1
