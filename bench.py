@@ -136,7 +136,6 @@ def run_kitty(args):
     if args.boost is not None:
         frac = args.boost
     cfg = kb.KittyConfig(h_kv=h_kv, h_q=h_q, boost_fraction=frac)
-    kb.select_attention_kernel(args.kernel)
     steps, warmup = args.steps, args.warmup
     max_tokens = ctx + warmup + steps + 2 * (warmup + steps) + 8
     gen = torch.Generator(device=dev)
@@ -154,9 +153,8 @@ def run_kitty(args):
             nb = min(chunk, batch - b0)
             k = (torch.randn((nb, cfg.h_kv, ctx, cfg.d), generator=gen, device=dev) * gain).bfloat16()
             v = torch.randn((nb, cfg.h_kv, ctx, cfg.d), generator=gen, device=dev).bfloat16()
-            _prefill_slice(cache, b0, nb, k, v)
+            cache.prefill_range(b0, nb, k, v)
             del k, v
-        cache.lengths = [ctx] * batch
     torch.cuda.synchronize()
     prefill_s = time.time() - t0
     for c in step.layers:
@@ -359,11 +357,6 @@ def run_kitty(args):
         dist.destroy_process_group()
 
 
-def _prefill_slice(cache, b0, nb, k, v):
-    """Prefill sequences [b0, b0 + nb) of a layer cache through the C ABI."""
-    cache.prefill_range(b0, nb, k, v)
-
-
 def _ncu_traffic(config):
     """DRAM bytes per attention launch from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -499,8 +492,6 @@ def main():
     ap.add_argument("--boost", type=float, default=None)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--kernel", choices=["default", "tc"], default="default",
-                    help="decode-attention kernel (experiments): default dispatch or the tcgen05 kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -42,6 +42,8 @@ typedef enum KittyStatus {
 #define KITTY_STATUS_NONFINITE 0x1u   /* pages.py:88-89,152-153: non-finite page input */
 #define KITTY_STATUS_PAGE_FORMAT 0x2u /* pages.py:128-135: sentinel count / bijection   */
 #define KITTY_STATUS_OVERFLOW 0x4u    /* append past the block-table capacity          */
+#define KITTY_STATUS_LENGTH 0x8u      /* a unit is longer than the attention call's
+                                         max_tokens (its tokens beyond it were not read) */
 
 /* Element types for inputs that the reference accepts as float32. */
 #define KITTY_F32 0
@@ -192,13 +194,6 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv,
 
 /* ---- debug / experiments (not part of the reference interface) ------- */
 
-/* Select the decode-attention kernel: 0 = default dispatch (mma.sync kernel
- * for GQA groups <= 4, tcgen05 kernel for group 8), 1 = the tcgen05 kernel
- * wherever it applies.  Process-wide; not thread-safe. */
-int kitty_debug_select_attention(int impl);
-/* Event timeline of CTA 0 of the tcgen05 kernel: enable != 0 records the next
- * launches; host_out (optional) receives max_rows x 16 int64 timestamps. */
-int kitty_debug_tc_trace(int enable, long long* host_out, int max_rows);
 /* Per-warp trace of the mma.sync kernel (same convention, 10 fields). */
 int kitty_debug_attention_trace(int enable, long long* host_out, int max_warps);
 

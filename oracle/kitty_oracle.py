@@ -441,6 +441,46 @@ class OracleCache:
         return [key_page_body(p) for p in hd["kpages"]], [value_page_body(p) for p in hd["vpages"]]
 
 
+def bulk_unit_state(keys, values, s, r, g, boost_fraction=0.125, metadata16=True):
+    """The state one KV head holds after the fold of insert_token over ``keys`` /
+    ``values`` (n, d) (cache.py:107-142), built directly from the occupancy
+    closed form (analysis.py:301-315) instead of token by token: key pages
+    are rows [s + i g, s + (i + 1) g) packed with their own magnitude
+    selection (cache.py:155-161), value pages the same rows of the values
+    (cache.py:168-174: the value q-buffer receives tokens in order once they
+    leave the local window).  Returns (flat_keys, flat_values, key_bodies,
+    value_bodies); the flattened rows follow cache.py:196-215.  For long
+    contexts (10^5 tokens) where the per-token fold is too slow; the fold's
+    equality with this is checked in tests/test_oracle.py."""
+    keys = np.asarray(keys, np.float32)
+    values = np.asarray(values, np.float32)
+    n, d = keys.shape
+    c = component_counts(s, r, g, n)
+    kp, vp = c["key_pages"], c["value_pages"]
+    kflat, vflat, kb, vb = [keys[: c["sink"]]], [values[: c["sink"]]], [], []
+    for i in range(kp):
+        block = keys[s + i * g : s + (i + 1) * g]
+        page = pack_key_page(block, select_boost(channel_scores(block), boost_fraction))
+        kb.append(key_page_body(page))
+        shown = f16_roundtrip(page) if metadata16 else page
+        kflat.append(np.ascontiguousarray(dequantize_key_page(shown).T))
+    kflat.append(keys[s + kp * g :])
+    for i in range(vp):
+        page = pack_value_page(values[s + i * g : s + (i + 1) * g])
+        vb.append(value_page_body(page))
+        shown = f16_roundtrip(page) if metadata16 else page
+        vflat.append(dequantize_value_page(shown))
+    vflat.append(values[s + vp * g :])
+    return np.concatenate(kflat, axis=0), np.concatenate(vflat, axis=0), kb, vb
+
+
+def attend_rows(keys, values, qg) -> np.ndarray:
+    """cache.py:240-248 for one KV head: qg (group, d) against flattened rows."""
+    sqrt_d = np.float32(np.sqrt(keys.shape[1]))
+    logits = (np.asarray(keys, np.float32) @ np.asarray(qg, np.float32).T) / sqrt_d
+    return softmax_columns(logits).T @ np.asarray(values, np.float32)
+
+
 def softmax_columns(logits: np.ndarray) -> np.ndarray:
     """cache.py:255-258."""
     shifted = logits - logits.max(axis=0, keepdims=True)

@@ -7,7 +7,7 @@ runs in ``libkitty_b200.so`` (hand-written sm_100a CUDA behind a C ABI,
 include/kitty_b200.h); there is no CPU fallback.
 """
 
-from ._lib import exported_symbols, load_library, select_attention_kernel
+from ._lib import exported_symbols, load_library
 from .analysis import MemoryReport, algorithmic_bytes_per_unit, measure_cache_bytes, memory_report
 from .cache import AttentionOutput, KittyBatchCache, KittyCacheState, component_counts, oracle_attend
 from .config import PASSTHROUGH_BITS, KittyConfig, boost_count, config_from_mapping
@@ -58,5 +58,5 @@ __all__ = [
     "dequant_value_pages", "dequantize_key_page", "dequantize_value_page", "deserialize_page",
     "exported_symbols", "load_library", "measure_cache_bytes", "memory_report", "oracle_attend",
     "pack_key_page", "pack_key_pages", "pack_value_page", "pack_value_pages", "page_byte_size",
-    "select_attention_kernel", "select_boost", "select_boost_batch", "serialize_page", "serialize_slot",
+    "select_boost", "select_boost_batch", "serialize_page", "serialize_slot",
 ]

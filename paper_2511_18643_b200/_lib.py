@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KITTY_B200_LIB") or os.path.join(_HERE, "libkitty_b200.so")
 
 KITTY_OK, KITTY_ERR_CONFIG, KITTY_ERR_INVALID, KITTY_ERR_PAGE_FORMAT, KITTY_ERR_CUDA, KITTY_ERR_UNSUPPORTED = range(6)
-STATUS_NONFINITE, STATUS_PAGE_FORMAT, STATUS_OVERFLOW = 1, 2, 4
+STATUS_NONFINITE, STATUS_PAGE_FORMAT, STATUS_OVERFLOW, STATUS_LENGTH = 1, 2, 4, 8
 KITTY_F32, KITTY_BF16 = 0, 1
 
 c_int32 = ctypes.c_int32
@@ -80,8 +80,6 @@ SIGNATURES = [
     ("kitty_dense_attention_workspace_bytes", c_size_t, [c_int32, c_int32, c_int32]),
     ("kitty_dense_attention", ctypes.c_int,
      [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
-    ("kitty_debug_select_attention", ctypes.c_int, [ctypes.c_int]),
-    ("kitty_debug_tc_trace", ctypes.c_int, [ctypes.c_int, c_void_p, ctypes.c_int]),
     ("kitty_debug_attention_trace", ctypes.c_int, [ctypes.c_int, c_void_p, ctypes.c_int]),
 ]
 
@@ -135,13 +133,9 @@ def raise_status(word: int, what: str = "") -> None:
         raise KittyError(f"{what}: page contains non-finite values")
     if word & STATUS_OVERFLOW:
         raise KittyError(f"{what}: cache capacity (block table) exceeded")
+    if word & STATUS_LENGTH:
+        raise KittyError(f"{what}: a sequence is longer than the max_tokens bound passed to attention")
     raise KittyError(f"{what}: device status 0x{word:x}")
-
-
-def select_attention_kernel(impl: str) -> None:
-    """Experiments: "default" (mma.sync kernel for GQA groups <= 4, tcgen05 for
-    group 8) or "tc" (the tcgen05 kernel wherever it applies)."""
-    check(load_library().kitty_debug_select_attention({"default": 0, "tc": 1}[impl]), "select attention")
 
 
 def exported_symbols() -> list[str]:

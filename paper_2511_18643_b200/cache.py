@@ -178,20 +178,23 @@ class KittyBatchCache:
         values = self._rows(values, (self.num_seqs, cfg.h_kv, p, cfg.d), "values")
         if all(x == p for x in lengths):
             _lib.check(self.lib.kitty_prefill(self._desc_ref, keys.data_ptr(), values.data_ptr(), p, _stream()), "prefill")
+            for b in range(self.num_seqs):
+                self._set_length(b, p)
         else:
             for b, n in enumerate(lengths):
                 if n:
                     self.prefill_range(b, 1, keys[b:b + 1, :, :n], values[b:b + 1, :, :n])
-        for b, n in enumerate(lengths):
-            for i in range(1, n + 1):
-                self._count_events(b, i)
-            self.lengths[b] = n
 
     def prefill_range(self, b0: int, nb: int, keys: torch.Tensor, values: torch.Tensor):
-        """kitty_prefill of sequences [b0, b0 + nb) through a sub-descriptor that
-        aliases this batch's buffers (keys/values [nb, h_kv, P, D] bf16 on the
-        device).  Does not update the host length mirror."""
+        """kitty_prefill of the empty sequences [b0, b0 + nb) through a
+        sub-descriptor that aliases this batch's buffers (keys/values
+        [nb, h_kv, P, D] bf16 on the device): the host length mirror and the
+        pack-event counters of those sequences become P."""
         cfg = self.cfg
+        if any(self.lengths[b0:b0 + nb]):
+            raise KittyError("prefill requires empty sequences")
+        if keys.shape[2] > self.max_tokens:
+            raise KittyError(f"prefill of {keys.shape[2]} tokens exceeds the capacity {self.max_tokens}")
         u0 = b0 * cfg.h_kv
         d = _lib.KittyCacheDesc()
         ctypes.memmove(ctypes.byref(d), ctypes.byref(self.desc), ctypes.sizeof(d))
@@ -210,6 +213,17 @@ class KittyBatchCache:
         kc, vc = keys.contiguous(), values.contiguous()
         _lib.check(self.lib.kitty_prefill(ctypes.byref(d), kc.data_ptr(), vc.data_ptr(), keys.shape[2], _stream()),
                    "prefill")
+        for b in range(b0, b0 + nb):
+            self._set_length(b, keys.shape[2])
+
+    def _set_length(self, b: int, n: int):
+        """Host mirror after a prefill of n tokens: the pack events of the fold
+        of n inserts (one per full key / value page, cache.py:144-178)."""
+        cfg = self.cfg
+        past = max(0, n - cfg.s)
+        self.lengths[b] = n
+        self.key_pack_events[b] = past // cfg.g
+        self.value_pack_events[b] = max(0, past - cfg.r) // cfg.g
 
     def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.bfloat16) -> torch.Tensor:
         """Step 2 for every sequence: q [B, h_q, D] bf16 -> [B, h_q, D]."""
@@ -230,9 +244,14 @@ class KittyBatchCache:
         return out
 
     def check(self):
-        """Synchronise and raise for any data-dependent error a kernel reported."""
+        """Synchronise and raise for any data-dependent error a kernel reported
+        since the last check.  The status word is cleared when read, so one
+        failed step does not poison later ones."""
         torch.cuda.current_stream().synchronize()
-        _lib.raise_status(int(self.status.item()) & 0xFFFFFFFF, "cache")
+        word = int(self.status.item()) & 0xFFFFFFFF
+        if word:
+            self.status.zero_()
+        _lib.raise_status(word, "cache")
 
     def _rows(self, t, shape, what):
         if not isinstance(t, torch.Tensor):

@@ -194,14 +194,4 @@ int kitty_debug_attention_trace(int enable, long long* host_out, int max_warps) 
     return cuda_status(kitty::fast_attention_trace(enable, host_out, max_warps));
 }
 
-int kitty_debug_select_attention(int impl) {
-    if (impl < 0 || impl > 1) return invalid("attention impl must be 0 (default) or 1 (tcgen05)");
-    kitty::set_attention_impl(impl);
-    return KITTY_OK;
-}
-
-int kitty_debug_tc_trace(int enable, long long* host_out, int max_rows) {
-    return cuda_status(kitty::tc_attention_trace(enable, host_out, max_rows));
-}
-
 }  // extern "C"

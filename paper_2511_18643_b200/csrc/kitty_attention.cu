@@ -20,10 +20,10 @@ constexpr int kGenericThreads = 128;
 struct CacheSource {
     KittyCacheDesc c;
     int u, n, kp, vp;
-    __device__ void init(const KittyCacheDesc& cd, int unit) {
+    __device__ void init(const KittyCacheDesc& cd, int unit, int max_tokens) {
         c = cd;
         u = unit;
-        n = cd.unit_len[unit];
+        n = min(cd.unit_len[unit], max_tokens);
         const int past = n > cd.cfg.s ? n - cd.cfg.s : 0;
         kp = past / cd.cfg.g;
         vp = (past - min(cd.cfg.r, past)) / cd.cfg.g;
@@ -136,7 +136,7 @@ __device__ void attend_split(const Src& src, int n, int d, int group, const floa
     }
 }
 
-__global__ void attention_generic_kernel(KittyCacheDesc c, const uint16_t* q, int splits,
+__global__ void attention_generic_kernel(KittyCacheDesc c, const uint16_t* q, int splits, int max_tokens,
                                          float* ws_acc, float* ws_ml) {
     extern __shared__ __align__(16) float gsm[];
     const int u = blockIdx.y;
@@ -147,7 +147,8 @@ __global__ void attention_generic_kernel(KittyCacheDesc c, const uint16_t* q, in
     const uint16_t* qg = q + ((int64_t)b * c.cfg.h_q + (int64_t)h * group) * d;
     for (int i = threadIdx.x; i < group * d; i += blockDim.x) qs[i] = bf16_to_f32(qg[i]);
     CacheSource src;
-    src.init(c, u);
+    src.init(c, u, max_tokens);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && c.unit_len[u] > max_tokens) set_status(c.status, KITTY_STATUS_LENGTH);
     __syncthreads();
     const float sqrt_d = static_cast<float>(sqrt(static_cast<double>(d)));
     const int64_t slot = (int64_t)u * splits + blockIdx.x;
@@ -208,17 +209,12 @@ static int generic_splits(int max_tokens) {
     return max_tokens <= 0 ? 1 : (max_tokens + kGenericChunk - 1) / kGenericChunk;
 }
 
-static int g_attention_impl = 0;
-void set_attention_impl(int impl) { g_attention_impl = impl; }
-
 size_t attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
     const int units = c.num_seqs * c.cfg.h_kv;
     const int group = c.cfg.h_q / c.cfg.h_kv;
     size_t generic = (size_t)units * generic_splits(max_tokens) * group * (c.cfg.d + 2) * sizeof(float);
     size_t fast = fast_attention_workspace_bytes(c, max_tokens);
-    size_t tc = tc_attention_workspace_bytes(c, max_tokens);
-    size_t w = generic > fast ? generic : fast;
-    return w > tc ? w : tc;
+    return generic > fast ? generic : fast;
 }
 
 cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, void* out,
@@ -226,11 +222,8 @@ cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, 
                                     cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
     if (units == 0) return cudaSuccess;
-    // mma.sync kernel (fastest measured); the tcgen05 kernel when
-    // selected (kitty_debug_select_attention)
-    if (fast_attention_supported(c) && !(g_attention_impl == 1 && tc_attention_supported(c)))
-        return launch_fast_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
-    if (tc_attention_supported(c)) return launch_tc_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
+    // d = g = 128, GQA groups 1/2/4/8: the fused tensor-core kernel
+    if (fast_attention_supported(c)) return launch_fast_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
     const int group = c.cfg.h_q / c.cfg.h_kv;
     const int d = c.cfg.d;
     const int splits = generic_splits(max_tokens);
@@ -239,8 +232,8 @@ cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, 
     float* ws_acc = static_cast<float*>(ws);
     float* ws_ml = ws_acc + (size_t)units * splits * group * d;
     const size_t sm = ((size_t)group * d + (size_t)group * kGenericChunk) * sizeof(float);
-    cudaFuncSetAttribute(attention_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attention_generic_kernel<<<dim3(splits, units), kGenericThreads, sm, st>>>(c, q, splits, ws_acc, ws_ml);
+    if (cudaError_t e0 = set_kernel_smem((const void*)attention_generic_kernel, (int)sm)) return e0;
+    attention_generic_kernel<<<dim3(splits, units), kGenericThreads, sm, st>>>(c, q, splits, max_tokens, ws_acc, ws_ml);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     combine_kernel<<<units, 128, 0, st>>>(ws_acc, ws_ml, splits, group, d, c.cfg.h_kv, c.cfg.h_q, 0, out, out_dtype);
@@ -261,7 +254,7 @@ cudaError_t launch_dense_attention(const float* keys, const float* values, int h
     float* ws_acc = static_cast<float*>(ws);
     float* ws_ml = ws_acc + (size_t)n_q * splits * d;
     const size_t sm = ((size_t)d + kGenericChunk) * sizeof(float);
-    cudaFuncSetAttribute(attention_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (cudaError_t e0 = set_kernel_smem((const void*)attention_dense_kernel, (int)sm)) return e0;
     attention_dense_kernel<<<dim3(splits, n_q), kGenericThreads, sm, st>>>(keys, values, length, d, queries, kv_map, splits, ws_acc, ws_ml);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -16,15 +16,4 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
 // Debug: enable the per-warp trace of the fused kernel / copy it out.
 cudaError_t fast_attention_trace(int enable, long long* host_out, int max_warps);
 
-// The tcgen05 (kind::i8) warp-specialised kernel (kitty_attention_tc.cu):
-// covers GQA groups 1/2/4/8; used for group 8 (outside the mma.sync kernel)
-// and on request for the others (kitty_debug_select_attention).
-bool tc_attention_supported(const KittyCacheDesc& c);
-size_t tc_attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens);
-cudaError_t launch_tc_attention(const KittyCacheDesc& c, const uint16_t* q, void* out, int out_dtype,
-                                int max_tokens, void* ws, size_t ws_bytes, cudaStream_t st);
-cudaError_t tc_attention_trace(int enable, long long* host_out, int max_rows);
-// 0 = default dispatch, 1 = tcgen05 kernel wherever it applies
-void set_attention_impl(int impl);
-
 }  // namespace kitty

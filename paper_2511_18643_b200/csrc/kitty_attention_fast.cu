@@ -110,6 +110,7 @@ struct Params {
     int lvl[4];   // level 1 / 2 starts in per mille of vp: units < 512 pages, >= 512 pages
     int nslot;    // partial slots per unit: fmax + cmx[0] + cmx[1] + cmx[2]
     int units;
+    int max_tokens;  // the caller's bound on the unit lengths (longer units: clamped + KITTY_STATUS_LENGTH)
     uint32_t units_mul, units_shift;  // fast division by units (quotient = (umulhi(n, mul) + n) >> shift)
     int* ctr;   // [0] next item, [1] finished warps
     float* part;
@@ -353,9 +354,9 @@ __host__ __device__ __forceinline__ int level_begin(int lv, int vp, const int* l
     return lv == 0 ? 0 : (lv == 1 ? (vp * lvl[0]) / 1000 : (lv == 2 ? (vp * lvl[1]) / 1000 : vp));
 }
 
-__device__ __forceinline__ UnitGeom unit_geom(const KittyCacheDesc& c, int u) {
+__device__ __forceinline__ UnitGeom unit_geom(const KittyCacheDesc& c, int u, int max_tokens) {
     UnitGeom g;
-    g.n = c.unit_len[u];
+    g.n = min(c.unit_len[u], max_tokens);
     const int S = c.cfg.s;
     const int past = g.n > S ? g.n - S : 0;
     g.kp = past / G;
@@ -423,12 +424,12 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) fast_attention_kernel
     int* s_ulen = reinterpret_cast<int*>(smem_raw + wbytes * kWarps);  // dynamic, units entries
     const bool len_table = P.units <= kMaxTableUnits;
     if (len_table) {
-        for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = c.unit_len[i];
+        for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = min(c.unit_len[i], P.max_tokens);
     }
     __syncthreads();
     auto geom = [&](int u) {
         UnitGeom g;
-        g.n = len_table ? s_ulen[u] : c.unit_len[u];
+        g.n = len_table ? s_ulen[u] : min(c.unit_len[u], P.max_tokens);
         const int S = c.cfg.s;
         const int past = g.n > S ? g.n - S : 0;
         g.kp = past / G;
@@ -1063,9 +1064,9 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
     extern __shared__ __align__(128) uint8_t fsm[];
     const int it = blockIdx.x;
     const int fc = it / P.units, u = it - fc * P.units;
-    const fptok::Geom gm = fptok::geom(P.c, u);
+    const fptok::Geom gm = fptok::geom(P.c, u, P.max_tokens);
     asm volatile("griddepcontrol.launch_dependents;");  // the merge may pre-launch
-    if (gm.n > 0 && fc * kFpChunk < gm.nfp) fptok::chunk_tc<GROUP>(P.c, P.q, P.part, P.nslot, part_stride(GROUP), fsm, u, fc);
+    if (gm.n > 0 && fc * kFpChunk < gm.nfp) fptok::chunk_tc<GROUP>(P.c, P.q, P.part, P.nslot, part_stride(GROUP), fsm, u, fc, P.max_tokens);
     // launched as a programmatic dependent of the page grid: finish only after it
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -1080,7 +1081,10 @@ __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
     const KittyCacheDesc& c = P.c;
     // the unit's part list depends only on its length (written by the append,
     // before the page grid): computed before waiting on the fp grid
-    const UnitGeom gm = unit_geom(c, u);
+    const UnitGeom gm = unit_geom(c, u, P.max_tokens);
+    // a unit longer than the caller's bound was attended over its first
+    // max_tokens tokens only: make the caller's check() raise
+    if (g == 0 && threadIdx.x == 0 && c.unit_len[u] > P.max_tokens) set_status(c.status, KITTY_STATUS_LENGTH);
     asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the fp grid (KITTY_PDL bit 2)
     if (gm.n == 0) return;
     const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
@@ -1109,16 +1113,7 @@ __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
 
 using namespace fastattn;
 
-static int num_sms() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+static int num_sms() { return device_sms(); }
 
 bool fast_attention_supported(const KittyCacheDesc& c) {
     const int group = c.cfg.h_q / c.cfg.h_kv;
@@ -1215,30 +1210,20 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     auto kfn = fast_attention_kernel<GROUP, NKH>;
     const size_t sm = (size_t)warp_smem_bytes<GROUP>((int)prm.c.key_slot_bytes, (int)prm.c.value_slot_bytes) * kWarps +
                       (prm.units <= kMaxTableUnits ? 4 * prm.units : 0);
-    static cudaError_t attr = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)(warp_smem_bytes<GROUP>(kKeySlotMax, kValueSlot) * kWarps +
-                                                         4 * kMaxTableUnits));  // once per instantiation
-    if (attr != cudaSuccess) return attr;
-    static cudaError_t carve =
-        cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    if (carve != cudaSuccess) return carve;
+    cudaError_t e = set_kernel_smem((const void*)kfn, (int)(warp_smem_bytes<GROUP>(kKeySlotMax, kValueSlot) * kWarps +
+                                                          4 * kMaxTableUnits), true);
+    if (e != cudaSuccess) return e;
     // persistent grid: kCtasPerSm CTAs per SM must be co-resident (their shared
     // memory, the 1 KB per-CTA reservation and the static part fit the SM), else
     // one fewer per SM.  (cudaOccupancyMaxActiveBlocksPerMultiprocessor reports
     // 1 for this kernel on B200 at any shared-memory size, so it is not used.)
-    static int smpm = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-        return v;
-    }();
+    const int smpm = device_smem_per_sm();
     int per_sm = kCtasPerSm;
     while (per_sm > 1 && (size_t)per_sm * (sm + 128 + 1024) > (size_t)smpm) --per_sm;
     if (grid > num_sms() * per_sm) grid = num_sms() * per_sm;
     // the pages first; the fp-token chunks as a programmatic dependent of the
     // page grid, so their CTAs backfill SMs as persistent page CTAs retire (the
     // fp grid waits on the page grid only before it exits); then the merge
-    cudaError_t e;
     cudaLaunchAttribute at[3];
     for (int i = 0; i < 3; ++i) {
         at[i].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1316,6 +1301,7 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     for (int i = 0; i < 4; ++i) prm.lvl[i] = p.lvl[i];
     prm.nslot = p.nslot;
     prm.units = p.units;
+    prm.max_tokens = max_tokens;
     {
         // fast division by units: q = (umulhi(n, mul) + n) >> shift, n < 2^31
         uint32_t sh = 0;

@@ -636,12 +636,12 @@ cudaError_t launch_pack_key_pages(const void* x, int dtype, int P, int g, int d,
     const size_t sm = pack_smem_bytes(g, d, d_boost, dtype == KITTY_F32 ? 4 : 2);
     if (dtype == KITTY_F32) {
         auto kfn = pack_key_pages_kernel<float>;
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (cudaError_t e = set_kernel_smem((const void*)kfn, (int)sm)) return e;
         kfn<<<P, 128, sm, st>>>(static_cast<const float*>(x), g, d, d_boost, sel, slots, stride,
                                 sc32, ze32, status);
     } else {
         auto kfn = pack_key_pages_kernel<uint16_t>;
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (cudaError_t e = set_kernel_smem((const void*)kfn, (int)sm)) return e;
         kfn<<<P, 128, sm, st>>>(static_cast<const uint16_t*>(x), g, d, d_boost, sel, slots,
                                 stride, sc32, ze32, status);
     }
@@ -655,11 +655,11 @@ cudaError_t launch_pack_value_pages(const void* x, int dtype, int P, int g, int 
     const size_t sm = pack_smem_bytes(g, d, 0, dtype == KITTY_F32 ? 4 : 2);
     if (dtype == KITTY_F32) {
         auto kfn = pack_value_pages_kernel<float>;
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (cudaError_t e = set_kernel_smem((const void*)kfn, (int)sm)) return e;
         kfn<<<P, 128, sm, st>>>(static_cast<const float*>(x), g, d, slots, stride, sc32, ze32, status);
     } else {
         auto kfn = pack_value_pages_kernel<uint16_t>;
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (cudaError_t e = set_kernel_smem((const void*)kfn, (int)sm)) return e;
         kfn<<<P, 128, sm, st>>>(static_cast<const uint16_t*>(x), g, d, slots, stride, sc32, ze32, status);
     }
     return cudaGetLastError();
@@ -705,7 +705,7 @@ cudaError_t launch_append(const KittyCacheDesc& c, const uint16_t* k_new, const 
     if (units == 0) return cudaSuccess;
     size_t sm = pack_smem_bytes(c.cfg.g, c.cfg.d, c.cfg.d_boost, 2);
     if (c.cfg.d == fastpack::kD && c.cfg.g == fastpack::kG && sm < sizeof(fastpack::Smem)) sm = sizeof(fastpack::Smem);
-    cudaFuncSetAttribute(append_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (cudaError_t e = set_kernel_smem((const void*)append_kernel, (int)sm)) return e;
     append_kernel<<<units, fastpack::kThreads, sm, st>>>(c, k_new, v_new);
     return cudaGetLastError();
 }
@@ -731,14 +731,12 @@ cudaError_t launch_prefill(const KittyCacheDesc& c, const uint16_t* keys, const 
     if (e != cudaSuccess || kp + vp == 0) return e;
     if (c.cfg.d == fastpack::kD && G == fastpack::kG && g_fast_pack) {
         const int sm = static_cast<int>(sizeof(fastpack::Smem));
-        static cudaError_t attr =
-            cudaFuncSetAttribute(prefill_pack_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        if (attr != cudaSuccess) return attr;
+        if ((e = set_kernel_smem((const void*)prefill_pack_fast_kernel, sm)) != cudaSuccess) return e;
         prefill_pack_fast_kernel<<<dim3(kp + vp, units), fastpack::kThreads, sm, st>>>(c, keys, values, P, kp, vp);
         return cudaGetLastError();
     }
     const size_t sm = pack_smem_bytes(G, c.cfg.d, c.cfg.d_boost, 2);
-    cudaFuncSetAttribute(prefill_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if ((e = set_kernel_smem((const void*)prefill_pack_kernel, (int)sm)) != cudaSuccess) return e;
     prefill_pack_kernel<<<dim3(kp + vp, units), 128, sm, st>>>(c, keys, values, P, kp, vp);
     return cudaGetLastError();
 }

@@ -21,12 +21,13 @@ __device__ __forceinline__ float merge_ex2(float x) {
 }
 
 // pb: the unit's first record; stride: floats per record; slot_of(i): record
-// index of part i (nparts <= kMaxParts); d = 128 (one float4 per lane).
-// Thread = part first: record index, (m, l) and the row max, so the weights
+// index of part i; d = 128 (one float4 per lane).
+// Thread = part first: (m, l) of every part and the row max, so the weights
 // 2^(m - max) are known before the accumulator rows are read; then every warp
 // streams a strided subset of the rows (address + weight from shared memory,
-// 8 rows' loads in flight).  The index arithmetic per row is a few
-// instructions -- the merge was instruction-bound on it (ncu) before.
+// F rows' loads in flight).  Parts are taken in batches of kMaxParts (one
+// batch below that: the (m, l) loads of the max pass are reused), so any part
+// count is merged -- a 256K-token unit alone on a GPU has ~2 000.
 constexpr int kMaxParts = 1024;
 template <int GROUP, class SlotFn, int WARPS = kMergeWarps>
 __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int nparts, SlotFn slot_of, int g,
@@ -38,18 +39,22 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
     __shared__ float s_w[kMaxParts];
     __shared__ float s_l[kMaxParts];
     __shared__ float s_red[WARPS];
+    __shared__ float s_lsum[WARPS];
     __shared__ float4 s_acc[WARPS][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (nparts > kMaxParts) nparts = kMaxParts;  // host plans keep nslot far below
+    auto load_ml = [&](int i) {
+        return __ldcg(reinterpret_cast<const float2*>(pb + (int64_t)slot_of(i) * stride + GROUP * D + 2 * g));
+    };
     float mloc = -INFINITY;
     for (int i = threadIdx.x; i < nparts; i += T) {
         const int sl = slot_of(i);
-        s_slot[i] = sl;
         const float2 ml = __ldcg(reinterpret_cast<const float2*>(pb + (int64_t)sl * stride + GROUP * D + 2 * g));
-        const float m = ml.x;
-        s_w[i] = m;
-        s_l[i] = ml.y;  // (m, l) in one load: no second round trip for l
-        mloc = fmaxf(mloc, m);
+        if (i < kMaxParts) {
+            s_slot[i] = sl;
+            s_w[i] = ml.x;
+            s_l[i] = ml.y;  // (m, l) in one load: no second round trip for l
+        }
+        mloc = fmaxf(mloc, ml.x);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
@@ -59,41 +64,53 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
 #pragma unroll
     for (int w = 1; w < WARPS; ++w) M = fmaxf(M, s_red[w]);
     float lsum = 0.f;
-    for (int i = threadIdx.x; i < nparts; i += T) {
-        const float m = s_w[i];
-        const float w = m == -INFINITY ? 0.f : merge_ex2(m - M);
-        s_w[i] = w;
-        lsum = fmaf(w, s_l[i], lsum);
+    const float* rowp = pb + g * D + 4 * lane;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int b0 = 0; b0 < nparts; b0 += kMaxParts) {
+        const int nb = min(kMaxParts, nparts - b0);
+        if (b0 > 0) {
+            __syncthreads();  // the previous batch's rows are read
+            for (int i = threadIdx.x; i < nb; i += T) {
+                const float2 ml = load_ml(b0 + i);
+                s_slot[i] = slot_of(b0 + i);
+                s_w[i] = ml.x;
+                s_l[i] = ml.y;
+            }
+        }
+        for (int i = threadIdx.x; i < nb; i += T) {  // this thread's own entries: no barrier needed
+            const float m = s_w[i];
+            const float w = m == -INFINITY ? 0.f : merge_ex2(m - M);
+            s_w[i] = w;
+            lsum = fmaf(w, s_l[i], lsum);
+        }
+        __syncthreads();  // s_w complete
+        for (int i0 = warp; i0 < nb; i0 += F * WARPS) {
+            float4 a[F];
+            float w[F];
+#pragma unroll
+            for (int j = 0; j < F; ++j) {
+                const int i = i0 + j * WARPS;
+                const bool ok = i < nb;
+                w[j] = ok ? s_w[i] : 0.f;
+                a[j] = ok ? __ldcg(reinterpret_cast<const float4*>(rowp + (int64_t)s_slot[i] * stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < F; ++j) {
+                acc.x = fmaf(w[j], a[j].x, acc.x);
+                acc.y = fmaf(w[j], a[j].y, acc.y);
+                acc.z = fmaf(w[j], a[j].z, acc.z);
+                acc.w = fmaf(w[j], a[j].w, acc.w);
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    __syncthreads();  // s_red reads done, s_w complete
-    if (lane == 0) s_red[warp] = lsum;
-    const float* rowp = pb + g * D + 4 * lane;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i0 = warp; i0 < nparts; i0 += F * WARPS) {
-        float4 a[F];
-        float w[F];
-#pragma unroll
-        for (int j = 0; j < F; ++j) {
-            const int i = i0 + j * WARPS;
-            const bool ok = i < nparts;
-            w[j] = ok ? s_w[i] : 0.f;
-            a[j] = ok ? __ldcg(reinterpret_cast<const float4*>(rowp + (int64_t)s_slot[i] * stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int j = 0; j < F; ++j) {
-            acc.x = fmaf(w[j], a[j].x, acc.x);
-            acc.y = fmaf(w[j], a[j].y, acc.y);
-            acc.z = fmaf(w[j], a[j].z, acc.z);
-            acc.w = fmaf(w[j], a[j].w, acc.w);
-        }
-    }
     s_acc[warp][lane] = acc;
+    if (lane == 0) s_lsum[warp] = lsum;
     __syncthreads();
     if (warp != 0) return;
     float4 o = s_acc[0][lane];
-    float lt = s_red[0];
+    float lt = s_lsum[0];
 #pragma unroll
     for (int w = 1; w < WARPS; ++w) {
         const float4 x = s_acc[w][lane];
@@ -101,7 +118,7 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
         o.y += x.y;
         o.z += x.z;
         o.w += x.w;
-        lt += s_red[w];
+        lt += s_lsum[w];
     }
     const float inv = 1.f / lt;
     if (out_dtype == KITTY_F32) {

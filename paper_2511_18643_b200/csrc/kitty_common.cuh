@@ -103,4 +103,12 @@ __device__ __forceinline__ void set_status(uint32_t* status, uint32_t bits) {
     if (status) atomicOr(status, bits);
 }
 
+// ---- host: per-device properties and kernel attributes (kitty_device.cu) ----
+// One process may drive several GPUs (one stream each), so nothing here is a
+// process-wide static: values are cached per (device ordinal) and kernel
+// attributes are set once per (kernel, device, value).
+int device_sms();                 // SM count of the current device
+int device_smem_per_sm();         // shared memory per SM (bytes)
+cudaError_t set_kernel_smem(const void* fn, int bytes, bool max_shared_carveout = false);
+
 }  // namespace kitty

@@ -1,0 +1,167 @@
+"""GPU parity of the fused decode attention (kitty_decode_attention) at the
+shapes and edge cases the benchmark configs reach, against the CPU oracle.
+
+* long single units (131 072 / 262 144 tokens, one KV head): more than 1 024
+  split-KV partials per unit, so the merge takes several batches;
+* every boost fraction of C3 (0 / 6.25 / 12.5 / 25 %) at GQA groups 4 and 8;
+* sinks and local windows that make a full-precision chunk straddle the sink
+  and several key pages (s = 4, r = 256 and friends);
+* the C2 bench shape (16 x 8 units at 32K, x8 outlier key channels), sampled
+  units against the oracle;
+* the max_tokens bound: a unit longer than the bound raises, and the status
+  word is clean afterwards.
+
+Bar (north_star): max-abs <= 1e-2 on the attention output against the
+oracle's attend over the same pages (f16 metadata, as the device stores them)
+and against the reference semantics (f32 metadata)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kitty_oracle as ko
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def _bf16(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).bfloat16().float().numpy()
+
+
+def _keys(rng, shape, outliers=16):
+    k = rng.normal(0, 1, shape).astype(np.float32)
+    ch = rng.choice(shape[-1], outliers, replace=False)
+    k[..., ch] *= 8
+    return _bf16(k)
+
+
+_LONG = {}
+
+
+def _long_state(n):
+    """One KV head of n tokens and its oracle state (computed once per n)."""
+    if n not in _LONG:
+        rng = np.random.default_rng(n)
+        k = _keys(rng, (n, 128))
+        v = _bf16(rng.normal(0, 1, (n, 128)))
+        kf, vf, _, _ = ko.bulk_unit_state(k, v, 32, 128, 128, 0.125, metadata16=True)
+        _LONG[n] = (k, v, kf, vf)
+    return _LONG[n]
+
+
+@pytest.mark.parametrize("n", [131072, 262144])
+@pytest.mark.parametrize("group", [4, 8])
+def test_long_single_unit_vs_oracle(cuda, n, group):
+    # 1 sequence x 1 KV head: the page schedule splits the unit into ~1 000 -
+    # 2 000 items, more partials than one merge batch (kMaxParts = 1 024)
+    k, v, kf, vf = _long_state(n)
+    cfg = cuda.KittyConfig(h_kv=1, h_q=group)
+    cache = cuda.KittyBatchCache(cfg, 1, n)
+    cache.prefill(torch.from_numpy(k)[None, None].cuda().bfloat16(), torch.from_numpy(v)[None, None].cuda().bfloat16())
+    q = _bf16(np.random.default_rng(group).normal(0, 1, (1, group, 128)))
+    out = cache.attend(torch.from_numpy(q).cuda(), out_dtype=torch.float32)[0].cpu().numpy()
+    cache.check()
+    want = ko.attend_rows(kf, vf, q[0])
+    assert np.max(np.abs(out - want)) <= TOL
+
+
+@pytest.mark.parametrize("frac", [0.0, 0.0625, 0.125, 0.25])
+@pytest.mark.parametrize("group", [4, 8])
+def test_boost_fractions_vs_oracle(cuda, frac, group):
+    # C3's boost variants: d_boost 0 / 8 / 16 / 32 (the NKH = 0 / 1 / 1 / 2
+    # instantiations; 8 boosted rows fill half of a 16-row high-bits tile)
+    rng = np.random.default_rng(int(frac * 1000) + group)
+    b, h_kv, n = 2, 2, 3000
+    h_q = h_kv * group
+    cfg = cuda.KittyConfig(h_kv=h_kv, h_q=h_q, boost_fraction=frac)
+    k = _keys(rng, (b, h_kv, n + 1, 128))
+    v = _bf16(rng.normal(0, 1, (b, h_kv, n + 1, 128)))
+    cache = cuda.KittyBatchCache(cfg, b, n + 1)
+    cache.prefill(torch.from_numpy(k[:, :, :n]), torch.from_numpy(v[:, :, :n]))
+    cache.append(torch.from_numpy(k[:, :, n]), torch.from_numpy(v[:, :, n]))
+    q = _bf16(rng.normal(0, 1, (b, h_q, 128)))
+    out = cache.attend(torch.from_numpy(q).cuda(), out_dtype=torch.float32).cpu().numpy()
+    cache.check()
+    for bi in range(b):
+        for h in range(h_kv):
+            qg = q[bi, h * group:(h + 1) * group]
+            for meta16 in (True, False):
+                kf, vf, kb, vb = ko.bulk_unit_state(k[bi, h], v[bi, h], 32, 128, 128, frac, metadata16=meta16)
+                err = np.max(np.abs(out[bi, h * group:(h + 1) * group] - ko.attend_rows(kf, vf, qg)))
+                assert err <= TOL, (bi, h, meta16, err)
+            dk, dv = cache.export_pages(bi, h)
+            assert [x[11:] for x in dk] == kb and [x[11:] for x in dv] == vb
+
+
+@pytest.mark.parametrize("s,r,n", [(4, 256, 1004), (4, 256, 1100), (40, 300, 1500), (0, 200, 777), (7, 129, 650),
+                                   (32, 128, 400)])
+@pytest.mark.parametrize("group", [4, 8])
+def test_fp_chunks_straddling_sink_and_pages(cuda, s, r, n, group):
+    # a 32-token full-precision chunk may hold sink tokens and local-window
+    # tokens whose keys sit in several key pages (r > g): those pages must all
+    # be dequantised (kitty_fp.cuh chunk_tc)
+    rng = np.random.default_rng(s * 1000 + r + n)
+    h_kv = 2
+    cfg = cuda.KittyConfig(s=s, r=r, h_kv=h_kv, h_q=h_kv * group)
+    k = _keys(rng, (h_kv, n, 128))
+    v = _bf16(rng.normal(0, 1, (h_kv, n, 128)))
+    q = _bf16(rng.normal(0, 1, (h_kv * group, 128)))
+    st = cuda.KittyCacheState(cfg, max_tokens=n)
+    st.prefill(k, v)
+    got = st.attend(q).outputs
+    oc = ko.OracleCache(s, r, 128, 128, h_kv, h_kv * group, 0.125, metadata16=True)
+    oc.prefill(k, v)
+    assert np.max(np.abs(got - oc.attend(q))) <= TOL
+
+
+def test_c2_shape_sampled_units_vs_oracle(cuda):
+    # the bench workload (BASELINE configs[1]): 16 sequences x 8 KV heads at
+    # 32K tokens, x8 outlier key channels, one decode step (append + attend);
+    # sampled units against the oracle's state built from the same rows
+    B, h_kv, h_q, n = 16, 8, 32, 32768
+    g = h_q // h_kv
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(2)
+    gain = torch.ones(128, device="cuda")
+    gain[torch.randperm(128, generator=gen, device="cuda")[:16]] = 8.0
+    k = (torch.randn((B, h_kv, n + 1, 128), generator=gen, device="cuda") * gain).bfloat16()
+    v = torch.randn((B, h_kv, n + 1, 128), generator=gen, device="cuda").bfloat16()
+    q = torch.randn((B, h_q, 128), generator=gen, device="cuda").bfloat16()
+    cfg = cuda.KittyConfig(h_kv=h_kv, h_q=h_q)
+    cache = cuda.KittyBatchCache(cfg, B, n + 1)
+    cache.prefill(k[:, :, :n], v[:, :, :n])
+    cache.append(k[:, :, n], v[:, :, n])
+    out = cache.attend(q).float().cpu().numpy()
+    cache.check()
+    for b, h in ((0, 0), (7, 3), (15, 7)):
+        kk = k[b, h].float().cpu().numpy()
+        vv = v[b, h].float().cpu().numpy()
+        kf, vf, _, _ = ko.bulk_unit_state(kk, vv, 32, 128, 128, 0.125, metadata16=True)
+        want = ko.attend_rows(kf, vf, q[b, h * g:(h + 1) * g].float().cpu().numpy())
+        assert np.max(np.abs(out[b, h * g:(h + 1) * g] - want)) <= TOL, (b, h)
+
+
+@pytest.mark.parametrize("d", [128, 16])
+def test_length_bound_is_reported(cuda, d):
+    # kitty_decode_attention's max_tokens bounds the unit lengths; a longer
+    # unit sets KITTY_STATUS_LENGTH (the shim raises) and check() clears it
+    cfg = cuda.KittyConfig(d=d, h_kv=1, h_q=4)
+    cache = cuda.KittyBatchCache(cfg, 1, 600)
+    kv = torch.randn(1, 1, 600, d).bfloat16()
+    cache.prefill(kv, kv)
+    lib = cuda.load_library()
+    ws = cache.workspace(600)
+    q = torch.randn(1, 4, d).bfloat16().cuda()
+    out = torch.empty(1, 4, d, dtype=torch.float32, device="cuda")
+    rc = lib.kitty_decode_attention(cache._desc_ref, q.data_ptr(), out.data_ptr(), 0, 300, ws.data_ptr(), ws.numel(),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    with pytest.raises(cuda.KittyError, match="max_tokens"):
+        cache.check()
+    cache.check()  # cleared
+    cache.attend(q)
+    cache.check()

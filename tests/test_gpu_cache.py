@@ -302,17 +302,8 @@ def _c1_like(rng, b, h_kv, h_q, n, d=128):
     return _bf16(k), _bf16(v), _bf16(q)
 
 
-@pytest.fixture(params=["default", "tc"])
-def kernel(request, cuda):
-    """Both decode-attention kernels: the default dispatch (mma.sync kernel,
-    GQA groups 1-8) and the tcgen05 kernel everywhere."""
-    cuda.select_attention_kernel(request.param)
-    yield request.param
-    cuda.select_attention_kernel("default")
-
-
 @pytest.mark.parametrize("n,group", [(4096, 4), (1000, 8), (160, 4), (33, 4), (290, 8), (700, 1), (1500, 2)])
-def test_batched_attention_default_shape_vs_oracle(cuda, kernel, n, group):
+def test_batched_attention_default_shape_vs_oracle(cuda, n, group):
     # C1 (1 seq, 8 kv / 32 q, 4K) and ragged-page lengths; bf16 out, max-abs <= 1e-2
     rng = np.random.default_rng(n + group)
     b, h_kv = 2, 8 if n == 4096 else 2
@@ -336,7 +327,7 @@ def test_batched_attention_default_shape_vs_oracle(cuda, kernel, n, group):
         assert np.max(np.abs(out[bi] - oc16.attend(q[bi]))) <= 1e-2
 
 
-def test_decode_loop_matches_oracle(cuda, kernel):
+def test_decode_loop_matches_oracle(cuda):
     # simulate-decode (cli.py:304-315) on the device: prompt, then steps of
     # append + attend, crossing key and value pack boundaries
     rng = np.random.default_rng(77)
@@ -412,7 +403,7 @@ def test_long_units_on_both_schedule_rules(cuda, group):
 
 
 @pytest.mark.parametrize("group", [4, 8])
-def test_ragged_batch_matches_oracle(cuda, kernel, group):
+def test_ragged_batch_matches_oracle(cuda, group):
     # a ragged batch -- every sequence has its own length,
     # page count and pack triggers -- through prefill, decode steps and attend
     rng = np.random.default_rng(11 + group)

@@ -164,3 +164,23 @@ def test_order_reconstruction_fuzz():
         assert len(hd["kpages"]) == c["key_pages"] and len(hd["kq"]) == c["key_qbuf"]
         assert len(hd["vpages"]) == c["value_pages"] and len(hd["vq"]) == c["value_qbuf"]
         assert len(hd["local"]) == c["local"]
+
+
+@pytest.mark.parametrize("s,r,g,n", [(4, 8, 8, 0), (4, 8, 8, 3), (4, 8, 8, 100), (0, 5, 4, 37), (32, 128, 128, 700), (4, 256, 128, 1004)])
+def test_bulk_state_equals_fold(s, r, g, n):
+    # bulk_unit_state (the closed-form state used by the long-context GPU tests)
+    # must equal the fold of insert_token, page bytes and flattened rows alike
+    rng = np.random.default_rng(n + s)
+    d = 16 if g < 128 else 128
+    k = rng.normal(0, 1, (1, n, d)).astype(np.float32)
+    v = rng.normal(0, 1, (1, n, d)).astype(np.float32)
+    oc = ko.OracleCache(s, r, g, d, 1, 1, 0.125, metadata16=True)
+    oc.prefill(k, v)
+    kf, vf, kb, vb = ko.bulk_unit_state(k[0], v[0], s, r, g, 0.125, metadata16=True)
+    assert np.array_equal(kf.reshape(-1, d), oc.flatten_keys(0).reshape(-1, d))
+    assert np.array_equal(vf.reshape(-1, d), oc.flatten_values(0).reshape(-1, d))
+    okb, ovb = oc.page_bodies(0)
+    assert kb == okb and vb == ovb
+    if n:
+        q = rng.normal(0, 1, (1, d)).astype(np.float32)
+        np.testing.assert_array_equal(ko.attend_rows(kf, vf, q), oc.attend(q))
