@@ -192,11 +192,6 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv,
                           const int32_t* kv_head_map, float* out, void* workspace,
                           size_t workspace_bytes, void* stream);
 
-/* ---- debug / experiments (not part of the reference interface) ------- */
-
-/* Per-warp trace of the mma.sync kernel (same convention, 10 fields). */
-int kitty_debug_attention_trace(int enable, long long* host_out, int max_warps);
-
 #ifdef __cplusplus
 }
 #endif

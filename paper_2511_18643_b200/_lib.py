@@ -80,7 +80,6 @@ SIGNATURES = [
     ("kitty_dense_attention_workspace_bytes", c_size_t, [c_int32, c_int32, c_int32]),
     ("kitty_dense_attention", ctypes.c_int,
      [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
-    ("kitty_debug_attention_trace", ctypes.c_int, [ctypes.c_int, c_void_p, ctypes.c_int]),
 ]
 
 _lib = None

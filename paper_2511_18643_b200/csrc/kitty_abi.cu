@@ -187,11 +187,4 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv, 
                                                      as_stream(stream)));
 }
 
-// Debug only (not part of include/kitty_b200.h): per-warp trace of the fused
-// attention kernel: {smid, t_start, t_end, fp items, pages, fp ns, merge ns,
-// wait ns, warp, 0} per warp, 10 int64 each.
-int kitty_debug_attention_trace(int enable, long long* host_out, int max_warps) {
-    return cuda_status(kitty::fast_attention_trace(enable, host_out, max_warps));
-}
-
 }  // extern "C"

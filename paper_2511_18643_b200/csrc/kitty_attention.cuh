@@ -13,7 +13,4 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
                                   int out_dtype, int max_tokens, void* ws, size_t ws_bytes,
                                   cudaStream_t st);
 
-// Debug: enable the per-warp trace of the fused kernel / copy it out.
-cudaError_t fast_attention_trace(int enable, long long* host_out, int max_warps);
-
 }  // namespace kitty
