@@ -20,8 +20,9 @@ from .pages import _stream
 
 
 class DecodeStep:
-    def __init__(self, cfg: KittyConfig, num_layers: int, num_seqs: int, max_tokens: int, device=None):
+    def __init__(self, cfg: KittyConfig, num_layers: int, num_seqs: int, max_tokens: int, device=None, shard=None):
         self.cfg = cfg
+        self.shard = shard  # sharding.Shard this step serves (None: the whole model on one GPU)
         self.num_layers = num_layers
         self.num_seqs = num_seqs
         self.max_tokens = max_tokens
@@ -37,6 +38,12 @@ class DecodeStep:
         self.ws = self.layers[0].workspace(max_tokens)
         self.graph = None
         self.lib = _lib.load_library()
+
+    @classmethod
+    def for_shard(cls, cfg: KittyConfig, shard, num_layers: int, max_tokens: int, device=None) -> "DecodeStep":
+        """The decode step of one rank of a multi-GPU partition (sharding.py):
+        its requests and KV heads of the model config ``cfg``."""
+        return cls(shard.local_config(cfg), num_layers, shard.num_seqs, max_tokens, device, shard)
 
     # bytes moved per step by the inputs / outputs (for the e2e host copies)
     def input_bytes(self) -> int:

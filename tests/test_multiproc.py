@@ -14,6 +14,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2511_18643_b200 import sharding
+from paper_2511_18643_b200.config import KittyConfig
 from oracle import kitty_oracle as ko
 
 CFG = dict(s=4, r=8, g=8, d=8, h_kv=4, h_q=8, boost_fraction=0.25)
@@ -43,16 +44,13 @@ def _worker(rank, world, port, mode, result):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     keys, values, q = _inputs()
-    group = CFG["h_q"] // CFG["h_kv"]
-    if mode == "request":
-        sh = sharding.shard_by_request(BATCH, CFG["h_kv"], world, rank)
-        local = _attend(keys[sh.seq_begin:sh.seq_end], values[sh.seq_begin:sh.seq_end],
-                        q[sh.seq_begin:sh.seq_end], CFG["h_kv"], CFG["h_q"])
-    else:
-        sh = sharding.shard_by_kv_head(BATCH, CFG["h_kv"], world, rank)
-        qs = q[:, sh.kv_begin * group: sh.kv_end * group]
-        local = _attend(keys[:, sh.kv_begin:sh.kv_end], values[:, sh.kv_begin:sh.kv_end], qs,
-                        sh.num_kv_heads, sh.num_kv_heads * group)
+    cfg = KittyConfig(**CFG)
+    sh = sharding.make_shard(mode, BATCH, cfg.h_kv, world, rank)
+    local_cfg = sh.local_config(cfg)  # the shape DecodeStep.for_shard allocates on this rank
+    assert local_cfg.group_size == cfg.group_size and local_cfg.d_boost == cfg.d_boost
+    k, v, qq = sh.select_kv(keys, cfg), sh.select_kv(values, cfg), sh.select_q(q, cfg)
+    assert k.shape[:2] == (sh.num_seqs, local_cfg.h_kv) and qq.shape[:2] == (sh.num_seqs, local_cfg.h_q)
+    local = _attend(k, v, qq, local_cfg.h_kv, local_cfg.h_q)
     full = sharding.gather_outputs(torch.from_numpy(local), mode)
     if rank == 0:
         result.put(full.numpy())
@@ -81,3 +79,16 @@ def test_two_rank_shards_rebuild_full_step(mode):
     keys, values, q = _inputs()
     want = _attend(keys, values, q, CFG["h_kv"], CFG["h_q"])
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_shards_cover_every_unit_once(world):
+    # every (sequence, KV head) unit of the C5 shape lands on exactly one rank
+    cfg = KittyConfig(h_kv=8, h_q=64)
+    for mode in ("request", "kv_head"):
+        seen = np.zeros((16, cfg.h_kv), int)
+        for r in range(world):
+            sh = sharding.make_shard(mode, 16, cfg.h_kv, world, r)
+            seen[sh.seq_begin:sh.seq_end, sh.kv_begin:sh.kv_end] += 1
+            assert sh.local_config(cfg).h_q == sh.num_kv_heads * 8
+        assert (seen == 1).all()
