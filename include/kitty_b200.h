@@ -69,7 +69,9 @@ typedef struct KittyConfigC {
  * Global token order is the reference's (cache.py:12-15):
  *   keys   = sink | key pages   | key q-buffer
  *   values = sink | value pages | value q-buffer | local
- * Full-precision rows are bf16.  Token t >= s of a unit lives at
+ * Full-precision rows are bf16 (row_dtype KITTY_BF16, the fused decode path)
+ * or float32 (KITTY_F32: the reference's own precision, generic kernels).
+ * Token t >= s of a unit lives at
  *   k_qbuf[u][(t - s) % g]          while not yet in a key page,
  *   v_ring[u][(t - s) % (r + g)]    while not yet in a value page
  * (the value ring holds q-buffer + local).  Page slots are byte-identical to
@@ -82,15 +84,25 @@ typedef struct KittyCacheDesc {
     int64_t key_slot_bytes;    /* = kitty_key_slot_bytes(d, g, d_boost)       */
     int64_t value_slot_bytes;  /* = kitty_value_slot_bytes(d, g)              */
     int32_t* unit_len;         /* [B*h_kv] tokens inserted per unit           */
-    uint16_t* k_sink;          /* [B*h_kv][s][d]   bf16                        */
-    uint16_t* v_sink;          /* [B*h_kv][s][d]   bf16                        */
-    uint16_t* k_qbuf;          /* [B*h_kv][g][d]   bf16                        */
-    uint16_t* v_ring;          /* [B*h_kv][r+g][d] bf16                        */
+    void* k_sink;              /* [B*h_kv][s][d]   row_dtype                   */
+    void* v_sink;              /* [B*h_kv][s][d]   row_dtype                   */
+    void* k_qbuf;              /* [B*h_kv][g][d]   row_dtype                   */
+    void* v_ring;              /* [B*h_kv][r+g][d] row_dtype                   */
     uint8_t* key_pool;         /* [slots][key_slot_bytes]                     */
     uint8_t* value_pool;       /* [slots][value_slot_bytes]                   */
     int32_t* key_block_table;  /* [B*h_kv][max_pages] slot index              */
     int32_t* value_block_table;/* [B*h_kv][max_pages] slot index              */
     uint32_t* status;          /* device status word (KITTY_STATUS_*)         */
+    int32_t row_dtype;         /* KITTY_BF16 or KITTY_F32: the rows above and the
+                                  rows / queries passed to append, prefill and
+                                  attention (set it: 0 is KITTY_F32)            */
+    int32_t reserved;
+    float* key_meta;           /* optional [slots][2 d]: f32 scale | zero of each
+                                  key slot, written by the packs; when set,
+                                  attention and flatten use it instead of the
+                                  slot's f16 copy (the reference keeps f32 in
+                                  memory, cache.py:157-161)                     */
+    float* value_meta;         /* optional [slots][2 g]: the same for values   */
 } KittyCacheDesc;
 
 /* ---- sizes / config --------------------------------------------------- */
@@ -149,19 +161,25 @@ int kitty_dequant_value_pages(const uint8_t* slots, int64_t slot_stride, int32_t
                               int32_t g, int32_t d, const float* scales_f32,
                               const float* zeros_f32, float* out, void* stream);
 
+/* fake_quantize_matrix (quant.py:145-177): x [rows][cols] float32; lanes are
+ * columns (per_token = 0, "per_channel") or rows (per_token = 1); bits [lanes]
+ * (device int32) in {2, 4, 16}, 16 passing the lane through; out like x. */
+int kitty_fake_quantize(const float* x, int32_t rows, int32_t cols, int32_t per_token, const int32_t* bits,
+                        float* out, void* stream);
+
 /* ---- cache runtime (cache.py) ----------------------------------------- */
 
 /* insert_token + maybe_pack (cache.py:107-123,144-178) for every unit of the
  * batch: k_new/v_new [B][h_kv][d] bf16.  A unit whose key q-buffer (value
  * q-buffer) reaches g rows is packed into its next key (value) slot inside
  * this call, so a following attention sees the page (pack-before-attend). */
-int kitty_append(const KittyCacheDesc* cache, const uint16_t* k_new, const uint16_t* v_new,
+int kitty_append(const KittyCacheDesc* cache, const void* k_new, const void* v_new,
                  void* stream);
 
 /* prefill (cache.py:125-142) of an empty batch: keys/values [B][h_kv][P][d]
  * bf16.  Produces the state of the fold of P appends; all pages of the prompt
  * are packed in parallel. */
-int kitty_prefill(const KittyCacheDesc* cache, const uint16_t* keys, const uint16_t* values,
+int kitty_prefill(const KittyCacheDesc* cache, const void* keys, const void* values,
                   int32_t prompt_len, void* stream);
 
 /* flatten_keys / flatten_values (cache.py:210-215) of one unit: [n][d] f32,
@@ -179,7 +197,7 @@ size_t kitty_attention_workspace_bytes(const KittyCacheDesc* cache, int32_t max_
  * head i / (h_q / h_kv) (cache.py:240).  Pages are dequantized on the fly
  * inside the QK^T / softmax / PV loop.  max_tokens bounds the unit lengths
  * (the caller's host mirror); it sizes the split-KV grid. */
-int kitty_decode_attention(const KittyCacheDesc* cache, const uint16_t* q, void* out,
+int kitty_decode_attention(const KittyCacheDesc* cache, const void* q, void* out,
                            int32_t out_dtype, int32_t max_tokens, void* workspace,
                            size_t workspace_bytes, void* stream);
 

@@ -35,6 +35,7 @@ from .pages import (
     dequantize_key_page,
     dequantize_value_page,
     deserialize_page,
+    fake_quantize_matrix,
     pack_key_page,
     pack_key_pages,
     pack_value_page,
@@ -56,6 +57,7 @@ __all__ = [
     "UnknownDtypeError", "algorithmic_bytes_per_unit", "boost_count", "channel_scores",
     "channel_scores_batch", "component_counts", "config_from_mapping", "dequant_key_pages",
     "dequant_value_pages", "dequantize_key_page", "dequantize_value_page", "deserialize_page",
+    "fake_quantize_matrix",
     "exported_symbols", "load_library", "measure_cache_bytes", "memory_report", "oracle_attend",
     "pack_key_page", "pack_key_pages", "pack_value_page", "pack_value_pages", "page_byte_size",
     "select_boost", "select_boost_batch", "serialize_page", "serialize_slot",

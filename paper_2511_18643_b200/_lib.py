@@ -51,6 +51,10 @@ class KittyCacheDesc(ctypes.Structure):
         ("key_block_table", c_void_p),
         ("value_block_table", c_void_p),
         ("status", c_void_p),
+        ("row_dtype", c_int32),
+        ("reserved", c_int32),
+        ("key_meta", c_void_p),
+        ("value_meta", c_void_p),
     ]
 
 
@@ -71,6 +75,7 @@ SIGNATURES = [
      [c_void_p, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("kitty_dequant_value_pages", ctypes.c_int,
      [c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("kitty_fake_quantize", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     ("kitty_append", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_void_p, c_void_p, c_void_p]),
     ("kitty_prefill", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_void_p, c_void_p, c_int32, c_void_p]),
     ("kitty_flatten", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_int32, c_int32, c_void_p, c_void_p, c_void_p]),

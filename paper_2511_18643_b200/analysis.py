@@ -86,12 +86,18 @@ def memory_report(cfg: KittyConfig, length: int) -> MemoryReport:
 
 
 def measure_cache_bytes(state) -> MemoryReport:
-    """analysis.py:360-371 from a live state (KittyCacheState or (KittyBatchCache, b))."""
+    """analysis.py:360-371: the accounting of an actually constructed state,
+    counted from what the device holds for KV head 0 -- its sink / q-buffer /
+    local rows and its pages, read back (KittyCacheState or (KittyBatchCache, b))."""
     if isinstance(state, tuple):
         batch, b = state
     else:
         batch, b = state.batch, 0
-    return _assemble(batch.cfg, batch.lengths[b], batch.page_counts(b))
+    rows = batch.head_rows(b, 0)
+    kpages, vpages = batch.pages(b, 0)
+    counts = dict(sink=len(rows["key_sink"]), key_pages=len(kpages), key_qbuf=len(rows["key_qbuffer"]),
+                  local=len(rows["value_local"]), value_pages=len(vpages), value_qbuf=len(rows["value_qbuffer"]))
+    return _assemble(batch.cfg, int(batch.unit_len[b * batch.cfg.h_kv].item()), counts)
 
 
 def algorithmic_bytes_per_unit(cfg: KittyConfig, n: int) -> int:

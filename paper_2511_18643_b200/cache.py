@@ -8,8 +8,12 @@ current stream and can be captured in a CUDA graph.
 
 ``KittyCacheState`` keeps the reference's single-sequence class name and
 methods (cache.py:83-252) on top of a batch of one, so tests written against
-``kittykv`` run unchanged (inputs are stored as bf16, like the paper's FP16
-system; pass bf16-representable values for bit-exact comparisons).
+``kittykv`` run unchanged: it keeps the reference's precision -- float32 rows
+and float32 page metadata (a side table beside the f16 KTYP slots) -- on the
+generic device kernels, and exposes the reference's per-head state
+(``heads[h].key_sink`` ... ``value_pages``) read back from the device.  The
+batched product path (``KittyBatchCache`` default) stores bf16 rows and runs
+the fused decode kernels.
 """
 
 from __future__ import annotations
@@ -54,8 +58,16 @@ def _check_device_config(cfg: KittyConfig):
 class KittyBatchCache:
     """B sequences of Kitty KV cache for one attention layer, resident in HBM."""
 
-    def __init__(self, cfg: KittyConfig, num_seqs: int, max_tokens: int, device=None):
+    def __init__(self, cfg: KittyConfig, num_seqs: int, max_tokens: int, device=None,
+                 row_dtype: torch.dtype = torch.bfloat16, f32_metadata: bool = False):
+        """``row_dtype``: bf16 (the fused decode path) or float32 (the reference's
+        precision, generic kernels); ``f32_metadata``: keep each page's float32
+        scale / zero (the reference's in-memory values) beside its f16 slot."""
         _check_device_config(cfg)
+        if row_dtype not in (torch.bfloat16, torch.float32):
+            raise KittyError("row_dtype must be torch.bfloat16 or torch.float32")
+        self.row_dtype = row_dtype
+        self.f32_metadata = bool(f32_metadata)
         self.lib = _lib.load_library()
         _lib.check(self.lib.kitty_validate_config(ctypes.byref(cfg.to_c())), "config")
         self.cfg = cfg
@@ -76,7 +88,7 @@ class KittyBatchCache:
         cfg, dev, u = self.cfg, self.device, self.units
         self.max_tokens = int(max_tokens)
         self.max_pages = max(1, -(-max(0, self.max_tokens - cfg.s) // cfg.g))
-        bf = torch.bfloat16
+        bf = self.row_dtype
         self.unit_len = torch.zeros(u, dtype=torch.int32, device=dev)
         self.k_sink = torch.zeros((u, cfg.s, cfg.d), dtype=bf, device=dev)
         self.v_sink = torch.zeros((u, cfg.s, cfg.d), dtype=bf, device=dev)
@@ -88,6 +100,11 @@ class KittyBatchCache:
         self.key_block_table = ident.clone()
         self.value_block_table = ident.clone()
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        if self.f32_metadata:
+            self.key_meta = torch.zeros((u * self.max_pages, 2 * cfg.d), dtype=torch.float32, device=dev)
+            self.value_meta = torch.zeros((u * self.max_pages, 2 * cfg.g), dtype=torch.float32, device=dev)
+        else:
+            self.key_meta = self.value_meta = None
         self._build_desc()
 
     def _build_desc(self):
@@ -107,6 +124,9 @@ class KittyBatchCache:
         d.key_block_table = self.key_block_table.data_ptr()
         d.value_block_table = self.value_block_table.data_ptr()
         d.status = self.status.data_ptr()
+        d.row_dtype = _lib.KITTY_F32 if self.row_dtype == torch.float32 else _lib.KITTY_BF16
+        d.key_meta = self.key_meta.data_ptr() if self.key_meta is not None else None
+        d.value_meta = self.value_meta.data_ptr() if self.value_meta is not None else None
         self.desc = d
         self._desc_ref = ctypes.byref(d)
 
@@ -114,13 +134,19 @@ class KittyBatchCache:
         """Re-allocate for longer sequences, keeping every page and row."""
         old = dict(kp=self.key_pool, vp=self.value_pool, ln=self.unit_len, ks=self.k_sink,
                    vs=self.v_sink, kq=self.k_qbuf, vr=self.v_ring, mp=self.max_pages,
-                   kbt=self.key_block_table, vbt=self.value_block_table, st=self.status)
+                   kbt=self.key_block_table, vbt=self.value_block_table, st=self.status,
+                   km=self.key_meta, vm=self.value_meta)
         self._alloc(max_tokens)
         u = self.units
         kv = self.key_pool.view(u, self.max_pages, -1)
         vv = self.value_pool.view(u, self.max_pages, -1)
         kv[:, : old["mp"]] = old["kp"][old["kbt"].reshape(-1).long()].view(u, old["mp"], -1)
         vv[:, : old["mp"]] = old["vp"][old["vbt"].reshape(-1).long()].view(u, old["mp"], -1)
+        if self.f32_metadata:
+            self.key_meta.view(u, self.max_pages, -1)[:, : old["mp"]] = \
+                old["km"][old["kbt"].reshape(-1).long()].view(u, old["mp"], -1)
+            self.value_meta.view(u, self.max_pages, -1)[:, : old["mp"]] = \
+                old["vm"][old["vbt"].reshape(-1).long()].view(u, old["mp"], -1)
         for name, key in (("unit_len", "ln"), ("k_sink", "ks"), ("v_sink", "vs"), ("k_qbuf", "kq"),
                           ("v_ring", "vr"), ("status", "st")):
             getattr(self, name).copy_(old[key])
@@ -258,7 +284,7 @@ class KittyBatchCache:
             t = torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32))
         if tuple(t.shape) != tuple(shape):
             raise KittyError(f"{what} must have shape {tuple(shape)}, got {tuple(t.shape)}")
-        return t.to(device=self.device, dtype=torch.bfloat16).contiguous()
+        return t.to(device=self.device, dtype=self.row_dtype).contiguous()
 
     # -- readout ------------------------------------------------------------------
 
@@ -270,6 +296,52 @@ class KittyBatchCache:
         vo = torch.empty((n, self.cfg.d), dtype=torch.float32, device=self.device)
         _lib.check(self.lib.kitty_flatten(self._desc_ref, u, n, ko.data_ptr(), vo.data_ptr(), _stream()), "flatten")
         return ko, vo
+
+    def head_rows(self, b: int, h: int) -> dict:
+        """The full-precision rows of unit (b, h) in the reference's segments
+        (cache.py:65-80): key / value sink, key q-buffer, value q-buffer, value
+        local window, each [rows, d] float32 read back from the device."""
+        cfg, n = self.cfg, self.lengths[b]
+        c = component_counts(cfg, n)
+        u = b * cfg.h_kv + h
+        W = cfg.r + cfg.g
+        f = lambda t: t.float().cpu().numpy()
+        S, kp, vp = cfg.s, c["key_pages"], c["value_pages"]
+        kq_pos = [(t - S) % cfg.g for t in range(S + kp * cfg.g, S + kp * cfg.g + c["key_qbuf"])]
+        vq_pos = [(t - S) % W for t in range(S + vp * cfg.g, S + vp * cfg.g + c["value_qbuf"])]
+        loc_pos = [(t - S) % W for t in range(n - c["local"], n)] if n > S else []
+        idx = lambda pos: torch.tensor(pos, dtype=torch.long, device=self.device)
+        return dict(key_sink=f(self.k_sink[u, : c["sink"]]), value_sink=f(self.v_sink[u, : c["sink"]]),
+                    key_qbuffer=f(self.k_qbuf[u][idx(kq_pos)]), value_qbuffer=f(self.v_ring[u][idx(vq_pos)]),
+                    value_local=f(self.v_ring[u][idx(loc_pos)]))
+
+    def pages(self, b: int, h: int):
+        """QuantizedKeyPage / QuantizedValuePage objects of unit (b, h) in page
+        order, decoded from the device slots; with f32 metadata kept, their
+        scales / zero points are the float32 values (the reference's in-memory
+        pages, pages.py:60-78), else the slots' f16."""
+        import dataclasses
+
+        from .pages import deserialize_page
+
+        cfg = self.cfg
+        kb, vb = self.export_pages(b, h)
+        kpg = [deserialize_page(x) for x in kb]
+        vpg = [deserialize_page(x) for x in vb]
+        if self.f32_metadata:
+            u = b * cfg.h_kv + h
+            c = self.page_counts(b)
+            km = self.key_meta[self.key_block_table[u, : c["key_pages"]].long()].cpu().numpy()
+            vm = self.value_meta[self.value_block_table[u, : c["value_pages"]].long()].cpu().numpy()
+
+            def frozen(a):
+                a = np.ascontiguousarray(a, np.float32)
+                a.flags.writeable = False
+                return a
+
+            kpg = [dataclasses.replace(pg, scales=frozen(m[: cfg.d]), zero_points=frozen(m[cfg.d:])) for pg, m in zip(kpg, km)]
+            vpg = [dataclasses.replace(pg, scales=frozen(m[: cfg.g]), zero_points=frozen(m[cfg.g:])) for pg, m in zip(vpg, vm)]
+        return kpg, vpg
 
     def page_counts(self, b: int) -> dict:
         return component_counts(self.cfg, self.lengths[b])
@@ -300,13 +372,44 @@ class KittyBatchCache:
             self.k_sink, self.v_sink, self.k_qbuf, self.v_ring, self.key_pool, self.value_pool))
 
 
-class KittyCacheState:
-    """The reference's per-sequence state (cache.py:83-252) on the device."""
+class _RowsView:
+    """The reference's _RowStore (cache.py:41-62) of rows read back from the device."""
 
-    def __init__(self, cfg: KittyConfig, max_tokens: int = 1024):
+    def __init__(self, rows: np.ndarray):
+        self._rows = rows
+
+    def __len__(self):
+        return self._rows.shape[0]
+
+    def view(self) -> np.ndarray:
+        return self._rows
+
+
+class _HeadView:
+    """The reference's _HeadState (cache.py:65-80) of one KV head, read back
+    from the device: sink row stores, q-buffer / local row lists, page lists."""
+
+    def __init__(self, batch: "KittyBatchCache", b: int, h: int):
+        rows = batch.head_rows(b, h)
+        self.key_sink = _RowsView(rows["key_sink"])
+        self.value_sink = _RowsView(rows["value_sink"])
+        self.key_qbuffer = list(rows["key_qbuffer"])
+        self.value_qbuffer = list(rows["value_qbuffer"])
+        self.value_local = list(rows["value_local"])
+        self.key_pages, self.value_pages = batch.pages(b, h)
+
+
+class KittyCacheState:
+    """The reference's per-sequence state (cache.py:83-252) on the device, at
+    the reference's precision: float32 rows and float32 page metadata, the
+    generic kernels (attention in f32 with expf, cache.py:241-258)."""
+
+    def __init__(self, cfg: KittyConfig, max_tokens: int = 1024, row_dtype: torch.dtype = torch.float32):
+        """``row_dtype`` float32 (default): the reference's precision; bfloat16:
+        the product path (fused kernels, f16 page metadata) behind the same API."""
         _check_device_config(cfg)
         self.cfg = cfg
-        self._b = KittyBatchCache(cfg, 1, max_tokens)
+        self._b = KittyBatchCache(cfg, 1, max_tokens, row_dtype=row_dtype, f32_metadata=row_dtype == torch.float32)
 
     @property
     def total_tokens(self) -> int:
@@ -324,13 +427,18 @@ class KittyCacheState:
     def batch(self) -> KittyBatchCache:
         return self._b
 
+    @property
+    def heads(self) -> list:
+        """Per-KV-head state (cache.py:88), read back from the device."""
+        return [_HeadView(self._b, 0, h) for h in range(self.cfg.h_kv)]
+
     def _coerce_rows(self, new, what):
         new = np.asarray(new.cpu() if isinstance(new, torch.Tensor) else new, dtype=np.float32)
         if new.ndim == 1:
             new = new[None, :]
         if new.shape != (self.cfg.h_kv, self.cfg.d):
             raise KittyError(f"{what} must have shape ({self.cfg.h_kv}, {self.cfg.d}), got {new.shape}")
-        return torch.from_numpy(new)[None]
+        return torch.from_numpy(np.ascontiguousarray(new))[None]
 
     def insert_token(self, k_new, v_new) -> None:
         """cache.py:107-123 (pack fires inside, before any attend)."""
@@ -351,7 +459,7 @@ class KittyCacheState:
             raise KittyError("prefill keys/values must be (h_kv, P, d) with equal shapes")
         if keys.shape[1] == 0:
             return
-        self._b.prefill(torch.from_numpy(keys)[None], torch.from_numpy(values)[None])
+        self._b.prefill(torch.from_numpy(np.ascontiguousarray(keys))[None], torch.from_numpy(np.ascontiguousarray(values))[None])
         self._b.check()
 
     def maybe_pack(self) -> int:
@@ -365,7 +473,7 @@ class KittyCacheState:
         return self._b.flatten(0, kv_head)[1].cpu().numpy()
 
     def attend(self, q, return_probs: bool = False) -> AttentionOutput:
-        """cache.py:217-252 on the device (fused dequant-attention)."""
+        """cache.py:217-252 on the device."""
         if self.total_tokens == 0:
             raise KittyError("attend on an empty cache")
         if return_probs:
@@ -375,7 +483,8 @@ class KittyCacheState:
             q = q[None, :]
         if q.shape != (self.cfg.h_q, self.cfg.d):
             raise KittyError(f"q must have shape ({self.cfg.h_q}, {self.cfg.d}), got {q.shape}")
-        out = self._b.attend(torch.from_numpy(q)[None], out_dtype=torch.float32)
+        out = self._b.attend(torch.from_numpy(np.ascontiguousarray(q))[None], out_dtype=torch.float32)
+        self._b.check()
         return AttentionOutput(outputs=out[0].cpu().numpy())
 
     def export_pages(self, kv_head: int = 0):

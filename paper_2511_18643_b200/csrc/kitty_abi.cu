@@ -40,6 +40,7 @@ int check_cache(const KittyCacheDesc* c) {
     if (c->key_slot_bytes != kitty_key_slot_bytes(c->cfg.d, c->cfg.g, c->cfg.d_boost) ||
         c->value_slot_bytes != kitty_value_slot_bytes(c->cfg.d, c->cfg.g))
         return invalid("slot sizes do not match the page layout");
+    if (c->row_dtype != KITTY_BF16 && c->row_dtype != KITTY_F32) return invalid("row_dtype must be KITTY_BF16 or KITTY_F32");
     return KITTY_OK;
 }
 
@@ -132,14 +133,20 @@ int kitty_dequant_value_pages(const uint8_t* slots, int64_t slot_stride, int32_t
                                                          scales_f32, zeros_f32, out, as_stream(stream)));
 }
 
-int kitty_append(const KittyCacheDesc* cache, const uint16_t* k_new, const uint16_t* v_new,
+int kitty_fake_quantize(const float* x, int32_t rows, int32_t cols, int32_t per_token, const int32_t* bits,
+                        float* out, void* stream) {
+    if (rows < 0 || cols < 0) return invalid("fake_quantize_matrix needs a 2-D matrix");
+    return cuda_status(kitty::launch_fake_quantize(x, rows, cols, per_token, bits, out, as_stream(stream)));
+}
+
+int kitty_append(const KittyCacheDesc* cache, const void* k_new, const void* v_new,
                  void* stream) {
     int rc = check_cache(cache);
     if (rc != KITTY_OK) return rc;
     return cuda_status(kitty::launch_append(*cache, k_new, v_new, as_stream(stream)));
 }
 
-int kitty_prefill(const KittyCacheDesc* cache, const uint16_t* keys, const uint16_t* values,
+int kitty_prefill(const KittyCacheDesc* cache, const void* keys, const void* values,
                   int32_t prompt_len, void* stream) {
     int rc = check_cache(cache);
     if (rc != KITTY_OK) return rc;
@@ -160,7 +167,7 @@ size_t kitty_attention_workspace_bytes(const KittyCacheDesc* cache, int32_t max_
     return kitty::attention_workspace_bytes(*cache, max_tokens);
 }
 
-int kitty_decode_attention(const KittyCacheDesc* cache, const uint16_t* q, void* out,
+int kitty_decode_attention(const KittyCacheDesc* cache, const void* q, void* out,
                            int32_t out_dtype, int32_t max_tokens, void* workspace,
                            size_t workspace_bytes, void* stream) {
     int rc = check_cache(cache);

@@ -16,7 +16,13 @@ namespace kitty {
 constexpr int kGenericChunk = 256;  // tokens per split of the generic path
 constexpr int kGenericThreads = 128;
 
-// Reads K/V elements of one unit in global token order (cache.py:12-15).
+// Row element of the cache rows / queries (row_dtype) as float
+__device__ __forceinline__ float rowf(const void* p, int64_t i, int f32) {
+    return f32 ? static_cast<const float*>(p)[i] : bf16_to_f32(static_cast<const uint16_t*>(p)[i]);
+}
+
+// Reads K/V elements of one unit in global token order (cache.py:12-15);
+// pages use the f32 metadata side table when the cache keeps one.
 struct CacheSource {
     KittyCacheDesc c;
     int u, n, kp, vp;
@@ -30,35 +36,41 @@ struct CacheSource {
     }
     __device__ float key(int t, int ch) const {
         const int d = c.cfg.d, S = c.cfg.s, G = c.cfg.g;
-        if (t < S) return bf16_to_f32(c.k_sink[((int64_t)u * S + t) * d + ch]);
+        const int f32 = c.row_dtype == KITTY_F32;
+        if (t < S) return rowf(c.k_sink, ((int64_t)u * S + t) * d + ch, f32);
         const int pc = t - S;
         if (pc < kp * G) {
             const int p = pc / G, tl = pc % G, gb = G / 4;
             const KeyLayout L{d, G, c.cfg.d_boost};
-            const uint8_t* slot = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes;
+            const int32_t sl = c.key_block_table[(int64_t)u * c.max_pages + p];
+            const uint8_t* slot = c.key_pool + (int64_t)sl * c.key_slot_bytes;
             uint32_t code = (slot[L.dense_off() + ch * gb + tl / 4] >> (2 * (tl % 4))) & 3u;
             const uint8_t r = slot[L.idx_off() + ch];
             if (r != kSentinel) code |= ((slot[L.high_off() + r * gb + tl / 4] >> (2 * (tl % 4))) & 3u) << 2;
-            const float s = half_bits_to_f32(ld_u16(slot + L.scale_off() + 2 * ch));
-            const float z = half_bits_to_f32(ld_u16(slot + L.zero_off() + 2 * ch));
+            const float* meta = c.key_meta ? c.key_meta + (int64_t)sl * 2 * d : nullptr;
+            const float s = meta ? meta[ch] : half_bits_to_f32(ld_u16(slot + L.scale_off() + 2 * ch));
+            const float z = meta ? meta[d + ch] : half_bits_to_f32(ld_u16(slot + L.zero_off() + 2 * ch));
             return __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
         }
-        return bf16_to_f32(c.k_qbuf[((int64_t)u * G + pc % G) * d + ch]);
+        return rowf(c.k_qbuf, ((int64_t)u * G + pc % G) * d + ch, f32);
     }
     __device__ float val(int t, int ch) const {
         const int d = c.cfg.d, S = c.cfg.s, G = c.cfg.g, W = c.cfg.r + c.cfg.g;
-        if (t < S) return bf16_to_f32(c.v_sink[((int64_t)u * S + t) * d + ch]);
+        const int f32 = c.row_dtype == KITTY_F32;
+        if (t < S) return rowf(c.v_sink, ((int64_t)u * S + t) * d + ch, f32);
         const int pc = t - S;
         if (pc < vp * G) {
             const int p = pc / G, tl = pc % G;
             const ValueLayout L{d, G};
-            const uint8_t* slot = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes;
+            const int32_t sl = c.value_block_table[(int64_t)u * c.max_pages + p];
+            const uint8_t* slot = c.value_pool + (int64_t)sl * c.value_slot_bytes;
             const uint32_t code = (slot[L.codes_off() + tl * (d / 4) + ch / 4] >> (2 * (ch % 4))) & 3u;
-            const float s = half_bits_to_f32(ld_u16(slot + L.scale_off() + 2 * tl));
-            const float z = half_bits_to_f32(ld_u16(slot + L.zero_off() + 2 * tl));
+            const float* meta = c.value_meta ? c.value_meta + (int64_t)sl * 2 * G : nullptr;
+            const float s = meta ? meta[tl] : half_bits_to_f32(ld_u16(slot + L.scale_off() + 2 * tl));
+            const float z = meta ? meta[G + tl] : half_bits_to_f32(ld_u16(slot + L.zero_off() + 2 * tl));
             return __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
         }
-        return bf16_to_f32(c.v_ring[((int64_t)u * W + pc % W) * d + ch]);
+        return rowf(c.v_ring, ((int64_t)u * W + pc % W) * d + ch, f32);
     }
 };
 
@@ -136,7 +148,7 @@ __device__ void attend_split(const Src& src, int n, int d, int group, const floa
     }
 }
 
-__global__ void attention_generic_kernel(KittyCacheDesc c, const uint16_t* q, int splits, int max_tokens,
+__global__ void attention_generic_kernel(KittyCacheDesc c, const void* q, int splits, int max_tokens,
                                          float* ws_acc, float* ws_ml) {
     extern __shared__ __align__(16) float gsm[];
     const int u = blockIdx.y;
@@ -144,8 +156,8 @@ __global__ void attention_generic_kernel(KittyCacheDesc c, const uint16_t* q, in
     const int b = u / c.cfg.h_kv, h = u % c.cfg.h_kv;
     float* qs = gsm;                    // [group][d]
     float* logit = gsm + group * d;     // [group][chunk]
-    const uint16_t* qg = q + ((int64_t)b * c.cfg.h_q + (int64_t)h * group) * d;
-    for (int i = threadIdx.x; i < group * d; i += blockDim.x) qs[i] = bf16_to_f32(qg[i]);
+    const int64_t q0 = ((int64_t)b * c.cfg.h_q + (int64_t)h * group) * d;
+    for (int i = threadIdx.x; i < group * d; i += blockDim.x) qs[i] = rowf(q, q0 + i, c.row_dtype == KITTY_F32);
     CacheSource src;
     src.init(c, u, max_tokens);
     if (blockIdx.x == 0 && threadIdx.x == 0 && c.unit_len[u] > max_tokens) set_status(c.status, KITTY_STATUS_LENGTH);
@@ -217,13 +229,14 @@ size_t attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
     return generic > fast ? generic : fast;
 }
 
-cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, void* out,
+cudaError_t launch_decode_attention(const KittyCacheDesc& c, const void* q, void* out,
                                     int out_dtype, int max_tokens, void* ws, size_t ws_bytes,
                                     cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
     if (units == 0) return cudaSuccess;
     // d = g = 128, GQA groups 1/2/4/8: the fused tensor-core kernel
-    if (fast_attention_supported(c)) return launch_fast_attention(c, q, out, out_dtype, max_tokens, ws, ws_bytes, st);
+    if (fast_attention_supported(c))
+        return launch_fast_attention(c, static_cast<const uint16_t*>(q), out, out_dtype, max_tokens, ws, ws_bytes, st);
     const int group = c.cfg.h_q / c.cfg.h_kv;
     const int d = c.cfg.d;
     const int splits = generic_splits(max_tokens);

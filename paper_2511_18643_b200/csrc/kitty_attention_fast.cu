@@ -778,7 +778,8 @@ static int num_sms() { return device_sms(); }
 
 bool fast_attention_supported(const KittyCacheDesc& c) {
     const int group = c.cfg.h_q / c.cfg.h_kv;
-    return c.cfg.d == D && c.cfg.g == G && c.cfg.key_bits == 2 && c.cfg.value_bits == 2 &&
+    return c.row_dtype == KITTY_BF16 && !c.key_meta && !c.value_meta && c.cfg.d == D && c.cfg.g == G &&
+           c.cfg.key_bits == 2 && c.cfg.value_bits == 2 &&
            (group == 1 || group == 2 || group == 4 || group == 8) && c.cfg.d_boost <= 32 &&
            c.key_slot_bytes <= kKeySlotMax && c.value_slot_bytes == kValueSlot;
 }

@@ -390,9 +390,15 @@ __global__ void dequant_value_pages_kernel(const uint8_t* slots, int64_t stride,
 // Cache runtime: append (insert_token + maybe_pack) and prefill
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void copy_row_bf16(uint16_t* dst, const uint16_t* src, int d) {
-    if ((d % 8) == 0) {
-        for (int i = threadIdx.x; i < d / 8; i += blockDim.x)
+// Row element of the cache (bf16 bits or float) as float
+__device__ __forceinline__ float row_elem(const uint16_t* p, int64_t i) { return bf16_to_f32(p[i]); }
+__device__ __forceinline__ float row_elem(const float* p, int64_t i) { return p[i]; }
+
+template <typename T>
+__device__ __forceinline__ void copy_row(T* dst, const T* src, int d) {
+    constexpr int kPer = 16 / sizeof(T);  // elements per 16-byte vector
+    if ((d % kPer) == 0) {
+        for (int i = threadIdx.x; i < d / kPer; i += blockDim.x)
             reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
     } else {
         for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
@@ -400,47 +406,53 @@ __device__ __forceinline__ void copy_row_bf16(uint16_t* dst, const uint16_t* src
 }
 
 // Pack key page `p` of unit `u` from `rows` (g consecutive rows of a ring of
-// size `wrap` starting at `start`) into its block-table slot.
-__device__ void pack_key_into_cache(const KittyCacheDesc& c, int u, int p, const uint16_t* base,
-                                    int start, int wrap, uint8_t* smem) {
+// size `wrap` starting at `start`) into its block-table slot (+ its f32
+// metadata into the side table when the cache keeps one).
+template <typename T>
+__device__ void pack_key_into_cache(const KittyCacheDesc& c, int u, int p, const T* base, int start, int wrap,
+                                    uint8_t* smem) {
     const KittyConfigC& k = c.cfg;
     if (p >= c.max_pages) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
         return;
     }
-    uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
-    size_t off = ((size_t)k.g * k.d * 2 + 15) & ~size_t(15);
+    T* tile = reinterpret_cast<T*>(smem);
+    size_t off = ((size_t)k.g * k.d * sizeof(T) + 15) & ~size_t(15);
     uint8_t* slot = smem + off;
     off += ((size_t)max(KeyLayout{k.d, k.g, k.d_boost}.bytes(), ValueLayout{k.d, k.g}.bytes()) + 15) & ~size_t(15);
     PackScratch sc = carve_scratch(smem + off, k.d);
     if (!stage_rows(tile, base, start, wrap, k.g, k.d)) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_NONFINITE);
     }
-    pack_key_tile(tile, k.g, k.d, k.d_boost, nullptr, slot, sc, nullptr, nullptr);
     const int32_t s = c.key_block_table[(int64_t)u * c.max_pages + p];
+    float* meta = c.key_meta ? c.key_meta + (int64_t)s * 2 * k.d : nullptr;
+    pack_key_tile(tile, k.g, k.d, k.d_boost, nullptr, slot, sc, meta, meta ? meta + k.d : nullptr);
     copy_slot_out(slot, c.key_pool + (int64_t)s * c.key_slot_bytes, KeyLayout{k.d, k.g, k.d_boost}.bytes());
 }
 
-__device__ void pack_value_into_cache(const KittyCacheDesc& c, int u, int p, const uint16_t* base,
-                                      int start, int wrap, uint8_t* smem) {
+template <typename T>
+__device__ void pack_value_into_cache(const KittyCacheDesc& c, int u, int p, const T* base, int start, int wrap,
+                                      uint8_t* smem) {
     const KittyConfigC& k = c.cfg;
     if (p >= c.max_pages) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
         return;
     }
-    uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
-    uint8_t* slot = smem + (((size_t)k.g * k.d * 2 + 15) & ~size_t(15));
+    T* tile = reinterpret_cast<T*>(smem);
+    uint8_t* slot = smem + (((size_t)k.g * k.d * sizeof(T) + 15) & ~size_t(15));
     if (!stage_rows(tile, base, start, wrap, k.g, k.d)) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_NONFINITE);
     }
-    pack_value_tile(tile, k.g, k.d, slot, nullptr, nullptr);
     const int32_t s = c.value_block_table[(int64_t)u * c.max_pages + p];
+    float* meta = c.value_meta ? c.value_meta + (int64_t)s * 2 * k.g : nullptr;
+    pack_value_tile(tile, k.g, k.d, slot, meta, meta ? meta + k.g : nullptr);
     copy_slot_out(slot, c.value_pool + (int64_t)s * c.value_slot_bytes, ValueLayout{k.d, k.g}.bytes());
 }
 
 // insert_token (cache.py:107-123) for one unit per CTA, then the pack trigger
-// of maybe_pack (cache.py:144-178) on this unit's own counts.
-__global__ void append_kernel(KittyCacheDesc c, const uint16_t* k_new, const uint16_t* v_new) {
+// of maybe_pack (cache.py:144-178) on this unit's own counts.  T = the row type.
+template <typename T>
+__global__ void append_kernel(KittyCacheDesc c, const T* k_new, const T* v_new) {
     extern __shared__ __align__(16) uint8_t smem[];
     // the attention grid that follows may run its prologue now (it waits on us
     // with griddepcontrol.wait before reading the cache)
@@ -449,47 +461,53 @@ __global__ void append_kernel(KittyCacheDesc c, const uint16_t* k_new, const uin
     const int u = blockIdx.x;
     const int d = k.d, S = k.s, G = k.g, W = k.r + k.g;
     const int t = c.unit_len[u];
-    const uint16_t* kr = k_new + (int64_t)u * d;
-    const uint16_t* vr = v_new + (int64_t)u * d;
-    uint16_t* kq = c.k_qbuf + (int64_t)u * G * d;
-    uint16_t* vring = c.v_ring + (int64_t)u * W * d;
+    const T* kr = k_new + (int64_t)u * d;
+    const T* vr = v_new + (int64_t)u * d;
+    T* ksink = static_cast<T*>(c.k_sink);
+    T* vsink = static_cast<T*>(c.v_sink);
+    T* kq = static_cast<T*>(c.k_qbuf) + (int64_t)u * G * d;
+    T* vring = static_cast<T*>(c.v_ring) + (int64_t)u * W * d;
     if (t < S) {
-        copy_row_bf16(c.k_sink + ((int64_t)u * S + t) * d, kr, d);
-        copy_row_bf16(c.v_sink + ((int64_t)u * S + t) * d, vr, d);
+        copy_row(ksink + ((int64_t)u * S + t) * d, kr, d);
+        copy_row(vsink + ((int64_t)u * S + t) * d, vr, d);
     } else {
         const int pc = t - S;  // position past the sink
-        copy_row_bf16(kq + (int64_t)(pc % G) * d, kr, d);
-        copy_row_bf16(vring + (int64_t)(pc % W) * d, vr, d);
+        copy_row(kq + (int64_t)(pc % G) * d, kr, d);
+        copy_row(vring + (int64_t)(pc % W) * d, vr, d);
     }
     const int n = t + 1;
     const int past = n > S ? n - S : 0;
     const int vtot = past > k.r ? past - k.r : 0;  // tokens that left the local window
     const bool kpack = past > 0 && past % G == 0, vpack = vtot > 0 && vtot % G == 0;
-    if (d == fastpack::kD && G == fastpack::kG && (kpack || vpack)) {
-        // the bulk packer's routines: the page rows arrive by TMA (async proxy),
-        // so the row this CTA just stored must be visible to it first
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncthreads();
-        fastpack::Smem& s = *reinterpret_cast<fastpack::Smem*>(smem);
-        if (kpack) {
-            const int p = past / G - 1;
-            if (p >= c.max_pages) {
-                if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
-            } else {
-                fastpack::key_page(s, kq, 0, G, k.d_boost,
-                                   c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes,
-                                   c.status);
-            }
+    bool fast = false;
+    if constexpr (sizeof(T) == 2) fast = d == fastpack::kD && G == fastpack::kG && !c.key_meta && !c.value_meta;
+    if (fast && (kpack || vpack)) {
+        if constexpr (sizeof(T) == 2) {
+            // the bulk packer's routines: the page rows arrive by TMA (async proxy),
+            // so the row this CTA just stored must be visible to it first
+            asm volatile("fence.proxy.async.global;" ::: "memory");
             __syncthreads();
-        }
-        if (vpack) {
-            const int p = vtot / G - 1;
-            if (p >= c.max_pages) {
-                if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
-            } else {
-                fastpack::value_page(s, vring, (p * G) % W, W,
-                                     c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes,
-                                     c.status);
+            fastpack::Smem& s = *reinterpret_cast<fastpack::Smem*>(smem);
+            if (kpack) {
+                const int p = past / G - 1;
+                if (p >= c.max_pages) {
+                    if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+                } else {
+                    fastpack::key_page(s, kq, 0, G, k.d_boost,
+                                       c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes,
+                                       c.status);
+                }
+                __syncthreads();
+            }
+            if (vpack) {
+                const int p = vtot / G - 1;
+                if (p >= c.max_pages) {
+                    if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+                } else {
+                    fastpack::value_page(s, vring, (p * G) % W, W,
+                                         c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes,
+                                         c.status);
+                }
             }
         }
     } else {
@@ -506,8 +524,8 @@ __global__ void append_kernel(KittyCacheDesc c, const uint16_t* k_new, const uin
 
 // Prefill, fp rows: every prompt token whose final home (after the fold of
 // `P` appends) is a sink / q-buffer / ring row is copied there.
-__global__ void prefill_rows_kernel(KittyCacheDesc c, const uint16_t* keys, const uint16_t* values,
-                                    int P) {
+template <typename T>
+__global__ void prefill_rows_kernel(KittyCacheDesc c, const T* keys, const T* values, int P) {
     const KittyConfigC& k = c.cfg;
     const int u = blockIdx.y;
     const int d = k.d, S = k.s, G = k.g, W = k.r + k.g;
@@ -521,15 +539,15 @@ __global__ void prefill_rows_kernel(KittyCacheDesc c, const uint16_t* keys, cons
     const int n_fp = min(P, S) + (P > t_fp ? P - t_fp : 0);
     for (int i = blockIdx.x; i < n_fp; i += gridDim.x) {
         const int t = i < min(P, S) ? i : t_fp + (i - min(P, S));
-        const uint16_t* kr = keys + ((int64_t)u * P + t) * d;
-        const uint16_t* vr = values + ((int64_t)u * P + t) * d;
+        const T* kr = keys + ((int64_t)u * P + t) * d;
+        const T* vr = values + ((int64_t)u * P + t) * d;
         if (t < S) {
-            copy_row_bf16(c.k_sink + ((int64_t)u * S + t) * d, kr, d);
-            copy_row_bf16(c.v_sink + ((int64_t)u * S + t) * d, vr, d);
+            copy_row(static_cast<T*>(c.k_sink) + ((int64_t)u * S + t) * d, kr, d);
+            copy_row(static_cast<T*>(c.v_sink) + ((int64_t)u * S + t) * d, vr, d);
         } else {
             const int pc = t - S;
-            if (pc >= kp * G) copy_row_bf16(c.k_qbuf + ((int64_t)u * G + pc % G) * d, kr, d);
-            if (pc >= vp * G) copy_row_bf16(c.v_ring + ((int64_t)u * W + pc % W) * d, vr, d);
+            if (pc >= kp * G) copy_row(static_cast<T*>(c.k_qbuf) + ((int64_t)u * G + pc % G) * d, kr, d);
+            if (pc >= vp * G) copy_row(static_cast<T*>(c.v_ring) + ((int64_t)u * W + pc % W) * d, vr, d);
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) c.unit_len[u] = P;
@@ -537,8 +555,8 @@ __global__ void prefill_rows_kernel(KittyCacheDesc c, const uint16_t* keys, cons
 
 // Prefill, pages: blockIdx.x < kp packs key page blockIdx.x, else value page
 // blockIdx.x - kp; a page depends only on its own g tokens.
-__global__ void prefill_pack_kernel(KittyCacheDesc c, const uint16_t* keys, const uint16_t* values,
-                                    int P, int kp, int vp) {
+template <typename T>
+__global__ void prefill_pack_kernel(KittyCacheDesc c, const T* keys, const T* values, int P, int kp, int vp) {
     extern __shared__ __align__(16) uint8_t smem[];
     const KittyConfigC& k = c.cfg;
     const int u = blockIdx.y;
@@ -551,8 +569,8 @@ __global__ void prefill_pack_kernel(KittyCacheDesc c, const uint16_t* keys, cons
     }
 }
 
-// The same pages for d = g = 128 (kitty_pack_fast.cuh): 64 threads, one page
-// per CTA, the page's rows by TMA, bytes straight to the slot.
+// The same pages for d = g = 128 and bf16 rows (kitty_pack_fast.cuh): one
+// page per CTA, the page's rows by TMA, bytes straight to the slot.
 __global__ void __launch_bounds__(fastpack::kThreads) prefill_pack_fast_kernel(KittyCacheDesc c, const uint16_t* keys,
                                                                               const uint16_t* values, int P, int kp,
                                                                               int vp) {
@@ -577,7 +595,9 @@ __global__ void __launch_bounds__(fastpack::kThreads) prefill_pack_fast_kernel(K
     }
 }
 
-// flatten_keys / flatten_values (cache.py:210-215) of one unit.
+// flatten_keys / flatten_values (cache.py:210-215) of one unit; pages use the
+// f32 metadata side table when the cache keeps one, else the slot's f16 copy.
+template <typename T>
 __global__ void flatten_kernel(KittyCacheDesc c, int u, int n, float* keys_out, float* values_out) {
     const KittyConfigC& k = c.cfg;
     const int d = k.d, S = k.s, G = k.g, W = k.r + k.g;
@@ -588,41 +608,96 @@ __global__ void flatten_kernel(KittyCacheDesc c, int u, int n, float* keys_out, 
     const KeyLayout KL{d, G, k.d_boost};
     const ValueLayout VL{d, G};
     const int gb = G / 4, db = d / 4;
+    const T* ksink = static_cast<const T*>(c.k_sink);
+    const T* vsink = static_cast<const T*>(c.v_sink);
+    const T* kq = static_cast<const T*>(c.k_qbuf);
+    const T* vring = static_cast<const T*>(c.v_ring);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)n * d;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int t = static_cast<int>(i / d), ch = static_cast<int>(i % d);
         float kv, vv;
         if (t < S) {
-            kv = bf16_to_f32(c.k_sink[((int64_t)u * S + t) * d + ch]);
-            vv = bf16_to_f32(c.v_sink[((int64_t)u * S + t) * d + ch]);
+            kv = row_elem(ksink, ((int64_t)u * S + t) * d + ch);
+            vv = row_elem(vsink, ((int64_t)u * S + t) * d + ch);
         } else {
             const int pc = t - S;
             if (pc < kp * G) {
                 const int p = pc / G, tl = pc % G;
-                const uint8_t* slot = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes;
+                const int32_t sl = c.key_block_table[(int64_t)u * c.max_pages + p];
+                const uint8_t* slot = c.key_pool + (int64_t)sl * c.key_slot_bytes;
                 uint32_t code = (slot[KL.dense_off() + ch * gb + tl / 4] >> (2 * (tl % 4))) & 3u;
                 const uint8_t r = slot[KL.idx_off() + ch];
                 if (r != kSentinel) code |= ((slot[KL.high_off() + r * gb + tl / 4] >> (2 * (tl % 4))) & 3u) << 2;
-                const float s = half_bits_to_f32(ld_u16(slot + KL.scale_off() + 2 * ch));
-                const float z = half_bits_to_f32(ld_u16(slot + KL.zero_off() + 2 * ch));
+                const float* meta = c.key_meta ? c.key_meta + (int64_t)sl * 2 * d : nullptr;
+                const float s = meta ? meta[ch] : half_bits_to_f32(ld_u16(slot + KL.scale_off() + 2 * ch));
+                const float z = meta ? meta[d + ch] : half_bits_to_f32(ld_u16(slot + KL.zero_off() + 2 * ch));
                 kv = __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
             } else {
-                kv = bf16_to_f32(c.k_qbuf[((int64_t)u * G + pc % G) * d + ch]);
+                kv = row_elem(kq, ((int64_t)u * G + pc % G) * d + ch);
             }
             if (pc < vp * G) {
                 const int p = pc / G, tl = pc % G;
-                const uint8_t* slot = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes;
+                const int32_t sl = c.value_block_table[(int64_t)u * c.max_pages + p];
+                const uint8_t* slot = c.value_pool + (int64_t)sl * c.value_slot_bytes;
                 const uint32_t code = (slot[VL.codes_off() + tl * db + ch / 4] >> (2 * (ch % 4))) & 3u;
-                const float s = half_bits_to_f32(ld_u16(slot + VL.scale_off() + 2 * tl));
-                const float z = half_bits_to_f32(ld_u16(slot + VL.zero_off() + 2 * tl));
+                const float* meta = c.value_meta ? c.value_meta + (int64_t)sl * 2 * G : nullptr;
+                const float s = meta ? meta[tl] : half_bits_to_f32(ld_u16(slot + VL.scale_off() + 2 * tl));
+                const float z = meta ? meta[G + tl] : half_bits_to_f32(ld_u16(slot + VL.zero_off() + 2 * tl));
                 vv = __fadd_rn(__fmul_rn(static_cast<float>(code), s), z);
             } else {
-                vv = bf16_to_f32(c.v_ring[((int64_t)u * W + pc % W) * d + ch]);
+                vv = row_elem(vring, ((int64_t)u * W + pc % W) * d + ch);
             }
         }
         keys_out[i] = kv;
         values_out[i] = vv;
     }
+}
+
+// fake_quantize_matrix (quant.py:145-177): every lane -- a column of x
+// [rows][cols] (per_channel) or a row (per_token) -- quantized and dequantized
+// at its own width: 2 / 4 bits with the column quantizer of quant.py:102-120
+// (min / max, IEEE scale, rint half-even, clip; multiply then add), 16 = the
+// lane passes through.  One thread per lane.
+__global__ void fake_quantize_kernel(const float* x, int rows, int cols, int per_token, const int32_t* bits,
+                                     float* out) {
+    const int lanes = per_token ? rows : cols, len = per_token ? cols : rows;
+    const int64_t step = per_token ? 1 : cols;
+    for (int lane = blockIdx.x * blockDim.x + threadIdx.x; lane < lanes; lane += gridDim.x * blockDim.x) {
+        const float* src = per_token ? x + (int64_t)lane * cols : x + lane;
+        float* dst = per_token ? out + (int64_t)lane * cols : out + lane;
+        const int b = bits[lane];
+        if (b != 2 && b != 4) {
+            for (int i = 0; i < len; ++i) dst[i * step] = src[i * step];
+            continue;
+        }
+        float mn = src[0], mx = mn;
+        for (int i = 1; i < len; ++i) {
+            mn = fminf(mn, src[i * step]);
+            mx = fmaxf(mx, src[i * step]);
+        }
+        if (mn == 0.f || mx == 0.f) {  // a zero min / max carries the sign of the lane's last zero
+            float z = 0.f;
+            for (int i = len - 1; i >= 0; --i) {
+                if (src[i * step] == 0.f) {
+                    z = src[i * step];
+                    break;
+                }
+            }
+            mn = mn == 0.f ? z : mn;
+            mx = mx == 0.f ? z : mx;
+        }
+        const LaneQuant q(mn, mx, static_cast<float>((1 << b) - 1));
+        for (int i = 0; i < len; ++i)
+            dst[i * step] = __fadd_rn(__fmul_rn(static_cast<float>(q.code(src[i * step])), q.scale), mn);
+    }
+}
+
+cudaError_t launch_fake_quantize(const float* x, int rows, int cols, int per_token, const int32_t* bits, float* out,
+                                 cudaStream_t st) {
+    const int lanes = per_token ? rows : cols;
+    if (lanes == 0 || rows == 0 || cols == 0) return cudaSuccess;
+    fake_quantize_kernel<<<(lanes + 127) / 128, 128, 0, st>>>(x, rows, cols, per_token, bits, out);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -699,15 +774,21 @@ cudaError_t launch_dequant_value_pages(const uint8_t* slots, int64_t stride, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_append(const KittyCacheDesc& c, const uint16_t* k_new, const uint16_t* v_new,
-                          cudaStream_t st) {
+template <typename T>
+static cudaError_t append_t(const KittyCacheDesc& c, const void* k_new, const void* v_new, cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
-    if (units == 0) return cudaSuccess;
-    size_t sm = pack_smem_bytes(c.cfg.g, c.cfg.d, c.cfg.d_boost, 2);
-    if (c.cfg.d == fastpack::kD && c.cfg.g == fastpack::kG && sm < sizeof(fastpack::Smem)) sm = sizeof(fastpack::Smem);
-    if (cudaError_t e = set_kernel_smem((const void*)append_kernel, (int)sm)) return e;
-    append_kernel<<<units, fastpack::kThreads, sm, st>>>(c, k_new, v_new);
+    size_t sm = pack_smem_bytes(c.cfg.g, c.cfg.d, c.cfg.d_boost, sizeof(T));
+    if (sizeof(T) == 2 && c.cfg.d == fastpack::kD && c.cfg.g == fastpack::kG && sm < sizeof(fastpack::Smem))
+        sm = sizeof(fastpack::Smem);
+    auto kfn = append_kernel<T>;
+    if (cudaError_t e = set_kernel_smem((const void*)kfn, (int)sm)) return e;
+    kfn<<<units, fastpack::kThreads, sm, st>>>(c, static_cast<const T*>(k_new), static_cast<const T*>(v_new));
     return cudaGetLastError();
+}
+
+cudaError_t launch_append(const KittyCacheDesc& c, const void* k_new, const void* v_new, cudaStream_t st) {
+    if (c.num_seqs * c.cfg.h_kv == 0) return cudaSuccess;
+    return c.row_dtype == KITTY_F32 ? append_t<float>(c, k_new, v_new, st) : append_t<uint16_t>(c, k_new, v_new, st);
 }
 
 // KITTY_FAST_PACK=0 keeps prefill on the generic packer (A/B and parity knob)
@@ -716,29 +797,38 @@ static const int g_fast_pack = [] {
     return e ? std::atoi(e) : 1;
 }();
 
-cudaError_t launch_prefill(const KittyCacheDesc& c, const uint16_t* keys, const uint16_t* values,
-                           int P, cudaStream_t st) {
+template <typename T>
+static cudaError_t prefill_t(const KittyCacheDesc& c, const T* keys, const T* values, int P, cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
-    if (units == 0) return cudaSuccess;
     const int S = c.cfg.s, G = c.cfg.g;
     const int past = P > S ? P - S : 0;
     const int kp = past / G;
     const int vp = (past - min(c.cfg.r, past)) / G;
     const int n_fp = min(P, S) + (P > S + vp * G ? P - (S + vp * G) : 0);
     const int gx = n_fp > 0 ? min(n_fp, 1024) : 1;
-    prefill_rows_kernel<<<dim3(gx, units), 128, 0, st>>>(c, keys, values, P);
+    prefill_rows_kernel<T><<<dim3(gx, units), 128, 0, st>>>(c, keys, values, P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || kp + vp == 0) return e;
-    if (c.cfg.d == fastpack::kD && G == fastpack::kG && g_fast_pack) {
-        const int sm = static_cast<int>(sizeof(fastpack::Smem));
-        if ((e = set_kernel_smem((const void*)prefill_pack_fast_kernel, sm)) != cudaSuccess) return e;
-        prefill_pack_fast_kernel<<<dim3(kp + vp, units), fastpack::kThreads, sm, st>>>(c, keys, values, P, kp, vp);
-        return cudaGetLastError();
+    if constexpr (sizeof(T) == 2) {
+        if (c.cfg.d == fastpack::kD && G == fastpack::kG && g_fast_pack && !c.key_meta && !c.value_meta) {
+            const int sm = static_cast<int>(sizeof(fastpack::Smem));
+            if ((e = set_kernel_smem((const void*)prefill_pack_fast_kernel, sm)) != cudaSuccess) return e;
+            prefill_pack_fast_kernel<<<dim3(kp + vp, units), fastpack::kThreads, sm, st>>>(c, keys, values, P, kp, vp);
+            return cudaGetLastError();
+        }
     }
-    const size_t sm = pack_smem_bytes(G, c.cfg.d, c.cfg.d_boost, 2);
-    if ((e = set_kernel_smem((const void*)prefill_pack_kernel, (int)sm)) != cudaSuccess) return e;
-    prefill_pack_kernel<<<dim3(kp + vp, units), 128, sm, st>>>(c, keys, values, P, kp, vp);
+    const size_t sm = pack_smem_bytes(G, c.cfg.d, c.cfg.d_boost, sizeof(T));
+    auto kfn = prefill_pack_kernel<T>;
+    if ((e = set_kernel_smem((const void*)kfn, (int)sm)) != cudaSuccess) return e;
+    kfn<<<dim3(kp + vp, units), 128, sm, st>>>(c, keys, values, P, kp, vp);
     return cudaGetLastError();
+}
+
+cudaError_t launch_prefill(const KittyCacheDesc& c, const void* keys, const void* values, int P, cudaStream_t st) {
+    if (c.num_seqs * c.cfg.h_kv == 0) return cudaSuccess;
+    if (c.row_dtype == KITTY_F32)
+        return prefill_t(c, static_cast<const float*>(keys), static_cast<const float*>(values), P, st);
+    return prefill_t(c, static_cast<const uint16_t*>(keys), static_cast<const uint16_t*>(values), P, st);
 }
 
 cudaError_t launch_flatten(const KittyCacheDesc& c, int u, int n, float* ko, float* vo,
@@ -747,7 +837,10 @@ cudaError_t launch_flatten(const KittyCacheDesc& c, int u, int n, float* ko, flo
     const int64_t total = (int64_t)n * c.cfg.d;
     const int64_t want = (total + 255) / 256;
     const int blocks = static_cast<int>(want < 4096 ? want : 4096);
-    flatten_kernel<<<blocks, 256, 0, st>>>(c, u, n, ko, vo);
+    if (c.row_dtype == KITTY_F32)
+        flatten_kernel<float><<<blocks, 256, 0, st>>>(c, u, n, ko, vo);
+    else
+        flatten_kernel<uint16_t><<<blocks, 256, 0, st>>>(c, u, n, ko, vo);
     return cudaGetLastError();
 }
 

@@ -32,16 +32,16 @@ cudaError_t launch_dequant_key_pages(const uint8_t* slots, int64_t stride, int P
 cudaError_t launch_dequant_value_pages(const uint8_t* slots, int64_t stride, int P, int g, int d,
                                        const float* sc32, const float* ze32, float* out,
                                        cudaStream_t st);
-cudaError_t launch_append(const KittyCacheDesc& c, const uint16_t* k_new, const uint16_t* v_new,
-                          cudaStream_t st);
-cudaError_t launch_prefill(const KittyCacheDesc& c, const uint16_t* keys, const uint16_t* values,
-                           int P, cudaStream_t st);
+cudaError_t launch_fake_quantize(const float* x, int rows, int cols, int per_token, const int32_t* bits, float* out,
+                                 cudaStream_t st);
+cudaError_t launch_append(const KittyCacheDesc& c, const void* k_new, const void* v_new, cudaStream_t st);
+cudaError_t launch_prefill(const KittyCacheDesc& c, const void* keys, const void* values, int P, cudaStream_t st);
 cudaError_t launch_flatten(const KittyCacheDesc& c, int u, int n, float* ko, float* vo,
                            cudaStream_t st);
 
 // attention (kitty_attention.cu)
 size_t attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens);
-cudaError_t launch_decode_attention(const KittyCacheDesc& c, const uint16_t* q, void* out,
+cudaError_t launch_decode_attention(const KittyCacheDesc& c, const void* q, void* out,
                                     int out_dtype, int max_tokens, void* ws, size_t ws_bytes,
                                     cudaStream_t st);
 size_t dense_attention_workspace_bytes(int n_q, int length, int d);

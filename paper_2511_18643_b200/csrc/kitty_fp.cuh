@@ -153,8 +153,11 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
     const bool paged = tt >= S && pct < gm.kp * G;
     uint4 kw[4], vw[4];
     {
-        const uint16_t* krow = tt < S ? c.k_sink + ((int64_t)u * S + tt) * D : c.k_qbuf + ((int64_t)u * G + (pct % G)) * D;
-        const uint16_t* vrow = tt < S ? c.v_sink + ((int64_t)u * S + tt) * D : c.v_ring + ((int64_t)u * W + (pct % W)) * D;
+        // bf16 rows (the fused path runs for row_dtype KITTY_BF16 only)
+        const uint16_t* ksink = static_cast<const uint16_t*>(c.k_sink);
+        const uint16_t* vsink = static_cast<const uint16_t*>(c.v_sink);
+        const uint16_t* krow = tt < S ? ksink + ((int64_t)u * S + tt) * D : static_cast<const uint16_t*>(c.k_qbuf) + ((int64_t)u * G + (pct % G)) * D;
+        const uint16_t* vrow = tt < S ? vsink + ((int64_t)u * S + tt) * D : static_cast<const uint16_t*>(c.v_ring) + ((int64_t)u * W + (pct % W)) * D;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             if (!paged) kw[i] = __ldg(reinterpret_cast<const uint4*>(krow + 32 * qq) + i);

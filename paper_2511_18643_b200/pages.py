@@ -263,6 +263,31 @@ def select_boost(scores, boost_fraction: float, heuristic: str = "magnitude", se
     raise KittyError(f"unknown selection heuristic {heuristic!r}")
 
 
+def fake_quantize_matrix(x, axis: str, bits_per_lane) -> np.ndarray:
+    """quant.py:145-177 on the device (kitty_fake_quantize): quantize-then-
+    dequantize every lane of ``x`` -- a column for ``per_channel``, a row for
+    ``per_token`` -- at its own width in {2, 4, 16} (16 passes through)."""
+    lib = _lib.load_library()
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.ndim != 2:
+        raise KittyError("fake_quantize_matrix needs a 2-D matrix")
+    if axis not in ("per_channel", "per_token"):
+        raise KittyError(f"axis must be per_channel or per_token, got {axis!r}")
+    lanes = x.shape[1] if axis == "per_channel" else x.shape[0]
+    bits = np.asarray(bits_per_lane, dtype=np.int64)
+    if bits.shape != (lanes,):
+        raise KittyError(f"need {lanes} lane widths, got shape {bits.shape}")
+    if not np.isin(bits, (2, 4, 16)).all():
+        raise KittyError("lane widths must be in {2, 4, 16}")
+    dev = _device()
+    xt = torch.from_numpy(x).to(dev)
+    bt = torch.from_numpy(bits.astype(np.int32)).to(dev)
+    out = torch.empty_like(xt)
+    _lib.check(lib.kitty_fake_quantize(xt.data_ptr(), x.shape[0], x.shape[1], int(axis == "per_token"),
+                                       bt.data_ptr(), out.data_ptr(), _stream()), "fake_quantize_matrix")
+    return out.cpu().numpy()
+
+
 def split_key_body(body: np.ndarray, d: int, g: int, d_boost: int):
     """Components of a KTYP key body in declaration order (pages.py:215-221)."""
     body = np.asarray(body, dtype=np.uint8)

@@ -5,6 +5,7 @@ reference's byte accounting and config validation (no compute calls)."""
 import ctypes
 import os
 import re
+import subprocess
 
 import pytest
 
@@ -12,7 +13,8 @@ import paper_2511_18643_b200 as kb
 from paper_2511_18643_b200 import _lib
 from oracle import kitty_oracle as ko
 
-HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "kitty_b200.h")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "kitty_b200.h")
 
 
 def declared_symbols():
@@ -100,13 +102,20 @@ def test_status_codes_map_to_reference_exceptions():
     _lib.raise_status(0)
 
 
-def test_desc_struct_layout_matches_header():
-    # offsets of the POD the C side reads (KittyCacheDesc in kitty_b200.h)
+def test_desc_struct_layout_matches_header(tmp_path):
+    # offsets of the POD the C side reads (KittyCacheDesc in kitty_b200.h), as
+    # the C compiler lays it out, against the ctypes mirror the shim passes
+    fields = [f[0] for f in _lib.KittyCacheDesc._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "kitty_b200.h"\nint main(void) {\n'
+                   + "".join(f'  printf("%zu\\n", offsetof(KittyCacheDesc, {f}));\n' for f in fields)
+                   + '  printf("%zu\\n", sizeof(KittyCacheDesc));\n  return 0;\n}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [getattr(_lib.KittyCacheDesc, f).offset for f in fields] + [ctypes.sizeof(_lib.KittyCacheDesc)]
+    assert got == want
     assert ctypes.sizeof(_lib.KittyConfigC) == 36
-    assert _lib.KittyCacheDesc.num_seqs.offset == 36
-    assert _lib.KittyCacheDesc.key_slot_bytes.offset == 48
-    assert _lib.KittyCacheDesc.unit_len.offset == 64
-    assert ctypes.sizeof(_lib.KittyCacheDesc) == 64 + 10 * 8
 
 
 def test_invalid_args_rejected_without_gpu():

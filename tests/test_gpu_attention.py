@@ -110,7 +110,7 @@ def test_fp_chunks_straddling_sink_and_pages(cuda, s, r, n, group):
     k = _keys(rng, (h_kv, n, 128))
     v = _bf16(rng.normal(0, 1, (h_kv, n, 128)))
     q = _bf16(rng.normal(0, 1, (h_kv * group, 128)))
-    st = cuda.KittyCacheState(cfg, max_tokens=n)
+    st = cuda.KittyCacheState(cfg, max_tokens=n, row_dtype=torch.bfloat16)  # the fused kernels
     st.prefill(k, v)
     got = st.attend(q).outputs
     oc = ko.OracleCache(s, r, 128, 128, h_kv, h_kv * group, 0.125, metadata16=True)

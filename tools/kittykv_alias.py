@@ -1,0 +1,33 @@
+"""pytest plugin: run the reference's own tests (kittykv's pkg/tests) against
+this package -- `import kittykv` resolves to paper_2511_18643_b200 -- and mark
+the cases that exercise parts of the reference outside the device hot path as
+expected failures, with the reason (SURVEY.md §2 scope column)."""
+import sys
+
+import pytest
+
+import paper_2511_18643_b200 as _kb
+
+OUT_OF_SCOPE = {
+    # 16-bit pass-through pages: a debug mode of the reference, not built on the device
+    "test_cache.py::test_prefill_equals_fold_of_inserts[16-": "pass-through (16-bit) pages are not built on the device",
+    "test_cache.py::test_passthrough_matches_dense_oracle": "pass-through (16-bit) pages are not built on the device",
+    "test_cache.py::test_order_reconstruction_fuzz": "uses pass-through (16-bit) pages, not built on the device",
+    # probabilities: a debug output a flash-decode never materialises
+    "test_cache.py::test_singleton_softmax": "return_probs is not materialised by the fused kernel",
+    "test_cache.py::test_probabilities_normalized": "return_probs is not materialised by the fused kernel",
+    "test_cache.py::test_oracle_uniform_keys_uniform_probs": "oracle_attend returns outputs only (no probs)",
+    "test_cache.py::test_oracle_concentration_on_aligned_key": "oracle_attend returns outputs only (no probs)",
+}
+
+
+def pytest_configure(config):
+    sys.modules["kittykv"] = _kb
+
+
+def pytest_collection_modifyitems(config, items):
+    for item in items:
+        nid = item.nodeid.split("/")[-1]
+        for key, why in OUT_OF_SCOPE.items():
+            if nid.startswith(key):
+                item.add_marker(pytest.mark.xfail(reason=why, strict=False))
