@@ -103,6 +103,18 @@ typedef struct KittyCacheDesc {
                                   slot's f16 copy (the reference keeps f32 in
                                   memory, cache.py:157-161)                     */
     float* value_meta;         /* optional [slots][2 g]: the same for values   */
+    /* Page pool (optional; NULL key_free = static block tables written by the
+     * caller).  With a pool the block tables start at -1 and a page's slot is
+     * popped from the side's free stack by the kernel that packs (or imports)
+     * the page, then recorded in the unit's block table; kitty_release_sequences
+     * pushes a retired sequence's slots back.  Pops and pushes never share a
+     * launch, so a stack is an array plus an atomic top.  An empty stack sets
+     * KITTY_STATUS_OVERFLOW and the page is dropped. */
+    int32_t* key_free;         /* [key_slots] free key-slot indices (stack)    */
+    int32_t* value_free;       /* [value_slots] free value-slot indices        */
+    int32_t* free_top;         /* [2] entries on the key / value stacks        */
+    int32_t key_slots;         /* key_pool capacity in slots                   */
+    int32_t value_slots;       /* value_pool capacity in slots                 */
 } KittyCacheDesc;
 
 /* ---- sizes / config --------------------------------------------------- */
@@ -181,6 +193,27 @@ int kitty_append(const KittyCacheDesc* cache, const void* k_new, const void* v_n
  * are packed in parallel. */
 int kitty_prefill(const KittyCacheDesc* cache, const void* keys, const void* values,
                   int32_t prompt_len, void* stream);
+
+/* Retire sequences [first_seq, first_seq + num_seqs): every unit's key and
+ * value slots go back to the pool's free stacks (no-op without a pool), its
+ * block-table entries become -1 and its length 0, so the rows can admit a new
+ * sequence (prefill / append).  The reference has one state per sequence and
+ * frees it by dropping the object (cache.py:83-105); this is that drop for a
+ * batch whose pages live in a shared pool. */
+int kitty_release_sequences(const KittyCacheDesc* cache, int32_t first_seq, int32_t num_seqs,
+                            void* stream);
+
+/* deserialize_page (pages.py:246-292) into the cache: `bodies` holds
+ * num_pages KTYP bodies (header stripped and checked by the caller against
+ * the cache's d / g / d_boost) of kind 0 = key, 1 = value, contiguous, in
+ * device memory.  Page first_page + i of `unit` gets a slot (popped from the
+ * pool, or the block table's entry) and the body is copied in; key pages are
+ * checked like dequantize_key_page (pages.py:128-135: d - d_boost sentinels,
+ * boost_idx a bijection onto 0..d_boost-1), a violation sets
+ * KITTY_STATUS_PAGE_FORMAT.  The f32 metadata side tables, when present, get
+ * the bodies' f16 scale / zero promoted to f32 (pages.py:263-264). */
+int kitty_import_pages(const KittyCacheDesc* cache, int32_t unit, int32_t kind, const uint8_t* bodies,
+                       int32_t first_page, int32_t num_pages, void* stream);
 
 /* flatten_keys / flatten_values (cache.py:210-215) of one unit: [n][d] f32,
  * pages dequantized from their f16 metadata.  n = tokens of the unit. */

@@ -55,6 +55,11 @@ class KittyCacheDesc(ctypes.Structure):
         ("reserved", c_int32),
         ("key_meta", c_void_p),
         ("value_meta", c_void_p),
+        ("key_free", c_void_p),
+        ("value_free", c_void_p),
+        ("free_top", c_void_p),
+        ("key_slots", c_int32),
+        ("value_slots", c_int32),
     ]
 
 
@@ -78,6 +83,9 @@ SIGNATURES = [
     ("kitty_fake_quantize", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     ("kitty_append", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_void_p, c_void_p, c_void_p]),
     ("kitty_prefill", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_void_p, c_void_p, c_int32, c_void_p]),
+    ("kitty_release_sequences", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_int32, c_int32, c_void_p]),
+    ("kitty_import_pages", ctypes.c_int,
+     [ctypes.POINTER(KittyCacheDesc), c_int32, c_int32, c_void_p, c_int32, c_int32, c_void_p]),
     ("kitty_flatten", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     ("kitty_attention_workspace_bytes", c_size_t, [ctypes.POINTER(KittyCacheDesc), c_int32]),
     ("kitty_decode_attention", ctypes.c_int,
@@ -136,7 +144,7 @@ def raise_status(word: int, what: str = "") -> None:
     if word & STATUS_NONFINITE:
         raise KittyError(f"{what}: page contains non-finite values")
     if word & STATUS_OVERFLOW:
-        raise KittyError(f"{what}: cache capacity (block table) exceeded")
+        raise KittyError(f"{what}: cache capacity exceeded (block table full or page pool empty)")
     if word & STATUS_LENGTH:
         raise KittyError(f"{what}: a sequence is longer than the max_tokens bound passed to attention")
     raise KittyError(f"{what}: device status 0x{word:x}")

@@ -56,13 +56,27 @@ def _check_device_config(cfg: KittyConfig):
 
 
 class KittyBatchCache:
-    """B sequences of Kitty KV cache for one attention layer, resident in HBM."""
+    """B sequences of Kitty KV cache for one attention layer, resident in HBM.
+
+    Pages live in a shared **page pool** (PagedAttention-style,
+    PAPER.md:371-374,392-396): ``key_pool`` / ``value_pool`` hold
+    ``pool_pages`` KTYP slots each, a device free stack per side hands a slot
+    to every page as it is packed (append / prefill / import, inside the
+    kernel: no host round trip, CUDA-graph safe), and each unit's block table
+    maps its page index to the slot.  ``retire`` returns a finished sequence's
+    slots and ``admit`` prefills a new one into the freed row (continuous
+    batching).  ``pool_pages=None`` sizes the pool for every sequence at
+    ``max_tokens`` and lets it grow; an explicit budget is fixed and an append /
+    prefill that would need more slots raises ``KittyError`` before launching.
+    """
 
     def __init__(self, cfg: KittyConfig, num_seqs: int, max_tokens: int, device=None,
-                 row_dtype: torch.dtype = torch.bfloat16, f32_metadata: bool = False):
+                 row_dtype: torch.dtype = torch.bfloat16, f32_metadata: bool = False,
+                 pool_pages: int | None = None):
         """``row_dtype``: bf16 (the fused decode path) or float32 (the reference's
         precision, generic kernels); ``f32_metadata``: keep each page's float32
-        scale / zero (the reference's in-memory values) beside its f16 slot."""
+        scale / zero (the reference's in-memory values) beside its f16 slot;
+        ``pool_pages``: slots per side (None = units x pages at max_tokens, growable)."""
         _check_device_config(cfg)
         if row_dtype not in (torch.bfloat16, torch.float32):
             raise KittyError("row_dtype must be torch.bfloat16 or torch.float32")
@@ -79,30 +93,46 @@ class KittyBatchCache:
         self.lengths = [0] * self.num_seqs  # host mirror of unit_len (no syncs needed)
         self.key_pack_events = [0] * self.num_seqs
         self.value_pack_events = [0] * self.num_seqs
-        self._alloc(max_tokens)
+        self.auto_pool = pool_pages is None
+        if pool_pages is not None and int(pool_pages) < 0:
+            raise KittyError("pool_pages must be >= 0")
+        self._alloc(max_tokens, None if pool_pages is None else int(pool_pages))
         self._ws = None
 
     # -- storage -------------------------------------------------------------
 
-    def _alloc(self, max_tokens: int):
+    def _pages_for(self, max_tokens: int) -> int:
+        return max(1, -(-max(0, int(max_tokens) - self.cfg.s) // self.cfg.g))
+
+    def _alloc(self, max_tokens: int, pool_pages: int | None):
         cfg, dev, u = self.cfg, self.device, self.units
         self.max_tokens = int(max_tokens)
-        self.max_pages = max(1, -(-max(0, self.max_tokens - cfg.s) // cfg.g))
+        self.max_pages = self._pages_for(self.max_tokens)
+        slots = u * self.max_pages if pool_pages is None else pool_pages
         bf = self.row_dtype
         self.unit_len = torch.zeros(u, dtype=torch.int32, device=dev)
         self.k_sink = torch.zeros((u, cfg.s, cfg.d), dtype=bf, device=dev)
         self.v_sink = torch.zeros((u, cfg.s, cfg.d), dtype=bf, device=dev)
         self.k_qbuf = torch.zeros((u, cfg.g, cfg.d), dtype=bf, device=dev)
         self.v_ring = torch.zeros((u, cfg.r + cfg.g, cfg.d), dtype=bf, device=dev)
-        self.key_pool = torch.zeros((u * self.max_pages, self.key_slot), dtype=torch.uint8, device=dev)
-        self.value_pool = torch.zeros((u * self.max_pages, self.value_slot), dtype=torch.uint8, device=dev)
-        ident = torch.arange(u * self.max_pages, dtype=torch.int32, device=dev).view(u, self.max_pages)
-        self.key_block_table = ident.clone()
-        self.value_block_table = ident.clone()
+        self.key_block_table = torch.full((u, self.max_pages), -1, dtype=torch.int32, device=dev)
+        self.value_block_table = torch.full((u, self.max_pages), -1, dtype=torch.int32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._alloc_pool(slots)
+
+    def _alloc_pool(self, slots: int):
+        cfg, dev = self.cfg, self.device
+        self.pool_pages = int(slots)
+        self.key_pool = torch.zeros((max(1, slots), self.key_slot), dtype=torch.uint8, device=dev)
+        self.value_pool = torch.zeros((max(1, slots), self.value_slot), dtype=torch.uint8, device=dev)
+        # free stacks: pops take the top, so slot 0 is handed out first
+        self.key_free = torch.arange(slots - 1, -1, -1, dtype=torch.int32, device=dev)
+        self.value_free = self.key_free.clone()
+        self.free_top = torch.full((2,), slots, dtype=torch.int32, device=dev)
+        self.free_pages = [slots, slots]  # host mirror of free_top
         if self.f32_metadata:
-            self.key_meta = torch.zeros((u * self.max_pages, 2 * cfg.d), dtype=torch.float32, device=dev)
-            self.value_meta = torch.zeros((u * self.max_pages, 2 * cfg.g), dtype=torch.float32, device=dev)
+            self.key_meta = torch.zeros((max(1, slots), 2 * cfg.d), dtype=torch.float32, device=dev)
+            self.value_meta = torch.zeros((max(1, slots), 2 * cfg.g), dtype=torch.float32, device=dev)
         else:
             self.key_meta = self.value_meta = None
         self._build_desc()
@@ -127,30 +157,67 @@ class KittyBatchCache:
         d.row_dtype = _lib.KITTY_F32 if self.row_dtype == torch.float32 else _lib.KITTY_BF16
         d.key_meta = self.key_meta.data_ptr() if self.key_meta is not None else None
         d.value_meta = self.value_meta.data_ptr() if self.value_meta is not None else None
+        d.key_free = self.key_free.data_ptr()
+        d.value_free = self.value_free.data_ptr()
+        d.free_top = self.free_top.data_ptr()
+        d.key_slots = self.pool_pages
+        d.value_slots = self.pool_pages
         self.desc = d
         self._desc_ref = ctypes.byref(d)
 
     def grow(self, max_tokens: int):
-        """Re-allocate for longer sequences, keeping every page and row."""
-        old = dict(kp=self.key_pool, vp=self.value_pool, ln=self.unit_len, ks=self.k_sink,
-                   vs=self.v_sink, kq=self.k_qbuf, vr=self.v_ring, mp=self.max_pages,
-                   kbt=self.key_block_table, vbt=self.value_block_table, st=self.status,
-                   km=self.key_meta, vm=self.value_meta)
-        self._alloc(max_tokens)
-        u = self.units
-        kv = self.key_pool.view(u, self.max_pages, -1)
-        vv = self.value_pool.view(u, self.max_pages, -1)
-        kv[:, : old["mp"]] = old["kp"][old["kbt"].reshape(-1).long()].view(u, old["mp"], -1)
-        vv[:, : old["mp"]] = old["vp"][old["vbt"].reshape(-1).long()].view(u, old["mp"], -1)
-        if self.f32_metadata:
-            self.key_meta.view(u, self.max_pages, -1)[:, : old["mp"]] = \
-                old["km"][old["kbt"].reshape(-1).long()].view(u, old["mp"], -1)
-            self.value_meta.view(u, self.max_pages, -1)[:, : old["mp"]] = \
-                old["vm"][old["vbt"].reshape(-1).long()].view(u, old["mp"], -1)
-        for name, key in (("unit_len", "ln"), ("k_sink", "ks"), ("v_sink", "vs"), ("k_qbuf", "kq"),
-                          ("v_ring", "vr"), ("status", "st")):
-            getattr(self, name).copy_(old[key])
+        """Longer sequences: widen the block tables (int32 per page; slots and
+        rows stay where they are).  An auto-sized pool also gains the slots the
+        new length needs -- the one path that copies page bytes."""
+        old_mp = self.max_pages
+        self.max_tokens = int(max_tokens)
+        self.max_pages = self._pages_for(self.max_tokens)
+        if self.max_pages > old_mp:
+            for name in ("key_block_table", "value_block_table"):
+                t = getattr(self, name)
+                nt = torch.full((self.units, self.max_pages), -1, dtype=torch.int32, device=self.device)
+                nt[:, :old_mp] = t
+                setattr(self, name, nt)
+        if self.auto_pool and self.units * self.max_pages > self.pool_pages:
+            self._grow_pool(self.units * self.max_pages)
+        self._build_desc()
         self._ws = None
+
+    def _grow_pool(self, slots: int):
+        old = dict(kp=self.key_pool, vp=self.value_pool, kf=self.key_free, vf=self.value_free,
+                   km=self.key_meta, vm=self.value_meta, n=self.pool_pages, free=list(self.free_pages))
+        self._alloc_pool(slots)
+        n = old["n"]
+        self.key_pool[:n] = old["kp"][:n]
+        self.value_pool[:n] = old["vp"][:n]
+        if self.f32_metadata:
+            self.key_meta[:n] = old["km"][:n]
+            self.value_meta[:n] = old["vm"][:n]
+        added = torch.arange(slots - 1, n - 1, -1, dtype=torch.int32, device=self.device)
+        for side, (stack, ostack) in enumerate(((self.key_free, old["kf"]), (self.value_free, old["vf"]))):
+            top = old["free"][side]
+            stack[: slots - n] = added
+            stack[slots - n: slots - n + top] = ostack[:top]
+            self.free_pages[side] = top + slots - n
+        self.free_top.copy_(torch.tensor(self.free_pages, dtype=torch.int32))
+
+    def _reserve(self, key_pages: int, value_pages: int):
+        """Host-side admission control: the pool must hold the pages the next
+        launch packs (the host mirror of the stacks is exact: page counts follow
+        from the lengths)."""
+        if key_pages <= self.free_pages[0] and value_pages <= self.free_pages[1]:
+            return
+        if self.auto_pool:
+            short = max(key_pages - self.free_pages[0], value_pages - self.free_pages[1])
+            self._grow_pool(self.pool_pages + max(short, self.pool_pages // 2, 1))
+            self._build_desc()
+            return
+        raise KittyError(f"page pool exhausted: {key_pages} key / {value_pages} value pages needed, "
+                         f"{self.free_pages[0]} / {self.free_pages[1]} free of {self.pool_pages}")
+
+    def _page_pair(self, n: int):
+        c = component_counts(self.cfg, n)
+        return c["key_pages"], c["value_pages"]
 
     def workspace(self, max_tokens: int) -> torch.Tensor:
         need = int(self.lib.kitty_attention_workspace_bytes(self._desc_ref, max_tokens))
@@ -171,13 +238,33 @@ class KittyBatchCache:
             self.value_pack_events[b] += 1
 
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor):
-        """Step 1 + step 3 for every sequence: k_new/v_new [B, h_kv, D] bf16."""
+        """Step 1 + step 3 for every sequence: k_new/v_new [B, h_kv, D] bf16.
+        Every row appends (a retired row restarts from its sink)."""
         cfg = self.cfg
         if max(self.lengths) + 1 > self.max_tokens:
             self.grow(max(2 * self.max_tokens, max(self.lengths) + 1))
+        need = self.append_page_need()
+        self._reserve(*need)
         k_new = self._rows(k_new, (self.num_seqs, cfg.h_kv, cfg.d), "k_new")
         v_new = self._rows(v_new, (self.num_seqs, cfg.h_kv, cfg.d), "v_new")
         _lib.check(self.lib.kitty_append(self._desc_ref, k_new.data_ptr(), v_new.data_ptr(), _stream()), "append")
+        self.advance_host(need)
+
+    def append_page_need(self):
+        """(key, value) pages the next append packs: the host mirror of its pops."""
+        kneed = vneed = 0
+        for n in self.lengths:
+            kp0, vp0 = self._page_pair(n)
+            kp1, vp1 = self._page_pair(n + 1)
+            kneed += (kp1 - kp0) * self.cfg.h_kv
+            vneed += (vp1 - vp0) * self.cfg.h_kv
+        return kneed, vneed
+
+    def advance_host(self, need=None):
+        """Host mirror after one append launch (eager or graph replay)."""
+        need = self.append_page_need() if need is None else need
+        self.free_pages[0] -= need[0]
+        self.free_pages[1] -= need[1]
         for b in range(self.num_seqs):
             self.lengths[b] += 1
             self._count_events(b, self.lengths[b])
@@ -203,7 +290,11 @@ class KittyBatchCache:
         keys = self._rows(keys, (self.num_seqs, cfg.h_kv, p, cfg.d), "keys")
         values = self._rows(values, (self.num_seqs, cfg.h_kv, p, cfg.d), "values")
         if all(x == p for x in lengths):
+            kp, vp = self._page_pair(p)
+            self._reserve(kp * self.units, vp * self.units)
             _lib.check(self.lib.kitty_prefill(self._desc_ref, keys.data_ptr(), values.data_ptr(), p, _stream()), "prefill")
+            self.free_pages[0] -= kp * self.units
+            self.free_pages[1] -= vp * self.units
             for b in range(self.num_seqs):
                 self._set_length(b, p)
         else:
@@ -220,7 +311,9 @@ class KittyBatchCache:
         if any(self.lengths[b0:b0 + nb]):
             raise KittyError("prefill requires empty sequences")
         if keys.shape[2] > self.max_tokens:
-            raise KittyError(f"prefill of {keys.shape[2]} tokens exceeds the capacity {self.max_tokens}")
+            self.grow(keys.shape[2])
+        kp, vp = self._page_pair(keys.shape[2])
+        self._reserve(kp * nb * cfg.h_kv, vp * nb * cfg.h_kv)
         u0 = b0 * cfg.h_kv
         d = _lib.KittyCacheDesc()
         ctypes.memmove(ctypes.byref(d), ctypes.byref(self.desc), ctypes.sizeof(d))
@@ -239,6 +332,8 @@ class KittyBatchCache:
         kc, vc = keys.contiguous(), values.contiguous()
         _lib.check(self.lib.kitty_prefill(ctypes.byref(d), kc.data_ptr(), vc.data_ptr(), keys.shape[2], _stream()),
                    "prefill")
+        self.free_pages[0] -= kp * nb * cfg.h_kv
+        self.free_pages[1] -= vp * nb * cfg.h_kv
         for b in range(b0, b0 + nb):
             self._set_length(b, keys.shape[2])
 
@@ -251,10 +346,33 @@ class KittyBatchCache:
         self.key_pack_events[b] = past // cfg.g
         self.value_pack_events[b] = max(0, past - cfg.r) // cfg.g
 
-    def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.bfloat16) -> torch.Tensor:
-        """Step 2 for every sequence: q [B, h_q, D] bf16 -> [B, h_q, D]."""
+    # -- continuous batching: retire / admit rows of the batch -----------------
+
+    def retire(self, b: int, nb: int = 1):
+        """Free sequences [b, b + nb): their slots return to the pool, the rows
+        become empty (attend writes zeros for them) and can admit new ones."""
+        if b < 0 or nb < 0 or b + nb > self.num_seqs:
+            raise KittyError(f"sequences [{b}, {b + nb}) outside the batch of {self.num_seqs}")
+        _lib.check(self.lib.kitty_release_sequences(self._desc_ref, b, nb, _stream()), "retire")
+        for i in range(b, b + nb):
+            kp, vp = self._page_pair(self.lengths[i])
+            self.free_pages[0] += kp * self.cfg.h_kv
+            self.free_pages[1] += vp * self.cfg.h_kv
+            self.lengths[i] = 0
+            self.key_pack_events[i] = self.value_pack_events[i] = 0
+
+    def admit(self, b: int, keys: torch.Tensor, values: torch.Tensor):
+        """Prefill a new sequence into the empty row b: keys/values [h_kv, P, D]."""
         cfg = self.cfg
-        if min(self.lengths) == 0:
+        keys = self._rows(keys, (cfg.h_kv, keys.shape[1], cfg.d), "keys")[None]
+        values = self._rows(values, (cfg.h_kv, keys.shape[2], cfg.d), "values")[None]
+        self.prefill_range(b, 1, keys, values)
+
+    def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.bfloat16) -> torch.Tensor:
+        """Step 2 for every sequence: q [B, h_q, D] bf16 -> [B, h_q, D] (zeros
+        for empty rows of the batch)."""
+        cfg = self.cfg
+        if max(self.lengths) == 0:
             raise KittyError("attend on an empty cache")
         q = self._rows(q, (self.num_seqs, cfg.h_q, cfg.d), "q")
         if out is None:
@@ -366,6 +484,71 @@ class KittyBatchCache:
         vs = self.value_page_slots(b, h).cpu().numpy()
         return ([serialize_slot(s.tobytes(), "key", cfg.d, cfg.g, cfg.d_boost) for s in ks],
                 [serialize_slot(s.tobytes(), "value", cfg.d, cfg.g) for s in vs])
+
+    # -- offload / restore: KTYP pages + full-precision rows --------------------
+
+    def export_sequence(self, b: int) -> dict:
+        """The state of sequence b for offload: its length, and per KV head the
+        KTYP pages (pages.py:207-237; header + memcpy of each slot) and the
+        full-precision rows of the reference's segments (cache.py:65-80)."""
+        heads = []
+        for h in range(self.cfg.h_kv):
+            kb, vb = self.export_pages(b, h)
+            heads.append(dict(key_pages=kb, value_pages=vb, **self.head_rows(b, h)))
+        return dict(length=self.lengths[b], heads=heads)
+
+    def import_sequence(self, b: int, state: dict):
+        """Restore an exported sequence into the empty row b: every page is
+        decoded on the host (KTYP header rules, pages.py:246-292), copied to a
+        slot the device claims from the pool and checked there (boost_idx
+        bijection, pages.py:128-135); the rows go back to their sink / q-buffer
+        / ring positions.  A round trip is byte-identical."""
+        from .pages import slot_body
+
+        cfg = self.cfg
+        if self.lengths[b]:
+            raise KittyError("import requires an empty sequence row")
+        n = int(state["length"])
+        c = component_counts(cfg, n)
+        if len(state["heads"]) != cfg.h_kv:
+            raise KittyError(f"state has {len(state['heads'])} heads, the cache {cfg.h_kv}")
+        if n > self.max_tokens:
+            self.grow(n)
+        kp, vp = c["key_pages"], c["value_pages"]
+        self._reserve(kp * cfg.h_kv, vp * cfg.h_kv)
+        S, G, W = cfg.s, cfg.g, cfg.r + cfg.g
+        idx = lambda pos: torch.tensor(pos, dtype=torch.long, device=self.device)
+        rows = lambda a, k: torch.as_tensor(np.asarray(a, np.float32).reshape(-1, cfg.d)[:k]).to(self.device, self.row_dtype)
+        keep = []
+        for h, hs in enumerate(state["heads"]):
+            u = b * cfg.h_kv + h
+            if len(hs["key_pages"]) != kp or len(hs["value_pages"]) != vp:
+                raise KittyError(f"head {h}: {len(hs['key_pages'])} / {len(hs['value_pages'])} pages, "
+                                 f"length {n} needs {kp} / {vp}")
+            for kind, pages, k in (("key", hs["key_pages"], 0), ("value", hs["value_pages"], 1)):
+                if not pages:
+                    continue
+                body = b"".join(slot_body(raw, kind, cfg.d, cfg.g, cfg.d_boost) for raw in pages)
+                t = torch.frombuffer(bytearray(body), dtype=torch.uint8).to(self.device)
+                keep.append(t)
+                _lib.check(self.lib.kitty_import_pages(self._desc_ref, u, k, t.data_ptr(), 0, len(pages), _stream()),
+                           "import")
+            self.k_sink[u, : c["sink"]] = rows(hs["key_sink"], c["sink"])
+            self.v_sink[u, : c["sink"]] = rows(hs["value_sink"], c["sink"])
+            kq_pos = [(t - S) % G for t in range(S + kp * G, S + kp * G + c["key_qbuf"])]
+            vq_pos = [(t - S) % W for t in range(S + vp * G, S + vp * G + c["value_qbuf"])]
+            loc_pos = [(t - S) % W for t in range(n - c["local"], n)] if n > S else []
+            if kq_pos:
+                self.k_qbuf[u][idx(kq_pos)] = rows(hs["key_qbuffer"], len(kq_pos))
+            if vq_pos:
+                self.v_ring[u][idx(vq_pos)] = rows(hs["value_qbuffer"], len(vq_pos))
+            if loc_pos:
+                self.v_ring[u][idx(loc_pos)] = rows(hs["value_local"], len(loc_pos))
+        self.unit_len[b * cfg.h_kv:(b + 1) * cfg.h_kv] = n
+        self.free_pages[0] -= kp * cfg.h_kv
+        self.free_pages[1] -= vp * cfg.h_kv
+        self._set_length(b, n)
+        self._keep = keep  # staging buffers stay alive until the copies ran (stream order)
 
     def hbm_bytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in (

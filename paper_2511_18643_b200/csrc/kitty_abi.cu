@@ -41,6 +41,8 @@ int check_cache(const KittyCacheDesc* c) {
         c->value_slot_bytes != kitty_value_slot_bytes(c->cfg.d, c->cfg.g))
         return invalid("slot sizes do not match the page layout");
     if (c->row_dtype != KITTY_BF16 && c->row_dtype != KITTY_F32) return invalid("row_dtype must be KITTY_BF16 or KITTY_F32");
+    if ((c->key_free == nullptr) != (c->value_free == nullptr)) return invalid("a page pool needs both free stacks");
+    if (c->key_free && (!c->free_top || c->key_slots < 0 || c->value_slots < 0)) return invalid("bad page pool");
     return KITTY_OK;
 }
 
@@ -152,6 +154,25 @@ int kitty_prefill(const KittyCacheDesc* cache, const void* keys, const void* val
     if (rc != KITTY_OK) return rc;
     if (prompt_len < 0) return invalid("prompt length must be >= 0");
     return cuda_status(kitty::launch_prefill(*cache, keys, values, prompt_len, as_stream(stream)));
+}
+
+int kitty_release_sequences(const KittyCacheDesc* cache, int32_t first_seq, int32_t num_seqs, void* stream) {
+    int rc = check_cache(cache);
+    if (rc != KITTY_OK) return rc;
+    if (first_seq < 0 || num_seqs < 0 || first_seq + num_seqs > cache->num_seqs) return invalid("sequence range out of bounds");
+    return cuda_status(kitty::launch_release(*cache, first_seq, num_seqs, as_stream(stream)));
+}
+
+int kitty_import_pages(const KittyCacheDesc* cache, int32_t unit, int32_t kind, const uint8_t* bodies,
+                       int32_t first_page, int32_t num_pages, void* stream) {
+    int rc = check_cache(cache);
+    if (rc != KITTY_OK) return rc;
+    if (unit < 0 || unit >= cache->num_seqs * cache->cfg.h_kv) return invalid("unit out of range");
+    if (kind != 0 && kind != 1) return invalid("page kind must be 0 (key) or 1 (value)", KITTY_ERR_PAGE_FORMAT);
+    if (first_page < 0 || num_pages < 0) return invalid("bad page range");
+    if ((int64_t)first_page + num_pages > cache->max_pages) return invalid("pages beyond the block-table capacity");
+    if (num_pages > 0 && !bodies) return invalid("null page bodies");
+    return cuda_status(kitty::launch_import_pages(*cache, unit, kind, bodies, first_page, num_pages, as_stream(stream)));
 }
 
 int kitty_flatten(const KittyCacheDesc* cache, int32_t unit, int32_t n, float* keys_out,

@@ -202,7 +202,7 @@ __global__ void combine_kernel(const float* ws_acc, const float* ws_ml, int spli
             l += ws_ml[base * 2 + 1] * w;
             acc += ws_acc[base * d + ch] * w;
         }
-        const float o = acc / l;
+        const float o = l > 0.f ? acc / l : 0.f;  // an empty (retired) unit: zero rows
         int64_t row;
         if (dense) {
             row = u;

@@ -743,7 +743,17 @@ __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
     // max_tokens tokens only: make the caller's check() raise
     if (g == 0 && threadIdx.x == 0 && c.unit_len[u] > P.max_tokens) set_status(c.status, KITTY_STATUS_LENGTH);
     asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the fp grid (KITTY_PDL bit 2)
-    if (gm.n == 0) return;
+    if (gm.n == 0) {  // an empty (retired) sequence of the batch: zero output rows
+        const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
+        const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
+        for (int i = threadIdx.x; i < D; i += blockDim.x) {
+            if (P.out_dtype == KITTY_F32)
+                static_cast<float*>(P.out)[row * D + i] = 0.f;
+            else
+                static_cast<uint16_t*>(P.out)[row * D + i] = 0;
+        }
+        return;
+    }
     const int nfc = (gm.nfp + kFpChunk - 1) / kFpChunk;
     int nch[3];
     for (int lv = 0; lv < 3; ++lv) {

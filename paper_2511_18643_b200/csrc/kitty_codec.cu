@@ -318,15 +318,11 @@ __global__ void select_boost_kernel(const double* scores, int d, int k, int64_t*
 
 // dequantize_key_page (pages.py:121-143): validate the sentinel pattern, then
 // X = low | high[boost_idx] << 2, out = X * scale + zero (mul then add).
-__global__ void dequant_key_pages_kernel(const uint8_t* slots, int64_t stride, int g, int d,
-                                         int d_boost, const float* sc32, const float* ze32,
-                                         float* out, uint32_t* status) {
+// pages.py:128-135 for one key page (block-uniform): d_boost non-sentinel
+// entries in boost_idx, forming a bijection onto the high-bit rows 0..d_boost-1.
+__device__ bool block_boost_index_ok(const uint8_t* idx, int d, int d_boost) {
     __shared__ int seen[256];
     __shared__ int total;
-    const int p = blockIdx.x;
-    const KeyLayout L{d, g, d_boost};
-    const uint8_t* slot = slots + p * stride;
-    const uint8_t* idx = slot + L.idx_off();
     for (int j = threadIdx.x; j < 256; j += blockDim.x) seen[j] = 0;
     if (threadIdx.x == 0) total = 0;
     __syncthreads();
@@ -340,7 +336,17 @@ __global__ void dequant_key_pages_kernel(const uint8_t* slots, int64_t stride, i
     __syncthreads();
     int bad = total != d_boost;
     for (int j = threadIdx.x; j < 256; j += blockDim.x) bad |= (j < d_boost) ? (seen[j] != 1) : (seen[j] != 0);
-    if (__syncthreads_or(bad)) {
+    return !__syncthreads_or(bad);
+}
+
+__global__ void dequant_key_pages_kernel(const uint8_t* slots, int64_t stride, int g, int d,
+                                         int d_boost, const float* sc32, const float* ze32,
+                                         float* out, uint32_t* status) {
+    const int p = blockIdx.x;
+    const KeyLayout L{d, g, d_boost};
+    const uint8_t* slot = slots + p * stride;
+    const uint8_t* idx = slot + L.idx_off();
+    if (!block_boost_index_ok(idx, d, d_boost)) {
         if (threadIdx.x == 0) set_status(status, KITTY_STATUS_PAGE_FORMAT);
         return;
     }
@@ -405,6 +411,37 @@ __device__ __forceinline__ void copy_row(T* dst, const T* src, int d) {
     }
 }
 
+// The slot of page p of unit u on one side (key / value) for a kernel about
+// to write it.  With a page pool (KittyCacheDesc.key_free) thread 0 pops a
+// free slot and records it in the unit's block table; without one the
+// caller's block table names it.  Block-uniform: every thread calls it and
+// gets the slot (-1 = the pool is empty: KITTY_STATUS_OVERFLOW is set).
+__device__ int32_t block_claim_slot(const KittyCacheDesc& c, bool key, int u, int p) {
+    __shared__ int32_t s_slot;
+    __syncthreads();  // a previous call's s_slot has been read by every thread
+    if (threadIdx.x == 0) {
+        int32_t* e = (key ? c.key_block_table : c.value_block_table) + (int64_t)u * c.max_pages + p;
+        int32_t* stack = key ? c.key_free : c.value_free;
+        int32_t s = -1;
+        if (!stack) {
+            s = *e;
+        } else {
+            int32_t* top = c.free_top + (key ? 0 : 1);
+            const int i = atomicSub(top, 1) - 1;
+            if (i < 0) {
+                atomicAdd(top, 1);
+                set_status(c.status, KITTY_STATUS_OVERFLOW);
+            } else {
+                s = stack[i];
+                *e = s;
+            }
+        }
+        s_slot = s;
+    }
+    __syncthreads();
+    return s_slot;
+}
+
 // Pack key page `p` of unit `u` from `rows` (g consecutive rows of a ring of
 // size `wrap` starting at `start`) into its block-table slot (+ its f32
 // metadata into the side table when the cache keeps one).
@@ -424,7 +461,8 @@ __device__ void pack_key_into_cache(const KittyCacheDesc& c, int u, int p, const
     if (!stage_rows(tile, base, start, wrap, k.g, k.d)) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_NONFINITE);
     }
-    const int32_t s = c.key_block_table[(int64_t)u * c.max_pages + p];
+    const int32_t s = block_claim_slot(c, true, u, p);
+    if (s < 0) return;
     float* meta = c.key_meta ? c.key_meta + (int64_t)s * 2 * k.d : nullptr;
     pack_key_tile(tile, k.g, k.d, k.d_boost, nullptr, slot, sc, meta, meta ? meta + k.d : nullptr);
     copy_slot_out(slot, c.key_pool + (int64_t)s * c.key_slot_bytes, KeyLayout{k.d, k.g, k.d_boost}.bytes());
@@ -443,7 +481,8 @@ __device__ void pack_value_into_cache(const KittyCacheDesc& c, int u, int p, con
     if (!stage_rows(tile, base, start, wrap, k.g, k.d)) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_NONFINITE);
     }
-    const int32_t s = c.value_block_table[(int64_t)u * c.max_pages + p];
+    const int32_t s = block_claim_slot(c, false, u, p);
+    if (s < 0) return;
     float* meta = c.value_meta ? c.value_meta + (int64_t)s * 2 * k.g : nullptr;
     pack_value_tile(tile, k.g, k.d, slot, meta, meta ? meta + k.g : nullptr);
     copy_slot_out(slot, c.value_pool + (int64_t)s * c.value_slot_bytes, ValueLayout{k.d, k.g}.bytes());
@@ -490,22 +529,21 @@ __global__ void append_kernel(KittyCacheDesc c, const T* k_new, const T* v_new) 
             fastpack::Smem& s = *reinterpret_cast<fastpack::Smem*>(smem);
             if (kpack) {
                 const int p = past / G - 1;
+                const int32_t sl = p < c.max_pages ? block_claim_slot(c, true, u, p) : -1;
                 if (p >= c.max_pages) {
                     if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
-                } else {
-                    fastpack::key_page(s, kq, 0, G, k.d_boost,
-                                       c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes,
-                                       c.status);
+                } else if (sl >= 0) {
+                    fastpack::key_page(s, kq, 0, G, k.d_boost, c.key_pool + (int64_t)sl * c.key_slot_bytes, c.status);
                 }
                 __syncthreads();
             }
             if (vpack) {
                 const int p = vtot / G - 1;
+                const int32_t sl = p < c.max_pages ? block_claim_slot(c, false, u, p) : -1;
                 if (p >= c.max_pages) {
                     if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
-                } else {
-                    fastpack::value_page(s, vring, (p * G) % W, W,
-                                         c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes,
+                } else if (sl >= 0) {
+                    fastpack::value_page(s, vring, (p * G) % W, W, c.value_pool + (int64_t)sl * c.value_slot_bytes,
                                          c.status);
                 }
             }
@@ -586,11 +624,13 @@ __global__ void __launch_bounds__(fastpack::kThreads) prefill_pack_fast_kernel(K
         return;
     }
     const int64_t row0 = (int64_t)u * P + k.s + (int64_t)p * fastpack::kG;
+    const int32_t sl = block_claim_slot(c, is_key, u, p);
+    if (sl < 0) return;
     if (is_key) {
-        uint8_t* slot = c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + p] * c.key_slot_bytes;
+        uint8_t* slot = c.key_pool + (int64_t)sl * c.key_slot_bytes;
         fastpack::key_page(s, keys + row0 * fastpack::kD, 0, fastpack::kG, k.d_boost, slot, c.status);
     } else {
-        uint8_t* slot = c.value_pool + (int64_t)c.value_block_table[(int64_t)u * c.max_pages + p] * c.value_slot_bytes;
+        uint8_t* slot = c.value_pool + (int64_t)sl * c.value_slot_bytes;
         fastpack::value_page(s, values + row0 * fastpack::kD, 0, fastpack::kG, slot, c.status);
     }
 }
@@ -698,6 +738,69 @@ cudaError_t launch_fake_quantize(const float* x, int rows, int cols, int per_tok
     if (lanes == 0 || rows == 0 || cols == 0) return cudaSuccess;
     fake_quantize_kernel<<<(lanes + 127) / 128, 128, 0, st>>>(x, rows, cols, per_token, bits, out);
     return cudaGetLastError();
+}
+
+// Retire sequence seq0 + blockIdx.x / h_kv's unit: its slots go back to the
+// pool's free stacks (pushes only: no pop runs in this launch), its block-table
+// entries become -1, its length 0.
+__global__ void release_kernel(KittyCacheDesc c, int seq0) {
+    const int u = seq0 * c.cfg.h_kv + blockIdx.x;
+    const int n = c.unit_len[u];
+    const int S = c.cfg.s, G = c.cfg.g;
+    const int past = n > S ? n - S : 0;
+    const int kp = min(past / G, c.max_pages);
+    const int vp = min((past - min(c.cfg.r, past)) / G, c.max_pages);
+    int32_t* kbt = c.key_block_table + (int64_t)u * c.max_pages;
+    int32_t* vbt = c.value_block_table + (int64_t)u * c.max_pages;
+    if (c.key_free) {
+        for (int p = threadIdx.x; p < kp; p += blockDim.x) {
+            const int32_t sl = kbt[p];
+            if (sl >= 0) c.key_free[atomicAdd(&c.free_top[0], 1)] = sl;
+            kbt[p] = -1;
+        }
+    }
+    if (c.value_free) {
+        for (int p = threadIdx.x; p < vp; p += blockDim.x) {
+            const int32_t sl = vbt[p];
+            if (sl >= 0) c.value_free[atomicAdd(&c.free_top[1], 1)] = sl;
+            vbt[p] = -1;
+        }
+    }
+    __syncthreads();  // every thread has read unit_len
+    if (threadIdx.x == 0) c.unit_len[u] = 0;
+}
+
+// Import page first_page + blockIdx.x of unit u: claim its slot, copy the KTYP
+// body in (16-byte vectors: slot sizes are multiples of 16), check a key
+// page's boost index (pages.py:128-135) and fill the f32 metadata side table.
+__global__ void import_pages_kernel(KittyCacheDesc c, int u, int kind, const uint8_t* bodies, int first_page) {
+    const bool key = kind == 0;
+    const int p = first_page + blockIdx.x;
+    const int64_t bytes = key ? c.key_slot_bytes : c.value_slot_bytes;
+    const uint8_t* src = bodies + (int64_t)blockIdx.x * bytes;
+    if (p >= c.max_pages) {
+        if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+        return;
+    }
+    const int32_t sl = block_claim_slot(c, key, u, p);
+    if (sl < 0) return;
+    uint8_t* dst = (key ? c.key_pool : c.value_pool) + (int64_t)sl * bytes;
+    for (int64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    const int d = c.cfg.d, g = c.cfg.g;
+    if (key) {
+        const KeyLayout L{d, g, c.cfg.d_boost};
+        if (!block_boost_index_ok(src + L.idx_off(), d, c.cfg.d_boost) && threadIdx.x == 0)
+            set_status(c.status, KITTY_STATUS_PAGE_FORMAT);
+        if (c.key_meta) {
+            float* m = c.key_meta + (int64_t)sl * 2 * d;
+            for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) m[i] = half_bits_to_f32(ld_u16(src + L.scale_off() + 2 * i));
+        }
+    } else if (c.value_meta) {
+        const ValueLayout L{d, g};
+        float* m = c.value_meta + (int64_t)sl * 2 * g;
+        for (int i = threadIdx.x; i < 2 * g; i += blockDim.x) m[i] = half_bits_to_f32(ld_u16(src + L.scale_off() + 2 * i));
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -829,6 +932,19 @@ cudaError_t launch_prefill(const KittyCacheDesc& c, const void* keys, const void
     if (c.row_dtype == KITTY_F32)
         return prefill_t(c, static_cast<const float*>(keys), static_cast<const float*>(values), P, st);
     return prefill_t(c, static_cast<const uint16_t*>(keys), static_cast<const uint16_t*>(values), P, st);
+}
+
+cudaError_t launch_release(const KittyCacheDesc& c, int seq0, int nseq, cudaStream_t st) {
+    if (nseq <= 0 || c.cfg.h_kv == 0) return cudaSuccess;
+    release_kernel<<<nseq * c.cfg.h_kv, 128, 0, st>>>(c, seq0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_import_pages(const KittyCacheDesc& c, int u, int kind, const uint8_t* bodies, int first_page,
+                                int n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    import_pages_kernel<<<n, 128, 0, st>>>(c, u, kind, bodies, first_page);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_flatten(const KittyCacheDesc& c, int u, int n, float* ko, float* vo,

@@ -36,6 +36,9 @@ cudaError_t launch_fake_quantize(const float* x, int rows, int cols, int per_tok
                                  cudaStream_t st);
 cudaError_t launch_append(const KittyCacheDesc& c, const void* k_new, const void* v_new, cudaStream_t st);
 cudaError_t launch_prefill(const KittyCacheDesc& c, const void* keys, const void* values, int P, cudaStream_t st);
+cudaError_t launch_release(const KittyCacheDesc& c, int seq0, int nseq, cudaStream_t st);
+cudaError_t launch_import_pages(const KittyCacheDesc& c, int u, int kind, const uint8_t* bodies, int first_page,
+                                int n, cudaStream_t st);
 cudaError_t launch_flatten(const KittyCacheDesc& c, int u, int n, float* ko, float* vo,
                            cudaStream_t st);
 

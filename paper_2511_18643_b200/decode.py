@@ -74,14 +74,16 @@ class DecodeStep:
 
     def _advance(self):
         for cache in self.layers:
-            for b in range(self.num_seqs):
-                cache.lengths[b] += 1
-                cache._count_events(b, cache.lengths[b])
+            cache.advance_host()
 
     def step(self):
         """One eager decode step over all layers."""
         if max(self.layers[0].lengths) + 1 > self.max_tokens:
             raise ValueError("decode step past the allocated context")
+        for cache in self.layers:  # the pools are sized for max_tokens: never short, but checked
+            need = cache.append_page_need()
+            if need[0] > cache.free_pages[0] or need[1] > cache.free_pages[1]:
+                raise ValueError("decode step would exhaust a layer's page pool")
         if self.graph is not None:
             self.graph.replay()
         else:

@@ -431,6 +431,31 @@ def serialize_slot(body: bytes | np.ndarray, kind: str, d: int, g: int, d_boost:
     return _PAGE_HEADER.pack(PAGE_MAGIC, k, d, g, d_boost if k == KIND_KEY else 0) + bytes(body)
 
 
+def slot_body(raw: bytes, kind: str, d: int, g: int, d_boost: int = 0) -> bytes:
+    """The body of a KTYP page (pages.py:246-292 header rules) for a device slot
+    of a cache with this d / g / d_boost: BadMagicError / TruncatedFileError for
+    a damaged header or body, PageFormatError for trailing bytes, another kind
+    or a page shape the cache does not hold."""
+    if len(raw) < len(PAGE_MAGIC) or raw[:4] != PAGE_MAGIC:
+        raise BadMagicError(f"bad page magic {raw[:4]!r}")
+    if len(raw) < _PAGE_HEADER.size:
+        raise TruncatedFileError("page truncated in header")
+    _, k, pd, pg, pb = _PAGE_HEADER.unpack_from(raw)
+    want = KIND_KEY if kind == "key" else KIND_VALUE
+    if k != want:
+        raise PageFormatError(f"expected a {kind} page, got kind {k}")
+    if (pd, pg) != (d, g) or (want == KIND_KEY and pb != d_boost):
+        raise PageFormatError(f"page shape (d={pd}, g={pg}, d_boost={pb}) does not match the cache "
+                              f"(d={d}, g={g}, d_boost={d_boost if want == KIND_KEY else 0})")
+    need = key_slot_bytes(d, g, d_boost) if want == KIND_KEY else value_slot_bytes(d, g)
+    body = raw[_PAGE_HEADER.size:]
+    if len(body) < need:
+        raise TruncatedFileError(f"{kind} page truncated")
+    if len(body) > need:
+        raise PageFormatError(f"{len(body) - need} trailing bytes after {kind} page")
+    return body
+
+
 def deserialize_page(raw: bytes):
     """pages.py:246-292."""
     if len(raw) < len(PAGE_MAGIC) or raw[:4] != PAGE_MAGIC:
