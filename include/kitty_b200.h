@@ -243,6 +243,29 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv,
                           const int32_t* kv_head_map, float* out, void* workspace,
                           size_t workspace_bytes, void* stream);
 
+/* ---- analysis (analysis.py) -------------------------------------------- */
+
+/* channel_sensitivity (analysis.py:63-104): mse[h_q][d] float64 = the mean
+ * squared difference of the (lq x length) attention-probability matrix of
+ * query head qh when key channel ch alone is fake-quantized per channel at
+ * `bits` (rank-1 logit update), fp64 throughout.  queries [h_q][lq][d] and
+ * keys [h_kv][length][d] float32; query head qh reads KV head qh / (h_q/h_kv).
+ * bits 16 is the identity (all zeros; the caller may skip the launch). */
+size_t kitty_sensitivity_workspace_bytes(int32_t h_q, int32_t lq, int32_t h_kv, int32_t length, int32_t d);
+int kitty_channel_sensitivity(const float* queries, int32_t h_q, int32_t lq, const float* keys, int32_t h_kv,
+                              int32_t length, int32_t d, int32_t bits, double* mse, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/* attention_mse (analysis.py:119-142): keys [length][d] float32 fake-quantized
+ * per channel at bits[d] (device int32: 4 for the boosted selection, 2
+ * elsewhere); out[0] float64 = mean over the `heads` query heads
+ * (queries [heads][lq][d]) of the probability-matrix MSE against the
+ * full-precision keys. */
+size_t kitty_attention_mse_workspace_bytes(int32_t heads, int32_t lq, int32_t length, int32_t d);
+int kitty_attention_mse(const float* keys, int32_t length, int32_t d, const float* queries, int32_t heads,
+                        int32_t lq, const int32_t* bits, double* out, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

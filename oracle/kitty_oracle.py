@@ -516,3 +516,60 @@ def algorithmic_bytes_per_unit(s, r, g, d, d_boost, group, n) -> int:
     val = c["value_pages"] * value_slot_bytes(d, g)
     fp = 2 * d * ((c["sink"] + c["key_qbuf"]) + (c["sink"] + c["local"] + c["value_qbuf"]))
     return key + val + fp + 2 * 2 * group * d
+
+
+# -- analysis.py: channel sensitivity and boost sweeps ---------------------------
+
+
+def _softmax_rows64(logits: np.ndarray) -> np.ndarray:
+    """analysis.py:32-35."""
+    shifted = logits - logits.max(axis=-1, keepdims=True)
+    e = np.exp(shifted)
+    return e / e.sum(axis=-1, keepdims=True)
+
+
+def channel_sensitivity(queries, keys, bits: int = 2) -> np.ndarray:
+    """analysis.py:63-104 (the mse matrix only): per query head and key
+    channel, the MSE between baseline and rank-1-perturbed fp64 attention
+    probabilities when that channel alone is fake-quantized at ``bits``."""
+    queries = np.asarray(queries, np.float32)
+    keys = np.asarray(keys, np.float32)
+    queries = queries[None] if queries.ndim == 2 else queries
+    keys = keys[None] if keys.ndim == 2 else keys
+    h_q, _, d = queries.shape
+    h_kv = keys.shape[0]
+    mse = np.zeros((h_q, d), np.float64)
+    if bits == 16:
+        return mse
+    inv = 1.0 / np.sqrt(d)
+    group = h_q // h_kv
+    for kv in range(h_kv):
+        k64 = keys[kv].astype(np.float64)
+        delta = fake_quantize_matrix(keys[kv], "per_channel", np.full(d, bits)).astype(np.float64) - k64
+        for j in range(group):
+            qh = kv * group + j
+            q64 = queries[qh].astype(np.float64)
+            base = (q64 @ k64.T) * inv
+            base_p = _softmax_rows64(base)
+            for ch in range(d):
+                p = _softmax_rows64(base + np.outer(q64[:, ch], delta[:, ch]) * inv)
+                mse[qh, ch] = np.mean((p - base_p) ** 2)
+    return mse
+
+
+def attention_mse(keys, queries, selection) -> float:
+    """analysis.py:119-142."""
+    keys = np.asarray(keys, np.float32)
+    queries = np.asarray(queries, np.float32)
+    queries = queries[None] if queries.ndim == 2 else queries
+    d = keys.shape[1]
+    widths = np.full(d, 2)
+    widths[np.asarray(selection, dtype=np.int64)] = 4
+    quantized = fake_quantize_matrix(keys, "per_channel", widths).astype(np.float64)
+    k64 = keys.astype(np.float64)
+    inv = 1.0 / np.sqrt(d)
+    total = 0.0
+    for q in queries:
+        q64 = q.astype(np.float64)
+        total += np.mean((_softmax_rows64((q64 @ quantized.T) * inv) - _softmax_rows64((q64 @ k64.T) * inv)) ** 2)
+    return total / len(queries)

@@ -10,6 +10,16 @@ include/kitty_b200.h); there is no CPU fallback.
 from ._lib import exported_symbols, load_library
 from .analysis import MemoryReport, algorithmic_bytes_per_unit, measure_cache_bytes, memory_report
 from .cache import AttentionOutput, KittyBatchCache, KittyCacheState, component_counts, oracle_attend
+from .sensitivity import (
+    SensitivityReport,
+    SweepRow,
+    SyntheticSpec,
+    attention_mse,
+    boost_sweep,
+    boost_sweep_experiment,
+    channel_sensitivity,
+    generate_synthetic,
+)
 from .config import PASSTHROUGH_BITS, KittyConfig, boost_count, config_from_mapping
 from .errors import (
     BadMagicError,
@@ -61,4 +71,6 @@ __all__ = [
     "exported_symbols", "load_library", "measure_cache_bytes", "memory_report", "oracle_attend",
     "pack_key_page", "pack_key_pages", "pack_value_page", "pack_value_pages", "page_byte_size",
     "select_boost", "select_boost_batch", "serialize_page", "serialize_slot",
+    "SensitivityReport", "SweepRow", "SyntheticSpec", "attention_mse", "boost_sweep", "boost_sweep_experiment",
+    "channel_sensitivity", "generate_synthetic",
 ]

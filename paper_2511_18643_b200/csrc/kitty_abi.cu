@@ -215,4 +215,35 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv, 
                                                      as_stream(stream)));
 }
 
+size_t kitty_sensitivity_workspace_bytes(int32_t h_q, int32_t lq, int32_t h_kv, int32_t length, int32_t d) {
+    if (h_q < 0 || lq < 0 || h_kv < 1 || length < 0 || d < 0) return 0;
+    return kitty::sensitivity_workspace_bytes(h_q, lq, h_kv, length, d);
+}
+
+int kitty_channel_sensitivity(const float* queries, int32_t h_q, int32_t lq, const float* keys, int32_t h_kv,
+                              int32_t length, int32_t d, int32_t bits, double* mse, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+    if (h_q < 1 || h_kv < 1 || lq < 1 || length < 1 || d < 1) return invalid("sensitivity needs non-empty queries and keys");
+    if (h_q % h_kv != 0) return invalid("query head count must be a multiple of KV head count");
+    if (bits != 2 && bits != 4 && bits != 16) return invalid("bits must be 2, 4 or 16");
+    if (workspace_bytes < kitty::sensitivity_workspace_bytes(h_q, lq, h_kv, length, d)) return invalid("workspace too small");
+    if (bits == 16) return cuda_status(cudaMemsetAsync(mse, 0, sizeof(double) * h_q * d, as_stream(stream)));
+    return cuda_status(kitty::launch_channel_sensitivity(queries, h_q, lq, keys, h_kv, length, d, bits, mse,
+                                                         workspace, as_stream(stream)));
+}
+
+size_t kitty_attention_mse_workspace_bytes(int32_t heads, int32_t lq, int32_t length, int32_t d) {
+    if (heads < 0 || lq < 0 || length < 0 || d < 0) return 0;
+    return kitty::attention_mse_workspace_bytes(heads, lq, length, d);
+}
+
+int kitty_attention_mse(const float* keys, int32_t length, int32_t d, const float* queries, int32_t heads,
+                        int32_t lq, const int32_t* bits, double* out, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+    if (heads < 1 || lq < 1 || length < 1 || d < 1) return invalid("attention_mse needs non-empty queries and keys");
+    if (workspace_bytes < kitty::attention_mse_workspace_bytes(heads, lq, length, d)) return invalid("workspace too small");
+    return cuda_status(kitty::launch_attention_mse(keys, length, d, queries, heads, lq, bits, out, workspace,
+                                                   as_stream(stream)));
+}
+
 }  // extern "C"

@@ -42,6 +42,14 @@ cudaError_t launch_import_pages(const KittyCacheDesc& c, int u, int kind, const 
 cudaError_t launch_flatten(const KittyCacheDesc& c, int u, int n, float* ko, float* vo,
                            cudaStream_t st);
 
+// analysis (kitty_analysis.cu)
+size_t sensitivity_workspace_bytes(int h_q, int lq, int h_kv, int L, int d);
+cudaError_t launch_channel_sensitivity(const float* q, int h_q, int lq, const float* keys, int h_kv, int L, int d,
+                                       int bits, double* mse, void* ws, cudaStream_t st);
+size_t attention_mse_workspace_bytes(int heads, int lq, int L, int d);
+cudaError_t launch_attention_mse(const float* keys, int L, int d, const float* q, int heads, int lq,
+                                 const int32_t* bits, double* out, void* ws, cudaStream_t st);
+
 // attention (kitty_attention.cu)
 size_t attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens);
 cudaError_t launch_decode_attention(const KittyCacheDesc& c, const void* q, void* out,
