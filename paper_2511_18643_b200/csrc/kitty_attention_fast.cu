@@ -52,6 +52,7 @@ constexpr int kValueSlot = 4608;
 constexpr int kPtWords = 68;
 constexpr int kFpChunk = 32;       // fp tokens per fp-kernel chunk
 constexpr float kAlpha = 0.12751743074f;  // log2(e) / sqrt(128)
+constexpr float kLazy = 8.f;  // log2-domain slack of the running max (P <= 256)
 constexpr uint32_t kMagic = 0x64006400u;  // f16x2 (1024, 1024)
 constexpr uint32_t kOnes = 0x3C003C00u;   // f16x2 (1, 1)
 
@@ -67,7 +68,8 @@ struct __align__(16) WarpFixedT {
     uint32_t qtab[PT_ROWS][D / 2];      // 4 q alpha (f16) of the QK side's unit: the boosted rows' B
     uint32_t ones[64];                  // f16x2 (1, 1): the aux lanes' "scale"
     uint8_t inv[32];                    // boosted channel of high_bits row j
-    unsigned long long full[2];         // the stage's key and value pages landed
+    unsigned long long kfull[2];        // key slot s landed
+    unsigned long long vfull[2];        // value slot s landed
 };
 template <int GROUP>
 __host__ __device__ constexpr int warp_fixed_bytes() {
@@ -134,11 +136,12 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar,
+                                         uint64_t pol) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first())
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 
@@ -320,8 +323,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
     const int hkv = c.cfg.h_kv;
 
     if (lane == 0) {
-        mbar_init(&sm.full[0], 1);
-        mbar_init(&sm.full[1], 1);
+        mbar_init(&sm.kfull[0], 1);
+        mbar_init(&sm.kfull[1], 1);
+        mbar_init(&sm.vfull[0], 1);
+        mbar_init(&sm.vfull[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     sm.ones[lane] = kOnes;
@@ -402,11 +407,30 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
         d.vs = __shfl_sync(0xffffffffu, vreg, (ip - ip0) & 31);
         return d;
     };
-    auto issue = [&](const Pg& d, int st) {
+    // Page p of the warp's stream lands in key slot p & 1 and value slot p & 1
+    // (use number p >> 1 of the slot: mbarrier phase (p >> 1) & 1).  QK runs
+    // one page ahead of PV, so a key page is issued one page earlier than its
+    // value page: each gets a full iteration of load time.
+    const uint64_t pol = l2_evict_first();
+    auto issue_key = [&](const Pg& d, int sl) {
         if (lane == 0 && d.u >= 0) {
-            mbar_expect_tx(&sm.full[st], kslot + vslot);
-            bulk_g2s(kslots + st * kslot, c.key_pool + (int64_t)d.ks * kslot, kslot, &sm.full[st]);
-            bulk_g2s(vslots + st * vslot, c.value_pool + (int64_t)d.vs * vslot, vslot, &sm.full[st]);
+            mbar_expect_tx(&sm.kfull[sl], kslot);
+            bulk_g2s(kslots + sl * kslot, c.key_pool + (int64_t)d.ks * kslot, kslot, &sm.kfull[sl], pol);
+        }
+    };
+    auto issue_val = [&](const Pg& d, int sl) {
+        if (lane == 0 && d.u >= 0) {
+            mbar_expect_tx(&sm.vfull[sl], vslot);
+            bulk_g2s(vslots + sl * vslot, c.value_pool + (int64_t)d.vs * vslot, vslot, &sm.vfull[sl], pol);
+        }
+    };
+    // a new unit's q rows (group x 256 B, L2-resident) are pulled into L1 two
+    // pages before its first QK reads them
+    auto prefetch_q = [&](const Pg& d, int prev_u) {
+        if (d.u >= 0 && d.u != prev_u && lane < GROUP * 2) {
+            const int b = d.u / hkv, h = d.u - b * hkv;
+            const uint16_t* qg = P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP) * D + lane * 64;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(qg));
         }
     };
 
@@ -417,7 +441,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
     float om[2] = {-INFINITY, -INFINITY};
     const int qcol = kFull ? gid : (gid & 3);
     // ---- PV side state: output accumulators, row sums, zero / offset constants ----
-    float oacc[8][4];
+    float oacc[8][4] = {};
     float ol[2] = {0.f, 0.f};
     float ob[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
     const int prow = kFull ? gid : (gid & 3);
@@ -446,7 +470,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
             }
         }
         if (d.p == (d.pq >> 16)) om[0] = om[1] = -INFINITY;  // an item's first page
-        mbar_wait(&sm.full[st], phase);
+        mbar_wait(&sm.kfull[st], phase);
         if (NKH > 0) {  // boosted rows -> channels (inverse of boost_idx)
             const uint8_t* kp = kslots + st * kslot;
             const uint32_t bw = lds32(kp + D * G / 4 + d_boost * G / 4 + 4 * lane);
@@ -540,8 +564,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 4));
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 8));
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 16));
-            mnew[j] = fmaxf(om[j], pm);
-            corr[j] = ex2(om[j] - mnew[j]);  // 0 on an item's first page (om = -inf)
+            // lazy rescaling: the reference max moves only when a page's max
+            // exceeds it by more than kLazy (log2 domain), so P stays <= 2^kLazy
+            // (f16-safe) and the output rescale below almost never runs
+            mnew[j] = pm > om[j] + kLazy ? pm : om[j];
+            corr[j] = ex2(om[j] - mnew[j]);  // 0 on an item's first page (om = -inf), else 1 unless moved
             om[j] = mnew[j];
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) bw[c4][j] -= mnew[j];
@@ -568,18 +595,19 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
     struct PvRegs {
         float vaux[4], vaux2[4];
     };
-    auto pv_head = [&](bool fresh, const float (&corr)[2]) {
-        if (fresh) {
-#pragma unroll
-            for (int m = 0; m < 8; ++m) oacc[m][0] = oacc[m][1] = oacc[m][2] = oacc[m][3] = 0.f;
-        } else if (__any_sync(0xffffffffu, (real0 && corr[0] != 1.f) || (real1 && corr[1] != 1.f))) {
-            // rescale the running output when a real column's max moved (warp vote)
+    auto pv_head = [&](bool fresh, const float (&corr)[2], int st, uint32_t phase) {
+        mbar_wait(&sm.vfull[st], phase);
+        // an item's first page zeroes the running output (factor 0); later
+        // pages rescale it only when a real column's max moved (warp vote;
+        // rare under lazy rescaling).  One in-place multiply path: no copies.
+        const float c0 = fresh ? 0.f : corr[0], c1 = fresh ? 0.f : corr[1];
+        if (__any_sync(0xffffffffu, fresh || (real0 && c0 != 1.f) || (real1 && c1 != 1.f))) {
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                oacc[m][0] *= corr[0];
-                oacc[m][2] *= corr[0];
-                oacc[m][1] *= corr[1];
-                oacc[m][3] *= corr[1];
+                oacc[m][0] *= c0;
+                oacc[m][2] *= c0;
+                oacc[m][1] *= c1;
+                oacc[m][3] *= c1;
             }
         }
     };
@@ -651,8 +679,13 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
     Pg d0 = next_page();
     if (d0.u >= 0) {
         Pg d1 = next_page();
-        issue(d0, 0);
-        issue(d1, 1);
+        Pg d2 = next_page();
+        issue_key(d0, 0);
+        issue_val(d0, 0);
+        issue_key(d1, 1);
+        issue_val(d1, 1);
+        prefetch_q(d1, d0.u);
+        prefetch_q(d2, d1.u);
         float corr0[2], mnew0[2];
         {
             qk_prologue(d0, 0, 0);
@@ -662,42 +695,51 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
             qk_tail(0, qr, corr0, mnew0);
         }
         __syncwarp();
+        issue_key(d2, 0);  // key slot 0 is free once QK(0) is done
+        // steady state: one path (QK of page k + 1 beside PV of page k), so the
+        // output accumulators keep their registers across the back edge
+        uint32_t k = 0;
 #pragma unroll 1
-        for (uint32_t k = 0;; ++k) {
+        for (; d1.u >= 0; ++k) {
             const int st = k & 1;
             const bool fresh0 = d0.p == (d0.pq >> 16), last0 = d0.p + 1 == (d0.pq & 0xffff);
-            Pg d2 = next_page();  // page k + 2: loaded into stage st once page k is done
+            Pg d3 = next_page();  // page k + 3: its key goes into key slot st ^ 1 after QK(k + 1)
+            prefetch_q(d3, d2.u);
             float corr1[2], mnew1[2];
             PvRegs pr;
-            if (d1.u >= 0) {
-                qk_prologue(d1, st ^ 1, ((k + 1) >> 1) & 1);
-                pv_head(fresh0, corr0);
-                QkRegs qr;
-                // the two pages' k-steps alternate: independent chains for the scheduler
+            qk_prologue(d1, st ^ 1, ((k + 1) >> 1) & 1);
+            pv_head(fresh0, corr0, st, (k >> 1) & 1);
+            QkRegs qr;
+            // the two pages' k-steps alternate: independent chains for the scheduler
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    pv_step(st, ks, pr);
-                    qk_step(st ^ 1, ks, qr);
-                }
-                pv_tail(fresh0, corr0, pr);
-                qk_tail(st ^ 1, qr, corr1, mnew1);
-            } else {
-                pv_head(fresh0, corr0);
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks) pv_step(st, ks, pr);
-                pv_tail(fresh0, corr0, pr);
+            for (int ks = 0; ks < 8; ++ks) {
+                pv_step(st, ks, pr);
+                qk_step(st ^ 1, ks, qr);
             }
+            pv_tail(fresh0, corr0, pr);
+            qk_tail(st ^ 1, qr, corr1, mnew1);
             if (last0) flush(d0, mnew0);
             __syncwarp();
-            issue(d2, st);
-            if (d1.u < 0) break;
+            issue_val(d2, st);     // value slot st (page k) -> page k + 2
+            issue_key(d3, st ^ 1);  // key slot st ^ 1 (page k + 1) -> page k + 3
             d0 = d1;
             d1 = d2;
+            d2 = d3;
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 corr0[j] = corr1[j];
                 mnew0[j] = mnew1[j];
             }
+        }
+        {  // the stream's last page: P V only
+            const int st = k & 1;
+            const bool fresh0 = d0.p == (d0.pq >> 16);
+            PvRegs pr;
+            pv_head(fresh0, corr0, st, (k >> 1) & 1);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) pv_step(st, ks, pr);
+            pv_tail(fresh0, corr0, pr);
+            flush(d0, mnew0);  // a stream's last page is its item's last
         }
     }
     // the last warp out resets the work queue for the next launch (after its
