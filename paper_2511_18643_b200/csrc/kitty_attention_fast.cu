@@ -49,7 +49,7 @@ constexpr int kValueSlot = 4608;
 // P^T row = one query: the f16x2 of tokens (2 k, 2 k + 1) at word k (64
 // used); rows 68 words apart so the PV loads (row = query, word 8 ks + t (+4))
 // are bank-conflict free.
-constexpr int kPtWords = 68;
+constexpr int kPtWords = 68;  // 272 B: rows stay 16-byte aligned for the P^T stores
 constexpr int kFpChunk = 32;       // fp tokens per fp-kernel chunk
 constexpr float kAlpha = 0.12751743074f;  // log2(e) / sqrt(128)
 constexpr float kLazy = 8.f;  // log2-domain slack of the running max (P <= 256)
@@ -579,13 +579,18 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 if (2 * tig + j < GROUP) {
-                    uint32_t* row = &sm.pt[st][(2 * tig + j) % PT_ROWS][8 * gid];
+                    uint32_t pw[8];
 #pragma unroll
                     for (int m = 0; m < 8; ++m) {
                         const float wlo = (m & 1) ? 1.f / 16.f : 1.f / 256.f, whi = (m & 1) ? 1.f / 64.f : 1.f / 4.f;
                         const int clo = (m & 1) ? 2 : 0, chi = (m & 1) ? 3 : 1;
-                        row[m] = ex2_h2(pack_f16x2(fmaf(acc[m][j], wlo, bw[clo][j]), fmaf(acc[m][2 + j], whi, bw[chi][j])));
+                        // two f32 ex2 + one pack: fewer instructions than ex2.f16x2 (3 on sm_100)
+                        pw[m] = pack_f16x2(ex2(fmaf(acc[m][j], wlo, bw[clo][j])), ex2(fmaf(acc[m][2 + j], whi, bw[chi][j])));
                     }
+                    // the row's 8 words are contiguous: two 16-byte stores
+                    uint4* row = reinterpret_cast<uint4*>(&sm.pt[st][(2 * tig + j) % PT_ROWS][8 * gid]);
+                    row[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+                    row[1] = make_uint4(pw[4], pw[5], pw[6], pw[7]);
                 }
             }
         }
@@ -774,9 +779,12 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
 // slots (short contexts: many small CTAs, one wave); 4 when 8-warp CTAs would
 // need more than one wave and a unit has <= 128 slots; 16 above 128 slots
 // (long contexts); else 8
-template <int GROUP, int WARPS>
+// (long contexts); else 8.  CSPLIT CTAs share a row (channel slices) when the
+// rows alone would not fill the GPU (a few long units: C4).
+template <int GROUP, int WARPS, int CSPLIT = 1>
 __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
-    const int u = blockIdx.x / GROUP, g = blockIdx.x - (blockIdx.x / GROUP) * GROUP;
+    const int slice = blockIdx.x % CSPLIT, r = blockIdx.x / CSPLIT;
+    const int u = r / GROUP, g = r - (r / GROUP) * GROUP;
     const KittyCacheDesc& c = P.c;
     // the unit's part list depends only on its length (written by the append,
     // before the page grid): computed before waiting on the fp grid
@@ -816,8 +824,8 @@ __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
     };
     const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
     const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
-    lse_merge_row<GROUP, decltype(slot_of), WARPS>(P.part + (int64_t)u * P.nslot * kStride, kStride, nparts, slot_of, g,
-                                                  P.out, P.out_dtype, row);
+    lse_merge_row<GROUP, decltype(slot_of), WARPS, CSPLIT>(P.part + (int64_t)u * P.nslot * kStride, kStride, nparts,
+                                                          slot_of, g, P.out, P.out_dtype, row, slice);
 }
 
 }  // namespace fastattn
@@ -978,6 +986,15 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
         }
         if (prm.nslot > 128) {  // long contexts: few rows, hundreds of parts each
             cfg.blockDim = dim3(16 * 32);
+            const long long rows = (long long)prm.units * GROUP;
+            if (rows * 2 <= num_sms()) {  // channel slices so that the merge spans the GPU
+                cfg.gridDim = dim3(static_cast<unsigned>(rows * 8));
+                return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 16, 8>, prm);
+            }
+            if (rows <= 2LL * num_sms()) {
+                cfg.gridDim = dim3(static_cast<unsigned>(rows * 4));
+                return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 16, 4>, prm);
+            }
             return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 16>, prm);
         }
         cfg.blockDim = dim3(kMergeWarps * 32);

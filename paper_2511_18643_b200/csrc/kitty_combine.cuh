@@ -29,19 +29,25 @@ __device__ __forceinline__ float merge_ex2(float x) {
 // batch below that: the (m, l) loads of the max pass are reused), so any part
 // count is merged -- a 256K-token unit alone on a GPU has ~2 000.
 constexpr int kMaxParts = 1024;
-template <int GROUP, class SlotFn, int WARPS = kMergeWarps>
+// CSPLIT > 1 (long contexts, few rows): the row's channels are split over
+// CSPLIT CTAs (`slice` = this CTA's), so a handful of (unit, row) merges still
+// fill the GPU; a part's slice is 128 / CSPLIT floats, read by 32 / CSPLIT
+// lanes, so a warp covers CSPLIT parts per step.
+template <int GROUP, class SlotFn, int WARPS = kMergeWarps, int CSPLIT = 1>
 __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int nparts, SlotFn slot_of, int g,
-                                              void* out, int out_dtype, int64_t row) {
+                                              void* out, int out_dtype, int64_t row, int slice = 0) {
     constexpr int D = 128;
     constexpr int T = WARPS * 32;
     constexpr int F = WARPS == 8 ? 8 : 16;  // accumulator rows in flight per warp
+    constexpr int LPP = 32 / CSPLIT;        // lanes per part slice
     __shared__ int s_slot[kMaxParts];
     __shared__ float s_w[kMaxParts];
     __shared__ float s_l[kMaxParts];
     __shared__ float s_red[WARPS];
     __shared__ float s_lsum[WARPS];
-    __shared__ float4 s_acc[WARPS][32];
+    __shared__ float4 s_acc[WARPS][LPP];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane / LPP, cl = lane - sub * LPP;
     auto load_ml = [&](int i) {
         return __ldcg(reinterpret_cast<const float2*>(pb + (int64_t)slot_of(i) * stride + GROUP * D + 2 * g));
     };
@@ -64,7 +70,8 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
 #pragma unroll
     for (int w = 1; w < WARPS; ++w) M = fmaxf(M, s_red[w]);
     float lsum = 0.f;
-    const float* rowp = pb + g * D + 4 * lane;
+    const int c0 = slice * (D / CSPLIT);
+    const float* rowp = pb + g * D + c0 + 4 * cl;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int b0 = 0; b0 < nparts; b0 += kMaxParts) {
         const int nb = min(kMaxParts, nparts - b0);
@@ -84,12 +91,12 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
             lsum = fmaf(w, s_l[i], lsum);
         }
         __syncthreads();  // s_w complete
-        for (int i0 = warp; i0 < nb; i0 += F * WARPS) {
+        for (int i0 = warp * CSPLIT + sub; i0 < nb; i0 += F * WARPS * CSPLIT) {
             float4 a[F];
             float w[F];
 #pragma unroll
             for (int j = 0; j < F; ++j) {
-                const int i = i0 + j * WARPS;
+                const int i = i0 + j * WARPS * CSPLIT;
                 const bool ok = i < nb;
                 w[j] = ok ? s_w[i] : 0.f;
                 a[j] = ok ? __ldcg(reinterpret_cast<const float4*>(rowp + (int64_t)s_slot[i] * stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -105,10 +112,17 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    s_acc[warp][lane] = acc;
+#pragma unroll
+    for (int o = LPP; o < 32; o <<= 1) {  // the warp's CSPLIT parts per step -> one slice sum
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+    }
+    if (sub == 0) s_acc[warp][cl] = acc;
     if (lane == 0) s_lsum[warp] = lsum;
     __syncthreads();
-    if (warp != 0) return;
+    if (warp != 0 || lane >= LPP) return;
     float4 o = s_acc[0][lane];
     float lt = s_lsum[0];
 #pragma unroll
@@ -121,13 +135,14 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
         lt += s_lsum[w];
     }
     const float inv = 1.f / lt;
+    const int64_t ob = row * D + c0 + 4 * lane;
     if (out_dtype == KITTY_F32) {
-        reinterpret_cast<float4*>(static_cast<float*>(out) + row * D)[lane] = make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
+        *reinterpret_cast<float4*>(static_cast<float*>(out) + ob) = make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
     } else {
         uint2 v;
         v.x = f32_to_bf16_bits(o.x * inv) | (f32_to_bf16_bits(o.y * inv) << 16);
         v.y = f32_to_bf16_bits(o.z * inv) | (f32_to_bf16_bits(o.w * inv) << 16);
-        reinterpret_cast<uint2*>(static_cast<uint16_t*>(out) + row * D)[lane] = v;
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(out) + ob) = v;
     }
 }
 
