@@ -793,6 +793,8 @@ __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
     // max_tokens tokens only: make the caller's check() raise
     if (g == 0 && threadIdx.x == 0 && c.unit_len[u] > P.max_tokens) set_status(c.status, KITTY_STATUS_LENGTH);
     asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the fp grid (KITTY_PDL bit 2)
+    // the next kernel on the stream (the next layer's append) may become resident
+    asm volatile("griddepcontrol.launch_dependents;");
     if (gm.n == 0) {  // an empty (retired) sequence of the batch: zero output rows
         const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
         const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
@@ -959,10 +961,12 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
         if (e != cudaSuccess) return e;
     }
     {
+        const int fsm = fptok::tc_scratch_bytes((int)prm.c.key_slot_bytes);
+        if ((e = set_kernel_smem((const void*)fp_tokens_kernel<GROUP>, fsm, true)) != cudaSuccess) return e;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(prm.units * prm.fmax);
         cfg.blockDim = dim3(128);
-        cfg.dynamicSmemBytes = fptok::tc_scratch_bytes((int)prm.c.key_slot_bytes);
+        cfg.dynamicSmemBytes = fsm;
         cfg.stream = st;
         cfg.attrs = at + 1;
         cfg.numAttrs = 1;
@@ -975,30 +979,34 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
         cfg.stream = st;
         cfg.attrs = at + 2;
         cfg.numAttrs = 1;
+        auto go = [&](auto kfn) -> cudaError_t {
+            cudaError_t e2 = set_kernel_smem((const void*)kfn, 0, true);
+            return e2 != cudaSuccess ? e2 : cudaLaunchKernelEx(&cfg, kfn, prm);
+        };
         if (prm.nslot <= 32) {
             cfg.blockDim = dim3(2 * 32);
-            return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 2>, prm);
+            return go(combine_parts_kernel<GROUP, 2>);
         }
         // 4 warps when 8-warp CTAs would not be resident in one wave (~48 warps / SM)
         if (prm.nslot <= 128 && (long long)prm.units * GROUP * kMergeWarps > 48LL * num_sms()) {
             cfg.blockDim = dim3(4 * 32);
-            return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 4>, prm);
+            return go(combine_parts_kernel<GROUP, 4>);
         }
         if (prm.nslot > 128) {  // long contexts: few rows, hundreds of parts each
             cfg.blockDim = dim3(16 * 32);
             const long long rows = (long long)prm.units * GROUP;
             if (rows * 2 <= num_sms()) {  // channel slices so that the merge spans the GPU
                 cfg.gridDim = dim3(static_cast<unsigned>(rows * 8));
-                return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 16, 8>, prm);
+                return go(combine_parts_kernel<GROUP, 16, 8>);
             }
             if (rows <= 2LL * num_sms()) {
                 cfg.gridDim = dim3(static_cast<unsigned>(rows * 4));
-                return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 16, 4>, prm);
+                return go(combine_parts_kernel<GROUP, 16, 4>);
             }
-            return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, 16>, prm);
+            return go(combine_parts_kernel<GROUP, 16>);
         }
         cfg.blockDim = dim3(kMergeWarps * 32);
-        return cudaLaunchKernelEx(&cfg, combine_parts_kernel<GROUP, kMergeWarps>, prm);
+        return go(combine_parts_kernel<GROUP, kMergeWarps>);
     }
 }
 

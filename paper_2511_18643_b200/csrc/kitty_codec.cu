@@ -493,6 +493,9 @@ __device__ void pack_value_into_cache(const KittyCacheDesc& c, int u, int p, con
 template <typename T>
 __global__ void append_kernel(KittyCacheDesc c, const T* k_new, const T* v_new) {
     extern __shared__ __align__(16) uint8_t smem[];
+    // launched as a programmatic dependent of the preceding kernel (e.g. the
+    // previous layer's merge): everything below waits for it to complete
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // the attention grid that follows may run its prologue now (it waits on us
     // with griddepcontrol.wait before reading the cache)
     asm volatile("griddepcontrol.launch_dependents;");
@@ -877,6 +880,12 @@ cudaError_t launch_dequant_value_pages(const uint8_t* slots, int64_t stride, int
     return cudaGetLastError();
 }
 
+// KITTY_PDL bit 3: the append as a programmatic dependent of the preceding kernel
+static const int g_pdl_append = [] {
+    const char* e = std::getenv("KITTY_PDL");
+    return e ? (std::atoi(e) >> 3) & 1 : 1;
+}();
+
 template <typename T>
 static cudaError_t append_t(const KittyCacheDesc& c, const void* k_new, const void* v_new, cudaStream_t st) {
     const int units = c.num_seqs * c.cfg.h_kv;
@@ -884,9 +893,23 @@ static cudaError_t append_t(const KittyCacheDesc& c, const void* k_new, const vo
     if (sizeof(T) == 2 && c.cfg.d == fastpack::kD && c.cfg.g == fastpack::kG && sm < sizeof(fastpack::Smem))
         sm = sizeof(fastpack::Smem);
     auto kfn = append_kernel<T>;
-    if (cudaError_t e = set_kernel_smem((const void*)kfn, (int)sm)) return e;
-    kfn<<<units, fastpack::kThreads, sm, st>>>(c, static_cast<const T*>(k_new), static_cast<const T*>(v_new));
-    return cudaGetLastError();
+    // the decode kernels all prefer the max-shared carveout: an SM never has to
+    // reconfigure between them, and PDL dependents can become resident beside
+    // their predecessor
+    if (cudaError_t e = set_kernel_smem((const void*)kfn, (int)sm, true)) return e;
+    // programmatic dependent launch: the CTAs become resident while the
+    // preceding kernel drains and wait for it in griddepcontrol.wait
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at.val.programmaticStreamSerializationAllowed = g_pdl_append;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units);
+    cfg.blockDim = dim3(fastpack::kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, c, static_cast<const T*>(k_new), static_cast<const T*>(v_new));
 }
 
 cudaError_t launch_append(const KittyCacheDesc& c, const void* k_new, const void* v_new, cudaStream_t st) {
