@@ -3,6 +3,8 @@
 // launches on the caller's stream and returns a KittyStatus.
 #include <cstdio>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kitty_attention.cuh"
 #include "kitty_codec.cuh"
 
@@ -23,6 +25,13 @@ int invalid(const char* msg, int code = KITTY_ERR_INVALID) {
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// NVTX range around every compute entry point (host-side enqueue; shows the
+// append / pack / attend phases on an Nsight timeline; a no-op without a tool)
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+};
 
 int check_page_shape(int num_pages, int g, int d) {
     if (num_pages < 0) return invalid("num_pages must be >= 0");
@@ -81,12 +90,14 @@ const char* kitty_last_error(void) { return g_last_error; }
 
 int kitty_channel_scores(const void* x, int32_t dtype, int32_t num_pages, int32_t g, int32_t d,
                          double* scores, void* stream) {
+    Range nvtx_range("kitty_channel_scores");
     if (num_pages < 0 || g < 1 || d < 1) return invalid("scores need a (tokens, channels) matrix with tokens >= 1");
     return cuda_status(kitty::launch_channel_scores(x, dtype, num_pages, g, d, scores, as_stream(stream)));
 }
 
 int kitty_select_boost(const double* scores, int32_t num_pages, int32_t d, int32_t k,
                        int64_t* boosted, void* stream) {
+    Range nvtx_range("kitty_select_boost");
     if (num_pages < 0 || d < 0 || k < 0 || k > d) return invalid("bad selection size");
     return cuda_status(kitty::launch_select_boost(scores, num_pages, d, k, boosted, as_stream(stream)));
 }
@@ -95,6 +106,7 @@ int kitty_pack_key_pages(const void* x, int32_t dtype, int32_t num_pages, int32_
                          int32_t d_boost, const int64_t* boosted, uint8_t* slots,
                          int64_t slot_stride, float* scales_f32, float* zeros_f32,
                          uint32_t* status, void* stream) {
+    Range nvtx_range("kitty_pack_key_pages");
     int rc = check_page_shape(num_pages, g, d);
     if (rc != KITTY_OK) return rc;
     if (d_boost < 0 || d_boost > d) return invalid("boost selection indexes a channel outside the page");
@@ -108,6 +120,7 @@ int kitty_pack_key_pages(const void* x, int32_t dtype, int32_t num_pages, int32_
 int kitty_pack_value_pages(const void* x, int32_t dtype, int32_t num_pages, int32_t g, int32_t d,
                            uint8_t* slots, int64_t slot_stride, float* scales_f32,
                            float* zeros_f32, uint32_t* status, void* stream) {
+    Range nvtx_range("kitty_pack_value_pages");
     int rc = check_page_shape(num_pages, g, d);
     if (rc != KITTY_OK) return rc;
     if (slot_stride < kitty_value_slot_bytes(d, g)) return invalid("slot stride smaller than a value page");
@@ -118,6 +131,7 @@ int kitty_pack_value_pages(const void* x, int32_t dtype, int32_t num_pages, int3
 int kitty_dequant_key_pages(const uint8_t* slots, int64_t slot_stride, int32_t num_pages, int32_t g,
                             int32_t d, int32_t d_boost, const float* scales_f32,
                             const float* zeros_f32, float* out, uint32_t* status, void* stream) {
+    Range nvtx_range("kitty_dequant_key_pages");
     int rc = check_page_shape(num_pages, g, d);
     if (rc != KITTY_OK) return rc;
     if (d_boost < 0 || d_boost > 255) return invalid("bad d_boost");
@@ -129,6 +143,7 @@ int kitty_dequant_key_pages(const uint8_t* slots, int64_t slot_stride, int32_t n
 int kitty_dequant_value_pages(const uint8_t* slots, int64_t slot_stride, int32_t num_pages,
                               int32_t g, int32_t d, const float* scales_f32,
                               const float* zeros_f32, float* out, void* stream) {
+    Range nvtx_range("kitty_dequant_value_pages");
     int rc = check_page_shape(num_pages, g, d);
     if (rc != KITTY_OK) return rc;
     return cuda_status(kitty::launch_dequant_value_pages(slots, slot_stride, num_pages, g, d,
@@ -137,12 +152,14 @@ int kitty_dequant_value_pages(const uint8_t* slots, int64_t slot_stride, int32_t
 
 int kitty_fake_quantize(const float* x, int32_t rows, int32_t cols, int32_t per_token, const int32_t* bits,
                         float* out, void* stream) {
+    Range nvtx_range("kitty_fake_quantize");
     if (rows < 0 || cols < 0) return invalid("fake_quantize_matrix needs a 2-D matrix");
     return cuda_status(kitty::launch_fake_quantize(x, rows, cols, per_token, bits, out, as_stream(stream)));
 }
 
 int kitty_append(const KittyCacheDesc* cache, const void* k_new, const void* v_new,
                  void* stream) {
+    Range nvtx_range("kitty_append");
     int rc = check_cache(cache);
     if (rc != KITTY_OK) return rc;
     return cuda_status(kitty::launch_append(*cache, k_new, v_new, as_stream(stream)));
@@ -150,6 +167,7 @@ int kitty_append(const KittyCacheDesc* cache, const void* k_new, const void* v_n
 
 int kitty_prefill(const KittyCacheDesc* cache, const void* keys, const void* values,
                   int32_t prompt_len, void* stream) {
+    Range nvtx_range("kitty_prefill");
     int rc = check_cache(cache);
     if (rc != KITTY_OK) return rc;
     if (prompt_len < 0) return invalid("prompt length must be >= 0");
@@ -157,6 +175,7 @@ int kitty_prefill(const KittyCacheDesc* cache, const void* keys, const void* val
 }
 
 int kitty_release_sequences(const KittyCacheDesc* cache, int32_t first_seq, int32_t num_seqs, void* stream) {
+    Range nvtx_range("kitty_release_sequences");
     int rc = check_cache(cache);
     if (rc != KITTY_OK) return rc;
     if (first_seq < 0 || num_seqs < 0 || first_seq + num_seqs > cache->num_seqs) return invalid("sequence range out of bounds");
@@ -165,6 +184,7 @@ int kitty_release_sequences(const KittyCacheDesc* cache, int32_t first_seq, int3
 
 int kitty_import_pages(const KittyCacheDesc* cache, int32_t unit, int32_t kind, const uint8_t* bodies,
                        int32_t first_page, int32_t num_pages, void* stream) {
+    Range nvtx_range("kitty_import_pages");
     int rc = check_cache(cache);
     if (rc != KITTY_OK) return rc;
     if (unit < 0 || unit >= cache->num_seqs * cache->cfg.h_kv) return invalid("unit out of range");
@@ -177,6 +197,7 @@ int kitty_import_pages(const KittyCacheDesc* cache, int32_t unit, int32_t kind, 
 
 int kitty_flatten(const KittyCacheDesc* cache, int32_t unit, int32_t n, float* keys_out,
                   float* values_out, void* stream) {
+    Range nvtx_range("kitty_flatten");
     int rc = check_cache(cache);
     if (rc != KITTY_OK) return rc;
     if (unit < 0 || unit >= cache->num_seqs * cache->cfg.h_kv) return invalid("unit out of range");
@@ -191,6 +212,7 @@ size_t kitty_attention_workspace_bytes(const KittyCacheDesc* cache, int32_t max_
 int kitty_decode_attention(const KittyCacheDesc* cache, const void* q, void* out,
                            int32_t out_dtype, int32_t max_tokens, void* workspace,
                            size_t workspace_bytes, void* stream) {
+    Range nvtx_range("kitty_decode_attention");
     int rc = check_cache(cache);
     if (rc != KITTY_OK) return rc;
     if (max_tokens < 1) return invalid("attend on an empty cache");
@@ -208,6 +230,7 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv, 
                           int32_t d, const float* queries, int32_t n_q,
                           const int32_t* kv_head_map, float* out, void* workspace,
                           size_t workspace_bytes, void* stream) {
+    Range nvtx_range("kitty_dense_attention");
     if (length <= 0) return invalid("attention over zero tokens");
     if (h_kv < 1 || d < 1 || n_q < 0) return invalid("bad dense attention shape");
     return cuda_status(kitty::launch_dense_attention(keys, values, h_kv, length, d, queries, n_q,
@@ -223,6 +246,7 @@ size_t kitty_sensitivity_workspace_bytes(int32_t h_q, int32_t lq, int32_t h_kv, 
 int kitty_channel_sensitivity(const float* queries, int32_t h_q, int32_t lq, const float* keys, int32_t h_kv,
                               int32_t length, int32_t d, int32_t bits, double* mse, void* workspace,
                               size_t workspace_bytes, void* stream) {
+    Range nvtx_range("kitty_channel_sensitivity");
     if (h_q < 1 || h_kv < 1 || lq < 1 || length < 1 || d < 1) return invalid("sensitivity needs non-empty queries and keys");
     if (h_q % h_kv != 0) return invalid("query head count must be a multiple of KV head count");
     if (bits != 2 && bits != 4 && bits != 16) return invalid("bits must be 2, 4 or 16");
@@ -240,6 +264,7 @@ size_t kitty_attention_mse_workspace_bytes(int32_t heads, int32_t lq, int32_t le
 int kitty_attention_mse(const float* keys, int32_t length, int32_t d, const float* queries, int32_t heads,
                         int32_t lq, const int32_t* bits, double* out, void* workspace, size_t workspace_bytes,
                         void* stream) {
+    Range nvtx_range("kitty_attention_mse");
     if (heads < 1 || lq < 1 || length < 1 || d < 1) return invalid("attention_mse needs non-empty queries and keys");
     if (workspace_bytes < kitty::attention_mse_workspace_bytes(heads, lq, length, d)) return invalid("workspace too small");
     return cuda_status(kitty::launch_attention_mse(keys, length, d, queries, heads, lq, bits, out, workspace,

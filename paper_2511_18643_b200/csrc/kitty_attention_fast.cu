@@ -9,14 +9,12 @@
 //
 // One attention call = three launches chained by programmatic dependent
 // launch:
-//  * page_pair_kernel: the 2-bit pages.  A CTA is a warp PAIR: warp 0 (QK)
-//    pulls work items (chunks of a unit's pages) from an atomic queue, streams
-//    key pages through a 2-stage shared-memory ring (cp.async.bulk + mbarrier),
-//    computes Q K^T and the online softmax and hands the probabilities P^T of
-//    each page to warp 1 (PV) through a 2-stage P^T ring; warp 1 streams the
-//    value pages through its own 2-stage ring and accumulates P V in
-//    registers.  The two warps work on consecutive pages at once (QK of page
-//    i + 1 beside PV of page i), 8 pairs per SM;
+//  * page_kernel: the 2-bit pages.  Persistent CTAs (2 per SM x 4 warps);
+//    every warp is one page stream: it pulls work items (chunks of a unit's
+//    pages) from an atomic queue, stages key and value pages through 2-slot
+//    rings (cp.async.bulk + mbarrier; keys are issued one page ahead of
+//    values) and runs QK^T + online softmax of page k + 1 interleaved with
+//    P V of page k in one basic block;
 //  * 2-bit codes become fp16 MMA operands with one PRMT (pair two channel /
 //    token rows) plus one LOP3 per 2 codes: (x & mask) | 0x6400 = 1024 + w c;
 //    the 1024 offset and w are removed per row after the MMA;
@@ -26,6 +24,8 @@
 //    carry the unscaled q / p (GQA group <= 4; group 8 uses a second MMA);
 //  * mma.sync.m16n8k16 f16 x f16 -> f32, swap-AB: M = 16 tokens (QK) or 16
 //    channels (PV), N = the GQA group, K = 16 channels (QK) or tokens (PV);
+//  * softmax in the log2 domain with lazy rescaling (the running max moves
+//    only when a page exceeds it by 2^8);
 //  * each work item leaves a partial record (acc, m, l) in the workspace;
 //  * fp_tokens_kernel: the sink / q-buffer / local tokens (kitty_fp.cuh);
 //  * combine_parts_kernel: LSE merge of a unit's partials (kitty_combine.cuh).
@@ -529,10 +529,13 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
                 const uint32_t s01 = static_cast<uint32_t>(sc[c0]) | (static_cast<uint32_t>(sc[c1]) << 16);
                 const uint32_t q89 = static_cast<uint32_t>(qt[c8]) | (static_cast<uint32_t>(qt[c9]) << 16);
                 const uint32_t s89 = static_cast<uint32_t>(sc[c8]) | (static_cast<uint32_t>(sc[c9]) << 16);
-                // rows past d_boost (d_boost 8: rows 8-15 of the tile) are not high-bit rows
+                // rows past d_boost (d_boost 8: rows 8-15 of the tile; an odd
+                // d_boost: the second half of a pair) are not high-bit rows
                 const bool ok = main_col && qcol < GROUP;
-                const uint32_t b0 = ok && j0 < d_boost ? hmul2(q01, s01) : 0u;
-                const uint32_t b1 = ok && j0 + 8 < d_boost ? hmul2(q89, s89) : 0u;
+                const uint32_t m0 = (ok && j0 < d_boost ? 0xffffu : 0u) | (ok && j0 + 1 < d_boost ? 0xffff0000u : 0u);
+                const uint32_t m1 = (ok && j0 + 8 < d_boost ? 0xffffu : 0u) | (ok && j0 + 9 < d_boost ? 0xffff0000u : 0u);
+                const uint32_t b0 = hmul2(q01, s01) & m0;
+                const uint32_t b1 = hmul2(q89, s89) & m1;
                 const uint32_t* hw = reinterpret_cast<const uint32_t*>(kp + D * G / 4);
                 mma_codes(kc, acc, hw[8 * j0 + gid], hw[8 * (j0 + 1) + gid], hw[8 * (j0 + 8) + gid],
                           hw[8 * (j0 + 9) + gid], b0, b1);

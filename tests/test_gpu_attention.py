@@ -69,11 +69,13 @@ def test_long_single_unit_vs_oracle(cuda, n, group):
     assert np.max(np.abs(out - want)) <= TOL
 
 
-@pytest.mark.parametrize("frac", [0.0, 0.0625, 0.125, 0.25])
+@pytest.mark.parametrize("frac", [0.0, 0.03, 0.0625, 0.1, 0.125, 0.15, 0.2, 0.25])
 @pytest.mark.parametrize("group", [4, 8])
 def test_boost_fractions_vs_oracle(cuda, frac, group):
     # C3's boost variants: d_boost 0 / 8 / 16 / 32 (the NKH = 0 / 1 / 1 / 2
-    # instantiations; 8 boosted rows fill half of a 16-row high-bits tile)
+    # instantiations; 8 boosted rows fill half of a 16-row high-bits tile),
+    # and fractions whose d_boost is not a multiple of 8 or is odd (4, 13, 19,
+    # 26): high-bit rows past d_boost must not contribute
     rng = np.random.default_rng(int(frac * 1000) + group)
     b, h_kv, n = 2, 2, 3000
     h_q = h_kv * group
