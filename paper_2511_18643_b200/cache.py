@@ -228,15 +228,6 @@ class KittyBatchCache:
 
     # -- decode step -----------------------------------------------------------
 
-    def _count_events(self, b: int, n_after: int):
-        cfg = self.cfg
-        past = max(0, n_after - cfg.s)
-        if past and past % cfg.g == 0:
-            self.key_pack_events[b] += 1
-        vtot = max(0, past - cfg.r)
-        if vtot and vtot % cfg.g == 0:
-            self.value_pack_events[b] += 1
-
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor):
         """Step 1 + step 3 for every sequence: k_new/v_new [B, h_kv, D] bf16.
         Every row appends (a retired row restarts from its sink)."""
@@ -250,24 +241,31 @@ class KittyBatchCache:
         _lib.check(self.lib.kitty_append(self._desc_ref, k_new.data_ptr(), v_new.data_ptr(), _stream()), "append")
         self.advance_host(need)
 
-    def append_page_need(self):
-        """(key, value) pages the next append packs: the host mirror of its pops."""
-        kneed = vneed = 0
-        for n in self.lengths:
-            kp0, vp0 = self._page_pair(n)
-            kp1, vp1 = self._page_pair(n + 1)
-            kneed += (kp1 - kp0) * self.cfg.h_kv
-            vneed += (vp1 - vp0) * self.cfg.h_kv
-        return kneed, vneed
+    def append_packs(self):
+        """Which sequences' next append packs a key / a value page (boolean
+        arrays): the host mirror of the device's pack triggers and slot pops
+        (vectorised: a decode step's host work must stay far below its GPU time)."""
+        cfg = self.cfg
+        past = np.maximum(np.asarray(self.lengths, dtype=np.int64) + 1 - cfg.s, 0)
+        vtot = np.maximum(past - cfg.r, 0)
+        return (past > 0) & (past % cfg.g == 0), (vtot > 0) & (vtot % cfg.g == 0)
 
-    def advance_host(self, need=None):
+    def append_page_need(self, packs=None):
+        """(key, value) pages the next append packs."""
+        kpk, vpk = self.append_packs() if packs is None else packs
+        return int(kpk.sum()) * self.cfg.h_kv, int(vpk.sum()) * self.cfg.h_kv
+
+    def advance_host(self, need=None, packs=None):
         """Host mirror after one append launch (eager or graph replay)."""
-        need = self.append_page_need() if need is None else need
+        packs = self.append_packs() if packs is None else packs
+        need = self.append_page_need(packs) if need is None else need
         self.free_pages[0] -= need[0]
         self.free_pages[1] -= need[1]
-        for b in range(self.num_seqs):
-            self.lengths[b] += 1
-            self._count_events(b, self.lengths[b])
+        self.lengths = [x + 1 for x in self.lengths]
+        if packs[0].any():
+            self.key_pack_events = (np.asarray(self.key_pack_events) + packs[0]).tolist()
+        if packs[1].any():
+            self.value_pack_events = (np.asarray(self.value_pack_events) + packs[1]).tolist()
 
     def prefill(self, keys: torch.Tensor, values: torch.Tensor, lengths=None):
         """cache.py:125-142 for an empty batch: keys/values [B, h_kv, P, D].

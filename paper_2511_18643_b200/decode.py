@@ -73,17 +73,19 @@ class DecodeStep:
                                                   self.ws.numel(), st), "attend")
 
     def _advance(self):
+        # every layer holds the same lengths: the pack mirror is computed once
+        packs = self.layers[0].append_packs()
+        need = self.layers[0].append_page_need(packs)
         for cache in self.layers:
-            cache.advance_host()
+            cache.advance_host(need, packs)
 
     def step(self):
         """One eager decode step over all layers."""
         if max(self.layers[0].lengths) + 1 > self.max_tokens:
             raise ValueError("decode step past the allocated context")
-        for cache in self.layers:  # the pools are sized for max_tokens: never short, but checked
-            need = cache.append_page_need()
-            if need[0] > cache.free_pages[0] or need[1] > cache.free_pages[1]:
-                raise ValueError("decode step would exhaust a layer's page pool")
+        need = self.layers[0].append_page_need()  # the pools are sized for max_tokens: never short, but checked
+        if any(need[0] > c.free_pages[0] or need[1] > c.free_pages[1] for c in self.layers):
+            raise ValueError("decode step would exhaust a layer's page pool")
         if self.graph is not None:
             self.graph.replay()
         else:
