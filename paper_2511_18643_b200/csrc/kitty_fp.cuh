@@ -104,6 +104,112 @@ __device__ __forceinline__ void page_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
+__device__ __forceinline__ uint32_t fprmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+__device__ __forceinline__ uint32_t fand_or(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ uint32_t fhmul2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+// Logits of a chunk whose 32 keys all sit in one key page at a 16-token
+// aligned offset (the local window at the default shapes): computed from the
+// 2-bit codes like the page kernel does (PRMT + LOP3 -> f16 1024 + w c, the
+// per-channel scale folded into B = q alpha s, offset and zero points from an
+// auxiliary MMA, boosted rows as extra k-steps) instead of dequantising every
+// key element.  Warp w covers channels [32 w, 32 w + 32) (k-steps 2w, 2w + 1)
+// and boosted k-step w; lane gid's tokens are off0 + 4 gid + j, code j of one
+// byte: j = 0 / 1 -> tile 0 rows gid / gid + 8 (w 256 / 4), j = 2 / 3 -> tile 1
+// (w 16 / 64).  Writes the warp's partial logits lg[token][8] (columns = query).
+template <int GROUP>
+__device__ __forceinline__ void qk_from_codes(const uint8_t* kbuf, int d_boost, int off0, const uint16_t* qbase,
+                                              const uint8_t* inv, float* lg) {
+    constexpr bool kFull = GROUP == 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const bool main_col = kFull || gid < 4;
+    const int qcol = kFull ? gid : (gid & 3);
+    const bool qok = qcol < GROUP;
+    const int scale_off = D * G / 4 + d_boost * G / 4 + D, zero_off = scale_off + 2 * D;
+    const uint32_t* kw = reinterpret_cast<const uint32_t*>(kbuf);
+    const int wi = (off0 >> 4) + (gid >> 2);
+    const uint32_t B = gid & 3;
+    const uint32_t sel = B | (B << 4) | ((4 + B) << 8) | ((4 + B) << 12);
+    const uint32_t m0 = 0x03000300u, m1 = 0x000C000Cu, m2 = 0x00300030u, m3 = 0x00C000C0u, magic = 0x64006400u;
+    const uint32_t ones = 0x3C003C00u;
+    const uint16_t* qg = qbase + (qok ? qcol : 0) * D;
+    float acc[2][4] = {}, aux[4] = {}, aux2[4] = {};
+    auto kstep = [&](const uint32_t* rows, int r0, uint32_t b0, uint32_t b1) {
+        // rows r0, r0 + 1, r0 + 8, r0 + 9 of a 32-byte-row code array
+        const uint32_t w0 = rows[8 * r0 + wi], w1 = rows[8 * (r0 + 1) + wi];
+        const uint32_t w2 = rows[8 * (r0 + 8) + wi], w3 = rows[8 * (r0 + 9) + wi];
+        const uint32_t x = fprmt(w0, w1, sel), y = fprmt(w2, w3, sel);
+        hmma(acc[0], fand_or(x, m0, magic), fand_or(x, m1, magic), fand_or(y, m0, magic), fand_or(y, m1, magic), b0, b1);
+        hmma(acc[1], fand_or(x, m2, magic), fand_or(x, m3, magic), fand_or(y, m2, magic), fand_or(y, m3, magic), b0, b1);
+    };
+#pragma unroll
+    for (int k2 = 0; k2 < 2; ++k2) {
+        const int c0 = 16 * (2 * warp + k2) + 2 * tig;
+        uint32_t qa0 = 0u, qa1 = 0u;
+        if (qok) {
+            const uint32_t u0 = __ldg(reinterpret_cast<const uint32_t*>(qg + c0));
+            const uint32_t u1 = __ldg(reinterpret_cast<const uint32_t*>(qg + c0 + 8));
+            qa0 = f2h2(__uint_as_float(u0 << 16) * kAlpha, __uint_as_float(u0 & 0xffff0000u) * kAlpha);
+            qa1 = f2h2(__uint_as_float(u1 << 16) * kAlpha, __uint_as_float(u1 & 0xffff0000u) * kAlpha);
+        }
+        // B columns 0..group-1: q alpha s; group <= 4: columns 4-7 carry q alpha (aux sums)
+        const uint32_t s0 = main_col ? *reinterpret_cast<const uint32_t*>(kbuf + scale_off + 2 * c0) : ones;
+        const uint32_t s1 = main_col ? *reinterpret_cast<const uint32_t*>(kbuf + scale_off + 2 * (c0 + 8)) : ones;
+        const uint32_t b0 = fhmul2(qa0, s0), b1 = fhmul2(qa1, s1);
+        const uint32_t z0 = *reinterpret_cast<const uint32_t*>(kbuf + zero_off + 2 * c0);
+        const uint32_t z1 = *reinterpret_cast<const uint32_t*>(kbuf + zero_off + 2 * (c0 + 8));
+        kstep(kw, c0, b0, b1);
+        hmma(aux, ones, z0, ones, z1, b0, b1);  // row 0: sum B; row 8: sum z B
+        if (kFull) hmma(aux2, ones, z0, ones, z1, qa0, qa1);
+    }
+    // boosted rows: warp w takes high-bit rows [16 w, 16 w + 16)
+    if (16 * warp < d_boost) {
+        const int j0 = 16 * warp + 2 * tig;
+        auto qs = [&](int j) -> uint32_t {  // 4 q alpha s of the channel row j boosts (f16 bits), 0 past d_boost
+            if (j >= d_boost || !main_col || !qok) return 0u;
+            const int ch = inv[j];
+            const float qv = __uint_as_float(static_cast<uint32_t>(qg[ch]) << 16) * (4.f * kAlpha);
+            const uint16_t sv = *reinterpret_cast<const uint16_t*>(kbuf + scale_off + 2 * ch);
+            return __half_as_ushort(__hmul(__float2half_rn(qv), __ushort_as_half(sv)));
+        };
+        const uint32_t b0 = qs(j0) | (qs(j0 + 1) << 16), b1 = qs(j0 + 8) | (qs(j0 + 9) << 16);
+        kstep(kw + (D * G / 4) / 4, j0, b0, b1);
+        hmma(aux, ones, 0u, ones, 0u, b0, b1);
+    }
+    // corrections per column: L = acc / w - (1024 / w) sum B + sum z q alpha
+    float sumB[2], cst[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        sumB[j] = __shfl_sync(0xffffffffu, aux[j], kFull ? tig : (tig & 1));
+        cst[j] = kFull ? __shfl_sync(0xffffffffu, aux2[2 + j], tig) : __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
+    }
+    __syncthreads();  // every warp is done reading the page: the logits reuse its bytes
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int g = 2 * tig + j;
+        if (g < GROUP && (kFull || tig < 2)) {
+            // tile t, row gid + 8 h: code 2 t + h of byte gid -> token 4 gid + 2 t + h
+            lg[(4 * gid + 0) * 8 + g] = fmaf(acc[0][j], 1.f / 256.f, cst[j] - 4.f * sumB[j]);
+            lg[(4 * gid + 1) * 8 + g] = fmaf(acc[0][2 + j], 1.f / 4.f, cst[j] - 256.f * sumB[j]);
+            lg[(4 * gid + 2) * 8 + g] = fmaf(acc[1][j], 1.f / 16.f, cst[j] - 64.f * sumB[j]);
+            lg[(4 * gid + 3) * 8 + g] = fmaf(acc[1][2 + j], 1.f / 64.f, cst[j] - 16.f * sumB[j]);
+        }
+    }
+}
+
 template <int GROUP>
 __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part, int nslot, int stride,
                          uint8_t* scratch, int u, int fc, int max_tokens) {
@@ -117,9 +223,9 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
     uint16_t* vt = kt + kChunk * kRowH;                                          // [32][kRowH] f16 values
     uint64_t* bar = reinterpret_cast<uint64_t*>(vt + kChunk * kRowH);
     // after the dequantisation (a __syncthreads) the key page is dead: logits
-    // and P^T live in its bytes (2.5 KB <= the slot)
-    float* lgs = reinterpret_cast<float*>(kbuf);                   // [2][32][8] logit halves
-    uint16_t* pT = reinterpret_cast<uint16_t*>(lgs + 2 * kChunk * 8);  // [8][32] f16 probabilities
+    // and P^T live in its bytes (4.5 KB <= the slot)
+    float* lgs = reinterpret_cast<float*>(kbuf);                   // [4][32][8] partial logits
+    uint16_t* pT = reinterpret_cast<uint16_t*>(lgs + 4 * kChunk * 8);  // [8][32] f16 probabilities
     const Geom gm = geom(c, u, max_tokens);
     const int s_len = min(gm.n, S);
     const int c0 = fc * kChunk;
@@ -181,6 +287,26 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
         if (!paged) reinterpret_cast<uint4*>(kt + tk * kRowH + 32 * qq)[i] = bf16x8_to_f16x8(kw[i]);
         reinterpret_cast<uint4*>(vt + tk * kRowH + 32 * qq)[i] = bf16x8_to_f16x8(vw[i]);
     }
+    // a chunk whose keys all sit in one key page at a 16-token aligned offset
+    // (the local window at the default shapes): logits straight from the codes
+    int npart = 2;
+    {
+        const int pbase = vbase - S + c0 - s_len;
+        const int off0 = pbase - pg_lo * G;
+        if (pg_lo == pg_hi && c0 >= s_len && pbase + cnt - 1 < gm.kp * G && (off0 & 15) == 0 && off0 + kChunk <= G) {
+            uint8_t* inv = reinterpret_cast<uint8_t*>(kt);  // the key tile is not needed
+            if (tid == 0) page_wait(bar, 0);
+            __syncthreads();
+            if (tid < D) {
+                const uint8_t bi = kbuf[D * G / 4 + d_boost * G / 4 + tid];
+                if (bi < 32) inv[bi] = static_cast<uint8_t>(tid);
+            }
+            __syncthreads();
+            qk_from_codes<GROUP>(kbuf, d_boost, off0, qbase, inv, lgs + warp * kChunk * 8);
+            npart = 4;
+            pg_hi = pg_lo - 1;  // no dequantisation below
+        }
+    }
     // keys that sit in key pages: dequantise into the tile.  thread = (channel
     // pair cp, token half th); the half's codes come from one shifted 64-bit
     // window of each channel's code row (16 tokens = 32 bits)
@@ -239,7 +365,7 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
     const uint32_t kt_s = static_cast<uint32_t>(__cvta_generic_to_shared(kt));
     const uint32_t vt_s = static_cast<uint32_t>(__cvta_generic_to_shared(vt));
     // ---- QK: N = 8 query columns (q alpha as f16 B fragments) ----
-    {
+    if (npart == 2) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         const int i4 = lane >> 3, r8 = lane & 7;
 #pragma unroll
@@ -264,7 +390,9 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
     for (int pass = 0; pass < (GROUP + 3) / 4; ++pass) {
         const int g = 4 * pass + warp;
         if (g < GROUP) {
-            const float x = valid ? lgs[lane * 8 + g] + lgs[kChunk * 8 + lane * 8 + g] : -INFINITY;
+            float x = lgs[lane * 8 + g] + lgs[kChunk * 8 + lane * 8 + g];
+            if (npart == 4) x += lgs[2 * kChunk * 8 + lane * 8 + g] + lgs[3 * kChunk * 8 + lane * 8 + g];
+            x = valid ? x : -INFINITY;
             float mc = x;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
