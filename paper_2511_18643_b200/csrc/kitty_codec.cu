@@ -502,20 +502,32 @@ __global__ void append_kernel(KittyCacheDesc c, const T* k_new, const T* v_new) 
     const KittyConfigC& k = c.cfg;
     const int u = blockIdx.x;
     const int d = k.d, S = k.s, G = k.g, W = k.r + k.g;
-    const int t = c.unit_len[u];
     const T* kr = k_new + (int64_t)u * d;
     const T* vr = v_new + (int64_t)u * d;
+    // rows of 16-byte vectors that one pass of the CTA covers: their loads go
+    // out together with the length's (one round trip instead of two)
+    const int nv = static_cast<int>(d * sizeof(T) / 16);
+    const bool vec = (d * sizeof(T)) % 16 == 0 && nv <= static_cast<int>(blockDim.x);
+    uint4 kv4 = make_uint4(0, 0, 0, 0), vv4 = kv4;
+    if (vec && threadIdx.x < nv) {
+        kv4 = reinterpret_cast<const uint4*>(kr)[threadIdx.x];
+        vv4 = reinterpret_cast<const uint4*>(vr)[threadIdx.x];
+    }
+    const int t = c.unit_len[u];
     T* ksink = static_cast<T*>(c.k_sink);
     T* vsink = static_cast<T*>(c.v_sink);
     T* kq = static_cast<T*>(c.k_qbuf) + (int64_t)u * G * d;
     T* vring = static_cast<T*>(c.v_ring) + (int64_t)u * W * d;
-    if (t < S) {
-        copy_row(ksink + ((int64_t)u * S + t) * d, kr, d);
-        copy_row(vsink + ((int64_t)u * S + t) * d, vr, d);
+    T* kd = t < S ? ksink + ((int64_t)u * S + t) * d : kq + (int64_t)((t - S) % G) * d;
+    T* vd = t < S ? vsink + ((int64_t)u * S + t) * d : vring + (int64_t)((t - S) % W) * d;
+    if (vec) {
+        if (threadIdx.x < nv) {
+            reinterpret_cast<uint4*>(kd)[threadIdx.x] = kv4;
+            reinterpret_cast<uint4*>(vd)[threadIdx.x] = vv4;
+        }
     } else {
-        const int pc = t - S;  // position past the sink
-        copy_row(kq + (int64_t)(pc % G) * d, kr, d);
-        copy_row(vring + (int64_t)(pc % W) * d, vr, d);
+        copy_row(kd, kr, d);
+        copy_row(vd, vr, d);
     }
     const int n = t + 1;
     const int past = n > S ? n - S : 0;
