@@ -237,10 +237,12 @@ def run_kitty(args):
     if use_graph:
         step.capture()
 
+    xs = step.pack_inputs(ks, vs, qs)  # [n_in, k | v | q] resident in HBM
+    nk = ks[0].numel()  # ks / vs / qs become views of xs (one copy of the inputs in HBM)
+    ks, vs, qs = (xs[:, :nk].view(ks.shape), xs[:, nk:2 * nk].view(vs.shape), xs[:, 2 * nk:].view(qs.shape))
+
     def one(i):
-        step.k_in.copy_(ks[i])
-        step.v_in.copy_(vs[i])
-        step.q_in.copy_(qs[i])
+        step.inputs.copy_(xs[i])
         step.step()
 
     for i in range(warmup):
@@ -444,11 +446,9 @@ def _e2e(step, ks, vs, qs, warmup, steps, world, dev) -> float:
     import torch
     import torch.distributed as dist
 
-    host_k = ks[warmup:].cpu().pin_memory()
-    host_v = vs[warmup:].cpu().pin_memory()
-    host_q = qs[warmup:].cpu().pin_memory()
+    host_x = step.pack_inputs(ks[warmup:], vs[warmup:], qs[warmup:]).cpu().pin_memory()
     host_out = [torch.empty(step.out.shape, dtype=step.out.dtype).pin_memory() for _ in range(steps)]
-    st_in = [(torch.empty_like(step.k_in), torch.empty_like(step.v_in), torch.empty_like(step.q_in)) for _ in range(2)]
+    st_in = [torch.empty_like(step.inputs) for _ in range(2)]
     st_out = [torch.empty_like(step.out) for _ in range(2)]
     ev = lambda: torch.cuda.Event()
     in_ready, in_free, out_ready, out_free = [ev(), ev()], [ev(), ev()], [ev(), ev()], [ev(), ev()]
@@ -468,15 +468,12 @@ def _e2e(step, ks, vs, qs, warmup, steps, world, dev) -> float:
         with torch.cuda.stream(cp):
             if i >= 2:
                 cp.wait_event(in_free[i % 2])
-            for dst, src in zip(st_in[i % 2], (host_k[i], host_v[i], host_q[i])):
-                dst.copy_(src, non_blocking=True)
+            st_in[i % 2].copy_(host_x[i], non_blocking=True)
             in_ready[i % 2].record(cp)
 
     if not pipelined:
         for i in range(steps):
-            step.k_in.copy_(host_k[i], non_blocking=True)
-            step.v_in.copy_(host_v[i], non_blocking=True)
-            step.q_in.copy_(host_q[i], non_blocking=True)
+            step.inputs.copy_(host_x[i], non_blocking=True)
             step.step()
             host_out[i].copy_(step.out, non_blocking=True)
     else:
@@ -485,9 +482,7 @@ def _e2e(step, ks, vs, qs, warmup, steps, world, dev) -> float:
             if i + 1 < steps:
                 h2d(i + 1)
             main.wait_event(in_ready[i % 2])
-            step.k_in.copy_(st_in[i % 2][0])
-            step.v_in.copy_(st_in[i % 2][1])
-            step.q_in.copy_(st_in[i % 2][2])
+            step.inputs.copy_(st_in[i % 2])
             in_free[i % 2].record(main)
             step.step()
             if i >= 2:

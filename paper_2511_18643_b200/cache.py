@@ -242,18 +242,22 @@ class KittyBatchCache:
         self.advance_host(need)
 
     def append_packs(self):
-        """Which sequences' next append packs a key / a value page (boolean
-        arrays): the host mirror of the device's pack triggers and slot pops
-        (vectorised: a decode step's host work must stay far below its GPU time)."""
-        cfg = self.cfg
-        past = np.maximum(np.asarray(self.lengths, dtype=np.int64) + 1 - cfg.s, 0)
-        vtot = np.maximum(past - cfg.r, 0)
-        return (past > 0) & (past % cfg.g == 0), (vtot > 0) & (vtot % cfg.g == 0)
+        """Which sequences' next append packs a key / a value page (two lists of
+        bools): the host mirror of the device's pack triggers and slot pops.
+        One pass per decode step (``DecodeStep`` shares it across its layers)."""
+        S, R, G = self.cfg.s, self.cfg.r, self.cfg.g
+        kpk, vpk = [], []
+        for n in self.lengths:
+            past = n + 1 - S
+            kpk.append(past > 0 and past % G == 0)
+            vtot = past - R
+            vpk.append(vtot > 0 and vtot % G == 0)
+        return kpk, vpk
 
     def append_page_need(self, packs=None):
         """(key, value) pages the next append packs."""
         kpk, vpk = self.append_packs() if packs is None else packs
-        return int(kpk.sum()) * self.cfg.h_kv, int(vpk.sum()) * self.cfg.h_kv
+        return sum(kpk) * self.cfg.h_kv, sum(vpk) * self.cfg.h_kv
 
     def advance_host(self, need=None, packs=None):
         """Host mirror after one append launch (eager or graph replay)."""
@@ -262,10 +266,10 @@ class KittyBatchCache:
         self.free_pages[0] -= need[0]
         self.free_pages[1] -= need[1]
         self.lengths = [x + 1 for x in self.lengths]
-        if packs[0].any():
-            self.key_pack_events = (np.asarray(self.key_pack_events) + packs[0]).tolist()
-        if packs[1].any():
-            self.value_pack_events = (np.asarray(self.value_pack_events) + packs[1]).tolist()
+        if need[0]:
+            self.key_pack_events = [e + p for e, p in zip(self.key_pack_events, packs[0])]
+        if need[1]:
+            self.value_pack_events = [e + p for e, p in zip(self.value_pack_events, packs[1])]
 
     def prefill(self, keys: torch.Tensor, values: torch.Tensor, lengths=None):
         """cache.py:125-142 for an empty batch: keys/values [B, h_kv, P, D].

@@ -30,9 +30,14 @@ class DecodeStep:
         dev = self.layers[0].device
         self.device = dev
         bf = torch.bfloat16
-        self.k_in = torch.zeros((num_layers, num_seqs, cfg.h_kv, cfg.d), dtype=bf, device=dev)
-        self.v_in = torch.zeros((num_layers, num_seqs, cfg.h_kv, cfg.d), dtype=bf, device=dev)
-        self.q_in = torch.zeros((num_layers, num_seqs, cfg.h_q, cfg.d), dtype=bf, device=dev)
+        # the step's inputs in one flat buffer (k | v | q): a caller refreshes
+        # them with a single copy per step
+        nk = num_layers * num_seqs * cfg.h_kv * cfg.d
+        nq = num_layers * num_seqs * cfg.h_q * cfg.d
+        self.inputs = torch.zeros(2 * nk + nq, dtype=bf, device=dev)
+        self.k_in = self.inputs[:nk].view(num_layers, num_seqs, cfg.h_kv, cfg.d)
+        self.v_in = self.inputs[nk:2 * nk].view(num_layers, num_seqs, cfg.h_kv, cfg.d)
+        self.q_in = self.inputs[2 * nk:].view(num_layers, num_seqs, cfg.h_q, cfg.d)
         self.out = torch.zeros((num_layers, num_seqs, cfg.h_q, cfg.d), dtype=bf, device=dev)
         # one workspace shared by the layers (they run back to back on one stream)
         self.ws = self.layers[0].workspace(max_tokens)
@@ -47,7 +52,13 @@ class DecodeStep:
 
     # bytes moved per step by the inputs / outputs (for the e2e host copies)
     def input_bytes(self) -> int:
-        return sum(t.numel() * t.element_size() for t in (self.k_in, self.v_in, self.q_in))
+        return self.inputs.numel() * self.inputs.element_size()
+
+    def pack_inputs(self, k, v, q) -> torch.Tensor:
+        """k / v [layers, B, h_kv, D], q [layers, B, h_q, D] -> one flat tensor
+        laid out like ``inputs`` (leading batch dimensions of k, v, q kept)."""
+        lead = k.shape[:-4]
+        return torch.cat([k.reshape(*lead, -1), v.reshape(*lead, -1), q.reshape(*lead, -1)], dim=-1)
 
     def output_bytes(self) -> int:
         return self.out.numel() * self.out.element_size()
@@ -72,25 +83,22 @@ class DecodeStep:
                                                   _lib.KITTY_BF16, self.max_tokens, self.ws.data_ptr(),
                                                   self.ws.numel(), st), "attend")
 
-    def _advance(self):
-        # every layer holds the same lengths: the pack mirror is computed once
-        packs = self.layers[0].append_packs()
-        need = self.layers[0].append_page_need(packs)
-        for cache in self.layers:
-            cache.advance_host(need, packs)
-
     def step(self):
         """One eager decode step over all layers."""
         if max(self.layers[0].lengths) + 1 > self.max_tokens:
             raise ValueError("decode step past the allocated context")
-        need = self.layers[0].append_page_need()  # the pools are sized for max_tokens: never short, but checked
-        if any(need[0] > c.free_pages[0] or need[1] > c.free_pages[1] for c in self.layers):
-            raise ValueError("decode step would exhaust a layer's page pool")
+        # every layer holds the same lengths: the pack mirror is computed once per step
+        packs = self.layers[0].append_packs()
+        need = self.layers[0].append_page_need(packs)
+        if need[0] or need[1]:  # the pools are sized for max_tokens: never short, but checked
+            if any(need[0] > c.free_pages[0] or need[1] > c.free_pages[1] for c in self.layers):
+                raise ValueError("decode step would exhaust a layer's page pool")
         if self.graph is not None:
             self.graph.replay()
         else:
             self._launch()
-        self._advance()
+        for cache in self.layers:
+            cache.advance_host(need, packs)
 
     def capture(self):
         """Capture one step into a CUDA graph (does not advance the state)."""
