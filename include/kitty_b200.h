@@ -266,6 +266,14 @@ int kitty_attention_mse(const float* keys, int32_t length, int32_t d, const floa
                         int32_t lq, const int32_t* bits, double* out, void* workspace, size_t workspace_bytes,
                         void* stream);
 
+/* The attention probabilities oracle_attend returns (cache.py:291-299) and
+ * KittyCacheState.attend(return_probs=True) (cache.py:236-251): dense f32
+ * keys [h_kv][length][d], queries [n_q][d], query i reads KV head
+ * kv_head_map[i]; probs [n_q][length] f32 (max-subtracted softmax of
+ * (k . q) / sqrt(d)). */
+int kitty_dense_probs(const float* keys, int32_t h_kv, int32_t length, int32_t d, const float* queries,
+                      int32_t n_q, const int32_t* kv_head_map, float* probs, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

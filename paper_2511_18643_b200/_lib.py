@@ -96,6 +96,8 @@ SIGNATURES = [
     ("kitty_attention_mse_workspace_bytes", c_size_t, [c_int32, c_int32, c_int32, c_int32]),
     ("kitty_attention_mse", ctypes.c_int,
      [c_void_p, c_int32, c_int32, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("kitty_dense_probs", ctypes.c_int,
+     [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("kitty_dense_attention_workspace_bytes", c_size_t, [c_int32, c_int32, c_int32]),
     ("kitty_dense_attention", ctypes.c_int,
      [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),

@@ -658,22 +658,39 @@ class KittyCacheState:
         return self._b.flatten(0, kv_head)[1].cpu().numpy()
 
     def attend(self, q, return_probs: bool = False) -> AttentionOutput:
-        """cache.py:217-252 on the device."""
+        """cache.py:217-252 on the device.  With ``return_probs`` the (h_q, n)
+        probabilities come from ``kitty_dense_probs`` over the flattened keys
+        (the decode kernels never materialise them)."""
         if self.total_tokens == 0:
             raise KittyError("attend on an empty cache")
-        if return_probs:
-            raise KittyError("return_probs is a debug output the fused kernel never materialises")
         q = np.asarray(q.cpu() if isinstance(q, torch.Tensor) else q, dtype=np.float32)
         if q.ndim == 1:
             q = q[None, :]
         if q.shape != (self.cfg.h_q, self.cfg.d):
             raise KittyError(f"q must have shape ({self.cfg.h_q}, {self.cfg.d}), got {q.shape}")
-        out = self._b.attend(torch.from_numpy(np.ascontiguousarray(q))[None], out_dtype=torch.float32)
+        qt = torch.from_numpy(np.ascontiguousarray(q))
+        out = self._b.attend(qt[None], out_dtype=torch.float32)
+        probs = None
+        if return_probs:
+            keys = torch.stack([self._b.flatten(0, h)[0] for h in range(self.cfg.h_kv)])
+            probs = _dense_probs(keys, qt.to(keys.device), [i // self.cfg.group_size for i in range(self.cfg.h_q)])
         self._b.check()
-        return AttentionOutput(outputs=out[0].cpu().numpy())
+        return AttentionOutput(outputs=out[0].cpu().numpy(), probs=None if probs is None else probs.cpu().numpy())
 
     def export_pages(self, kv_head: int = 0):
         return self._b.export_pages(0, kv_head)
+
+
+def _dense_probs(keys: torch.Tensor, queries: torch.Tensor, kv_head_map) -> torch.Tensor:
+    """kitty_dense_probs: keys [h_kv, L, d] f32, queries [n_q, d] f32 on the device."""
+    lib = _lib.load_library()
+    h_kv, length, d = keys.shape
+    n_q = queries.shape[0]
+    kmap = torch.tensor(list(kv_head_map), dtype=torch.int32, device=keys.device)
+    probs = torch.empty((n_q, length), dtype=torch.float32, device=keys.device)
+    _lib.check(lib.kitty_dense_probs(keys.contiguous().data_ptr(), h_kv, length, d, queries.contiguous().data_ptr(), n_q,
+                                     kmap.data_ptr(), probs.data_ptr(), _stream()), "attention probabilities")
+    return probs
 
 
 def oracle_attend(keys, values, queries, kv_head_map=None) -> AttentionOutput:
@@ -704,4 +721,5 @@ def oracle_attend(keys, values, queries, kv_head_map=None) -> AttentionOutput:
     _lib.check(lib.kitty_dense_attention(k.data_ptr(), v.data_ptr(), h_kv, length, d, qs.data_ptr(), n_q,
                                          kmap.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream()),
                "oracle_attend")
-    return AttentionOutput(outputs=out.cpu().numpy())
+    probs = _dense_probs(k, qs, kv_head_map)
+    return AttentionOutput(outputs=out.cpu().numpy(), probs=probs.cpu().numpy())

@@ -238,6 +238,14 @@ int kitty_dense_attention(const float* keys, const float* values, int32_t h_kv, 
                                                      as_stream(stream)));
 }
 
+int kitty_dense_probs(const float* keys, int32_t h_kv, int32_t length, int32_t d, const float* queries,
+                      int32_t n_q, const int32_t* kv_head_map, float* probs, void* stream) {
+    Range nvtx_range("kitty_dense_probs");
+    if (length <= 0) return invalid("attention over zero tokens");
+    if (h_kv < 1 || d < 1 || n_q < 0) return invalid("bad dense attention shape");
+    return cuda_status(kitty::launch_dense_probs(keys, length, d, queries, n_q, kv_head_map, probs, as_stream(stream)));
+}
+
 size_t kitty_sensitivity_workspace_bytes(int32_t h_q, int32_t lq, int32_t h_kv, int32_t length, int32_t d) {
     if (h_q < 0 || lq < 0 || h_kv < 1 || length < 0 || d < 0) return 0;
     return kitty::sensitivity_workspace_bytes(h_q, lq, h_kv, length, d);

@@ -253,6 +253,62 @@ cudaError_t launch_decode_attention(const KittyCacheDesc& c, const void* q, void
     return cudaGetLastError();
 }
 
+// The attention probabilities of dense f32 keys (cache.py:241-244,252 and
+// oracle_attend's probs, cache.py:291-299): one CTA per query row; logits =
+// (k . q) / f32(sqrt d) as the generic kernel computes them, then the
+// max-subtracted exponentials (expf) over their sum.  The row of `probs`
+// holds the logits, then the exponentials, then the probabilities.
+__global__ void dense_probs_kernel(const float* keys, int length, int d, const float* queries,
+                                   const int32_t* kv_map, float* probs) {
+    extern __shared__ __align__(16) float qsm[];
+    __shared__ float red[32];
+    const int i = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    for (int ch = tid; ch < d; ch += nt) qsm[ch] = queries[(int64_t)i * d + ch];
+    __syncthreads();
+    const float* kb = keys + (int64_t)kv_map[i] * length * d;
+    float* row = probs + (int64_t)i * length;
+    const float sqrt_d = static_cast<float>(sqrt(static_cast<double>(d)));
+    float m = -INFINITY;
+    for (int t = tid; t < length; t += nt) {
+        float acc = 0.f;
+        for (int ch = 0; ch < d; ++ch) acc = fmaf(qsm[ch], kb[(int64_t)t * d + ch], acc);
+        const float l = __fdiv_rn(acc, sqrt_d);
+        row[t] = l;
+        m = fmaxf(m, l);
+    }
+    auto block_reduce = [&](float v, bool is_max) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float w = __shfl_xor_sync(0xffffffffu, v, o);
+            v = is_max ? fmaxf(v, w) : v + w;
+        }
+        __syncthreads();
+        if (lane == 0) red[warp] = v;
+        __syncthreads();
+        v = red[0];
+        for (int w = 1; w < (nt + 31) / 32; ++w) v = is_max ? fmaxf(v, red[w]) : v + red[w];
+        return v;
+    };
+    m = block_reduce(m, true);
+    float sum = 0.f;
+    for (int t = tid; t < length; t += nt) {
+        const float e = expf(row[t] - m);
+        row[t] = e;
+        sum += e;
+    }
+    sum = block_reduce(sum, false);
+    for (int t = tid; t < length; t += nt) row[t] = __fdiv_rn(row[t], sum);
+}
+
+cudaError_t launch_dense_probs(const float* keys, int length, int d, const float* queries, int n_q,
+                               const int32_t* kv_map, float* probs, cudaStream_t st) {
+    if (n_q == 0 || length == 0) return cudaSuccess;
+    const int sm = d * static_cast<int>(sizeof(float));
+    if (cudaError_t e = set_kernel_smem((const void*)dense_probs_kernel, sm)) return e;
+    dense_probs_kernel<<<n_q, 256, sm, st>>>(keys, length, d, queries, kv_map, probs);
+    return cudaGetLastError();
+}
+
 size_t dense_attention_workspace_bytes(int n_q, int length, int d) {
     return (size_t)n_q * generic_splits(length) * (d + 2) * sizeof(float);
 }

@@ -56,6 +56,8 @@ cudaError_t launch_decode_attention(const KittyCacheDesc& c, const void* q, void
                                     int out_dtype, int max_tokens, void* ws, size_t ws_bytes,
                                     cudaStream_t st);
 size_t dense_attention_workspace_bytes(int n_q, int length, int d);
+cudaError_t launch_dense_probs(const float* keys, int length, int d, const float* queries, int n_q,
+                               const int32_t* kv_map, float* probs, cudaStream_t st);
 cudaError_t launch_dense_attention(const float* keys, const float* values, int h_kv, int length,
                                    int d, const float* queries, int n_q, const int32_t* kv_map,
                                    float* out, void* ws, size_t ws_bytes, cudaStream_t st);

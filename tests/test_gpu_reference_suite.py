@@ -39,3 +39,37 @@ def test_fake_quantize_matrix_matches_oracle(cuda, axis, shape):
     got = cuda.fake_quantize_matrix(x, axis, bits)
     want = ko.fake_quantize_matrix(x, axis, bits)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def _np_probs(keys, q):
+    """cache.py:241-244 / :291-299 in numpy (float32 logits over sqrt(d), then
+    the max-subtracted softmax of _softmax_columns)."""
+    logits = (keys @ q) / np.float32(np.sqrt(keys.shape[-1]))
+    e = np.exp(logits - logits.max(), dtype=np.float32)
+    return e / e.sum()
+
+
+def test_attention_probabilities(cuda):
+    # oracle_attend(...).probs and KittyCacheState.attend(return_probs=True).probs
+    rng = np.random.default_rng(17)
+    keys = rng.normal(0, 1, (2, 300, 64)).astype(np.float32)
+    values = rng.normal(0, 1, (2, 300, 64)).astype(np.float32)
+    q = rng.normal(0, 1, (6, 64)).astype(np.float32)
+    res = cuda.oracle_attend(keys, values, q)
+    assert res.probs.shape == (6, 300)
+    for i in range(6):
+        np.testing.assert_allclose(res.probs[i], _np_probs(keys[i * 2 // 6], q[i]), rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(res.probs.sum(axis=1), 1.0, rtol=1e-5)
+    cfg = cuda.KittyConfig(s=4, r=8, g=8, d=16, h_kv=2, h_q=4)
+    st = cuda.KittyCacheState(cfg, max_tokens=64)
+    k = rng.normal(0, 1, (2, 41, 16)).astype(np.float32)
+    v = rng.normal(0, 1, (2, 41, 16)).astype(np.float32)
+    st.prefill(k, v)
+    qq = rng.normal(0, 1, (4, 16)).astype(np.float32)
+    out = st.attend(qq, return_probs=True)
+    assert out.probs.shape == (4, 41)
+    for i in range(4):
+        np.testing.assert_allclose(out.probs[i], _np_probs(st.flatten_keys(i // 2), qq[i]), rtol=1e-5, atol=1e-7)
+    # the outputs are the probabilities applied to the flattened values
+    for i in range(4):
+        np.testing.assert_allclose(out.outputs[i], out.probs[i] @ st.flatten_values(i // 2), rtol=1e-4, atol=1e-5)

@@ -13,11 +13,6 @@ OUT_OF_SCOPE = {
     "test_cache.py::test_prefill_equals_fold_of_inserts[16-": "pass-through (16-bit) pages are not built on the device",
     "test_cache.py::test_passthrough_matches_dense_oracle": "pass-through (16-bit) pages are not built on the device",
     "test_cache.py::test_order_reconstruction_fuzz": "uses pass-through (16-bit) pages, not built on the device",
-    # probabilities: a debug output a flash-decode never materialises
-    "test_cache.py::test_singleton_softmax": "return_probs is not materialised by the fused kernel",
-    "test_cache.py::test_probabilities_normalized": "return_probs is not materialised by the fused kernel",
-    "test_cache.py::test_oracle_uniform_keys_uniform_probs": "oracle_attend returns outputs only (no probs)",
-    "test_cache.py::test_oracle_concentration_on_aligned_key": "oracle_attend returns outputs only (no probs)",
 }
 
 
