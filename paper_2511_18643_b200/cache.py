@@ -49,8 +49,6 @@ def component_counts(cfg: KittyConfig, length: int) -> dict:
 
 
 def _check_device_config(cfg: KittyConfig):
-    if cfg.key_bits == PASSTHROUGH_BITS or cfg.value_bits == PASSTHROUGH_BITS:
-        raise KittyError("pass-through (16-bit) pages are not built on the device (key/value bits must be 2)")
     if cfg.heuristic != "magnitude":
         raise KittyError("the device pack path implements the magnitude heuristic only")
 
@@ -88,8 +86,11 @@ class KittyBatchCache:
         self.num_seqs = int(num_seqs)
         self.device = torch.device(device) if device is not None else _device()
         self.units = self.num_seqs * cfg.h_kv
-        self.key_slot = key_slot_bytes(cfg.d, cfg.g, cfg.d_boost)
-        self.value_slot = value_slot_bytes(cfg.d, cfg.g)
+        # a 2-bit page slot is its KTYP body; a pass-through (16-bit) page slot
+        # holds the block's g rows in the row dtype (cache.py:150-153,167-170)
+        rows = cfg.g * cfg.d * (4 if row_dtype == torch.float32 else 2)
+        self.key_slot = rows if cfg.key_bits == PASSTHROUGH_BITS else key_slot_bytes(cfg.d, cfg.g, cfg.d_boost)
+        self.value_slot = rows if cfg.value_bits == PASSTHROUGH_BITS else value_slot_bytes(cfg.d, cfg.g)
         self.lengths = [0] * self.num_seqs  # host mirror of unit_len (no syncs needed)
         self.key_pack_events = [0] * self.num_seqs
         self.value_pack_events = [0] * self.num_seqs
@@ -445,12 +446,26 @@ class KittyBatchCache:
         from .pages import deserialize_page
 
         cfg = self.cfg
-        kb, vb = self.export_pages(b, h)
-        kpg = [deserialize_page(x) for x in kb]
-        vpg = [deserialize_page(x) for x in vb]
+        c = self.page_counts(b)
+        u = b * cfg.h_kv + h
+        if cfg.key_bits == PASSTHROUGH_BITS or cfg.value_bits == PASSTHROUGH_BITS:
+            def raw(pool, table, count):  # pass-through pages: the stored rows as float32 (g, d) arrays
+                out = []
+                for sl in table[u, :count].tolist():
+                    a = pool[sl].view(self.row_dtype).view(cfg.g, cfg.d).float().cpu().numpy()
+                    out.append(np.ascontiguousarray(a))
+                return out
+            kraw = raw(self.key_pool, self.key_block_table, c["key_pages"]) if cfg.key_bits == PASSTHROUGH_BITS else None
+            vraw = raw(self.value_pool, self.value_block_table, c["value_pages"]) if cfg.value_bits == PASSTHROUGH_BITS else None
+        else:
+            kraw = vraw = None
+        ks_ = self.key_page_slots(b, h).cpu().numpy() if kraw is None else []
+        vs_ = self.value_page_slots(b, h).cpu().numpy() if vraw is None else []
+        kb = [serialize_slot(x.tobytes(), "key", cfg.d, cfg.g, cfg.d_boost) for x in ks_]
+        vb = [serialize_slot(x.tobytes(), "value", cfg.d, cfg.g) for x in vs_]
+        kpg = kraw if kraw is not None else [deserialize_page(x) for x in kb]
+        vpg = vraw if vraw is not None else [deserialize_page(x) for x in vb]
         if self.f32_metadata:
-            u = b * cfg.h_kv + h
-            c = self.page_counts(b)
             km = self.key_meta[self.key_block_table[u, : c["key_pages"]].long()].cpu().numpy()
             vm = self.value_meta[self.value_block_table[u, : c["value_pages"]].long()].cpu().numpy()
 
@@ -459,8 +474,10 @@ class KittyBatchCache:
                 a.flags.writeable = False
                 return a
 
-            kpg = [dataclasses.replace(pg, scales=frozen(m[: cfg.d]), zero_points=frozen(m[cfg.d:])) for pg, m in zip(kpg, km)]
-            vpg = [dataclasses.replace(pg, scales=frozen(m[: cfg.g]), zero_points=frozen(m[cfg.g:])) for pg, m in zip(vpg, vm)]
+            if kraw is None:
+                kpg = [dataclasses.replace(pg, scales=frozen(m[: cfg.d]), zero_points=frozen(m[cfg.d:])) for pg, m in zip(kpg, km)]
+            if vraw is None:
+                vpg = [dataclasses.replace(pg, scales=frozen(m[: cfg.g]), zero_points=frozen(m[cfg.g:])) for pg, m in zip(vpg, vm)]
         return kpg, vpg
 
     def page_counts(self, b: int) -> dict:
@@ -482,6 +499,8 @@ class KittyBatchCache:
     def export_pages(self, b: int, h: int):
         """KTYP byte strings of all pages of (b, h): header + memcpy of each slot."""
         cfg = self.cfg
+        if cfg.key_bits == PASSTHROUGH_BITS or cfg.value_bits == PASSTHROUGH_BITS:
+            raise KittyError("pass-through (16-bit) pages have no KTYP encoding (pages.py:207-237)")
         ks = self.key_page_slots(b, h).cpu().numpy()
         vs = self.value_page_slots(b, h).cpu().numpy()
         return ([serialize_slot(s.tobytes(), "key", cfg.d, cfg.g, cfg.d_boost) for s in ks],

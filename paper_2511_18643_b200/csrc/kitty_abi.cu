@@ -46,8 +46,10 @@ int check_cache(const KittyCacheDesc* c) {
     const int rc = kitty_validate_config(&c->cfg);
     if (rc != KITTY_OK) return rc;
     if (c->num_seqs < 0 || c->max_pages < 0) return invalid("bad batch geometry");
-    if (c->key_slot_bytes != kitty_key_slot_bytes(c->cfg.d, c->cfg.g, c->cfg.d_boost) ||
-        c->value_slot_bytes != kitty_value_slot_bytes(c->cfg.d, c->cfg.g))
+    // a 2-bit page slot is its KTYP body; a pass-through page slot holds g rows of the row dtype
+    const int64_t rows = (int64_t)c->cfg.g * c->cfg.d * (c->row_dtype == KITTY_F32 ? 4 : 2);
+    if (c->key_slot_bytes != (c->cfg.key_bits == 16 ? rows : kitty_key_slot_bytes(c->cfg.d, c->cfg.g, c->cfg.d_boost)) ||
+        c->value_slot_bytes != (c->cfg.value_bits == 16 ? rows : kitty_value_slot_bytes(c->cfg.d, c->cfg.g)))
         return invalid("slot sizes do not match the page layout");
     if (c->row_dtype != KITTY_BF16 && c->row_dtype != KITTY_F32) return invalid("row_dtype must be KITTY_BF16 or KITTY_F32");
     if ((c->key_free == nullptr) != (c->value_free == nullptr)) return invalid("a page pool needs both free stacks");
@@ -77,9 +79,7 @@ int kitty_validate_config(const KittyConfigC* c) {
         return invalid("key/value bits must be in (2, 16)", KITTY_ERR_CONFIG);
     if (c->d_boost < 0 || c->d_boost > c->d) return invalid("d_boost outside [0, d]", KITTY_ERR_CONFIG);
     if (c->d_boost > 255) return invalid("d_boost exceeds the uint8 boost-index space", KITTY_ERR_CONFIG);
-    // device limits
-    if (c->key_bits != 2 || c->value_bits != 2)
-        return invalid("pass-through (16-bit) pages are not built on the device", KITTY_ERR_UNSUPPORTED);
+    // device limits (pass-through 16-bit pages run on the generic kernels)
     if ((size_t)c->g * c->d * 2 + 8192 > 200 * 1024) return invalid("page too large for one CTA", KITTY_ERR_UNSUPPORTED);
     return KITTY_OK;
 }

@@ -39,6 +39,10 @@ struct CacheSource {
         const int f32 = c.row_dtype == KITTY_F32;
         if (t < S) return rowf(c.k_sink, ((int64_t)u * S + t) * d + ch, f32);
         const int pc = t - S;
+        if (pc < kp * G && c.cfg.key_bits == 16) {  // pass-through page: the block's rows as stored
+            const int32_t sl = c.key_block_table[(int64_t)u * c.max_pages + pc / G];
+            return rowf(c.key_pool + (int64_t)sl * c.key_slot_bytes, (int64_t)(pc % G) * d + ch, f32);
+        }
         if (pc < kp * G) {
             const int p = pc / G, tl = pc % G, gb = G / 4;
             const KeyLayout L{d, G, c.cfg.d_boost};
@@ -59,6 +63,10 @@ struct CacheSource {
         const int f32 = c.row_dtype == KITTY_F32;
         if (t < S) return rowf(c.v_sink, ((int64_t)u * S + t) * d + ch, f32);
         const int pc = t - S;
+        if (pc < vp * G && c.cfg.value_bits == 16) {
+            const int32_t sl = c.value_block_table[(int64_t)u * c.max_pages + pc / G];
+            return rowf(c.value_pool + (int64_t)sl * c.value_slot_bytes, (int64_t)(pc % G) * d + ch, f32);
+        }
         if (pc < vp * G) {
             const int p = pc / G, tl = pc % G;
             const ValueLayout L{d, G};

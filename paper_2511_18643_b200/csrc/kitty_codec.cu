@@ -445,12 +445,31 @@ __device__ int32_t block_claim_slot(const KittyCacheDesc& c, bool key, int u, in
 // Pack key page `p` of unit `u` from `rows` (g consecutive rows of a ring of
 // size `wrap` starting at `start`) into its block-table slot (+ its f32
 // metadata into the side table when the cache keeps one).
+// A pass-through (16-bit) page (cache.py:150-153,167-170): the block's g rows
+// copied as they are (row dtype) into the page's slot.
+template <typename T>
+__device__ void copy_rows_into_slot(const KittyCacheDesc& c, bool key, int u, int p, const T* base, int start,
+                                    int wrap) {
+    const int32_t s = block_claim_slot(c, key, u, p);
+    if (s < 0) return;
+    T* dst = reinterpret_cast<T*>((key ? c.key_pool : c.value_pool) + (int64_t)s * (key ? c.key_slot_bytes : c.value_slot_bytes));
+    const int d = c.cfg.d, g = c.cfg.g;
+    for (int i = threadIdx.x; i < g * d; i += blockDim.x) {
+        const int r = i / d, ch = i - r * d;
+        dst[i] = base[(int64_t)((start + r) % wrap) * d + ch];
+    }
+}
+
 template <typename T>
 __device__ void pack_key_into_cache(const KittyCacheDesc& c, int u, int p, const T* base, int start, int wrap,
                                     uint8_t* smem) {
     const KittyConfigC& k = c.cfg;
     if (p >= c.max_pages) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+        return;
+    }
+    if (k.key_bits == 16) {
+        copy_rows_into_slot(c, true, u, p, base, start, wrap);
         return;
     }
     T* tile = reinterpret_cast<T*>(smem);
@@ -474,6 +493,10 @@ __device__ void pack_value_into_cache(const KittyCacheDesc& c, int u, int p, con
     const KittyConfigC& k = c.cfg;
     if (p >= c.max_pages) {
         if (threadIdx.x == 0) set_status(c.status, KITTY_STATUS_OVERFLOW);
+        return;
+    }
+    if (k.value_bits == 16) {
+        copy_rows_into_slot(c, false, u, p, base, start, wrap);
         return;
     }
     T* tile = reinterpret_cast<T*>(smem);
@@ -534,7 +557,8 @@ __global__ void append_kernel(KittyCacheDesc c, const T* k_new, const T* v_new) 
     const int vtot = past > k.r ? past - k.r : 0;  // tokens that left the local window
     const bool kpack = past > 0 && past % G == 0, vpack = vtot > 0 && vtot % G == 0;
     bool fast = false;
-    if constexpr (sizeof(T) == 2) fast = d == fastpack::kD && G == fastpack::kG && !c.key_meta && !c.value_meta;
+    if constexpr (sizeof(T) == 2)
+        fast = d == fastpack::kD && G == fastpack::kG && !c.key_meta && !c.value_meta && k.key_bits == 2 && k.value_bits == 2;
     if (fast && (kpack || vpack)) {
         if constexpr (sizeof(T) == 2) {
             // the bulk packer's routines: the page rows arrive by TMA (async proxy),
@@ -676,7 +700,10 @@ __global__ void flatten_kernel(KittyCacheDesc c, int u, int n, float* keys_out, 
             vv = row_elem(vsink, ((int64_t)u * S + t) * d + ch);
         } else {
             const int pc = t - S;
-            if (pc < kp * G) {
+            if (pc < kp * G && k.key_bits == 16) {  // pass-through page: the block's rows as stored
+                const int32_t sl = c.key_block_table[(int64_t)u * c.max_pages + pc / G];
+                kv = row_elem(reinterpret_cast<const T*>(c.key_pool + (int64_t)sl * c.key_slot_bytes), (int64_t)(pc % G) * d + ch);
+            } else if (pc < kp * G) {
                 const int p = pc / G, tl = pc % G;
                 const int32_t sl = c.key_block_table[(int64_t)u * c.max_pages + p];
                 const uint8_t* slot = c.key_pool + (int64_t)sl * c.key_slot_bytes;
@@ -690,7 +717,10 @@ __global__ void flatten_kernel(KittyCacheDesc c, int u, int n, float* keys_out, 
             } else {
                 kv = row_elem(kq, ((int64_t)u * G + pc % G) * d + ch);
             }
-            if (pc < vp * G) {
+            if (pc < vp * G && k.value_bits == 16) {
+                const int32_t sl = c.value_block_table[(int64_t)u * c.max_pages + pc / G];
+                vv = row_elem(reinterpret_cast<const T*>(c.value_pool + (int64_t)sl * c.value_slot_bytes), (int64_t)(pc % G) * d + ch);
+            } else if (pc < vp * G) {
                 const int p = pc / G, tl = pc % G;
                 const int32_t sl = c.value_block_table[(int64_t)u * c.max_pages + p];
                 const uint8_t* slot = c.value_pool + (int64_t)sl * c.value_slot_bytes;
@@ -948,7 +978,8 @@ static cudaError_t prefill_t(const KittyCacheDesc& c, const T* keys, const T* va
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || kp + vp == 0) return e;
     if constexpr (sizeof(T) == 2) {
-        if (c.cfg.d == fastpack::kD && G == fastpack::kG && g_fast_pack && !c.key_meta && !c.value_meta) {
+        if (c.cfg.d == fastpack::kD && G == fastpack::kG && g_fast_pack && !c.key_meta && !c.value_meta &&
+            c.cfg.key_bits == 2 && c.cfg.value_bits == 2) {
             const int sm = static_cast<int>(sizeof(fastpack::Smem));
             if ((e = set_kernel_smem((const void*)prefill_pack_fast_kernel, sm)) != cudaSuccess) return e;
             prefill_pack_fast_kernel<<<dim3(kp + vp, units), fastpack::kThreads, sm, st>>>(c, keys, values, P, kp, vp);

@@ -78,7 +78,7 @@ def _cfg(**kw):
     (dict(key_bits=4), _lib.KITTY_ERR_CONFIG),
     (dict(value_bits=8), _lib.KITTY_ERR_CONFIG),
     (dict(d_boost=300, d=512), _lib.KITTY_ERR_CONFIG),
-    (dict(key_bits=16), _lib.KITTY_ERR_UNSUPPORTED),
+    (dict(key_bits=16), _lib.KITTY_OK),  # pass-through pages: generic kernels
 ])
 def test_validate_config_mirrors_reference(kw, code):
     # config.py:35-53 / test_cache.py:32-48

@@ -276,9 +276,36 @@ def test_amortization_bound(cuda):
     assert rep == cuda.memory_report(cfg, n)
 
 
-def test_passthrough_not_built_on_device(cuda):
-    with pytest.raises(cuda.KittyError):
-        cuda.KittyCacheState(cuda.KittyConfig(key_bits=16, value_bits=16, **SMALL))
+@pytest.mark.parametrize("bits", [(16, 16), (2, 16), (16, 2)])
+@pytest.mark.parametrize("row_dtype", ["f32", "bf16"])
+def test_passthrough_pages(cuda, bits, row_dtype):
+    # key_bits / value_bits 16 (cache.py:150-153,167-170): a full group becomes a
+    # page holding its rows as they are; order, attention and the pages against
+    # the dense reference over the same rows
+    rng = np.random.default_rng(sum(bits) + len(row_dtype))
+    cfg = cuda.KittyConfig(key_bits=bits[0], value_bits=bits[1], h_kv=2, h_q=4, **SMALL)
+    dt = torch.float32 if row_dtype == "f32" else torch.bfloat16
+    st = cuda.KittyCacheState(cfg, max_tokens=16, row_dtype=dt)
+    n = 45
+    k = _bf16(rng.normal(0, 1, (2, n, cfg.d)))
+    v = _bf16(rng.normal(0, 1, (2, n, cfg.d)))
+    st.prefill(k[:, :20], v[:, :20])
+    for t in range(20, n):
+        st.insert_token(k[:, t], v[:, t])
+    q = _bf16(rng.normal(0, 1, (cfg.h_q, cfg.d)))
+    for h in range(2):
+        kf, vf = st.flatten_keys(h), st.flatten_values(h)
+        if bits[0] == 16:
+            assert np.array_equal(kf, k[h])
+        if bits[1] == 16:
+            assert np.array_equal(vf, v[h])
+        pages = st.heads[h].key_pages if bits[0] == 16 else st.heads[h].value_pages
+        for i, pg in enumerate(pages):  # pass-through pages are the stored (g, d) rows
+            src = k[h] if bits[0] == 16 else v[h]
+            assert np.array_equal(pg, src[cfg.s + i * cfg.g: cfg.s + (i + 1) * cfg.g])
+    got = st.attend(q).outputs
+    want = np.stack([ko.attend_rows(st.flatten_keys(i // 2), st.flatten_values(i // 2), q[i:i + 1])[0] for i in range(4)])
+    assert _rel(got, want) <= 1e-5
 
 
 def test_dense_oracle_attend_on_device(cuda):

@@ -8,12 +8,7 @@ import pytest
 
 import paper_2511_18643_b200 as _kb
 
-OUT_OF_SCOPE = {
-    # 16-bit pass-through pages: a debug mode of the reference, not built on the device
-    "test_cache.py::test_prefill_equals_fold_of_inserts[16-": "pass-through (16-bit) pages are not built on the device",
-    "test_cache.py::test_passthrough_matches_dense_oracle": "pass-through (16-bit) pages are not built on the device",
-    "test_cache.py::test_order_reconstruction_fuzz": "uses pass-through (16-bit) pages, not built on the device",
-}
+OUT_OF_SCOPE = {}
 
 
 def pytest_configure(config):
