@@ -173,6 +173,19 @@ int kitty_dequant_value_pages(const uint8_t* slots, int64_t slot_stride, int32_t
                               int32_t g, int32_t d, const float* scales_f32,
                               const float* zeros_f32, float* out, void* stream);
 
+/* _quantize_columns / quantize_values (quant.py:102-132) of every lane of x
+ * [rows][cols] float32 (lanes = columns, or rows with per_token = 1) at
+ * bits[lane] in {2, 4} (device int32): codes [rows][cols] u8, scales / zeros
+ * [lanes] f32 (scale = (max - min) / (2^b - 1) in IEEE f32, zero = min, codes
+ * = clip(rint((x - min) / scale)), all-zero codes for a constant lane). */
+int kitty_quantize_lanes(const float* x, int32_t rows, int32_t cols, int32_t per_token, const int32_t* bits,
+                         uint8_t* codes, float* scales, float* zeros, void* stream);
+
+/* dequantize_values (quant.py:135-143): out = code * scale + zero per lane
+ * (multiply, then add). */
+int kitty_dequantize_lanes(const uint8_t* codes, int32_t rows, int32_t cols, int32_t per_token, const float* scales,
+                           const float* zeros, float* out, void* stream);
+
 /* fake_quantize_matrix (quant.py:145-177): x [rows][cols] float32; lanes are
  * columns (per_token = 0, "per_channel") or rows (per_token = 1); bits [lanes]
  * (device int32) in {2, 4, 16}, 16 passing the lane through; out like x. */

@@ -36,6 +36,7 @@ from .pages import (
     SENTINEL,
     BoostSelection,
     PageByteCounts,
+    QuantParams,
     QuantizedKeyPage,
     QuantizedValuePage,
     channel_scores,
@@ -45,12 +46,14 @@ from .pages import (
     dequantize_key_page,
     dequantize_value_page,
     deserialize_page,
+    dequantize_values,
     fake_quantize_matrix,
     pack_key_page,
     pack_key_pages,
     pack_value_page,
     pack_value_pages,
     page_byte_size,
+    quantize_values,
     select_boost,
     select_boost_batch,
     serialize_page,
@@ -72,5 +75,5 @@ __all__ = [
     "pack_key_page", "pack_key_pages", "pack_value_page", "pack_value_pages", "page_byte_size",
     "select_boost", "select_boost_batch", "serialize_page", "serialize_slot",
     "SensitivityReport", "SweepRow", "SyntheticSpec", "attention_mse", "boost_sweep", "boost_sweep_experiment",
-    "channel_sensitivity", "generate_synthetic",
+    "channel_sensitivity", "generate_synthetic", "QuantParams", "quantize_values", "dequantize_values",
 ]

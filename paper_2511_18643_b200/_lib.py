@@ -80,6 +80,10 @@ SIGNATURES = [
      [c_void_p, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("kitty_dequant_value_pages", ctypes.c_int,
      [c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("kitty_quantize_lanes", ctypes.c_int,
+     [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("kitty_dequantize_lanes", ctypes.c_int,
+     [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("kitty_fake_quantize", ctypes.c_int, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     ("kitty_append", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_void_p, c_void_p, c_void_p]),
     ("kitty_prefill", ctypes.c_int, [ctypes.POINTER(KittyCacheDesc), c_void_p, c_void_p, c_int32, c_void_p]),

@@ -109,3 +109,54 @@ def algorithmic_bytes_per_unit(cfg: KittyConfig, n: int) -> int:
     val = c["value_pages"] * page_byte_size("value", cfg).total
     fp = FP_BYTES * cfg.d * ((c["sink"] + c["key_qbuf"]) + (c["sink"] + c["local"] + c["value_qbuf"]))
     return key + val + fp + 2 * FP_BYTES * cfg.group_size * cfg.d
+
+
+# -- report rendering (analysis.py:377-444: host text formatting of the results) --
+
+PRNG_ID = "pcg64"  # tensor_io.py:37: the generator every seeded input comes from
+
+
+def report_header(command: str, seed, config_mapping: dict | None = None) -> list[str]:
+    """analysis.py:377-387: self-describing comment block."""
+    from . import __version__
+
+    lines = [f"# kittykv {__version__}", f"# command: {command}", f"# prng: {PRNG_ID}", f"# seed: {seed}"]
+    for key in sorted(config_mapping or {}):
+        lines.append(f"# {key} = {config_mapping[key]}")
+    return lines
+
+
+def _fmt(value) -> str:
+    return format(value, ".10g") if isinstance(value, float) else str(value)
+
+
+def write_csv(path, header_lines, columns, rows) -> None:
+    """analysis.py:396-402."""
+    with open(path, "w") as fh:
+        for line in header_lines:
+            fh.write(line + "\n")
+        fh.write(",".join(columns) + "\n")
+        for row in rows:
+            fh.write(",".join(_fmt(v) for v in row) + "\n")
+
+
+def sensitivity_csv_rows(report):
+    """analysis.py:405-412: one row per channel, one column per query head."""
+    h_q, d = report.mse.shape
+    columns = ["channel"] + [f"mse_qhead_{h}" for h in range(h_q)] + ["mean_mse"]
+    return columns, [[ch, *(float(report.mse[h, ch]) for h in range(h_q)), float(report.mean_mse[ch])] for ch in range(d)]
+
+
+def sweep_csv_rows(rows):
+    """analysis.py:415-419."""
+    return ["fraction", "heuristic", "mean_mse", "max_deviation", "runs"], [
+        [r.fraction, r.heuristic, r.mean_mse, r.max_deviation, r.runs] for r in rows]
+
+
+def memory_summary(report: MemoryReport) -> list[str]:
+    """analysis.py:422-444: ``key: value`` lines of a memory report."""
+    keys = ["length", "key_sink_bytes", "key_qbuffer_bytes", "key_page_count", "key_pages_payload",
+            "key_pages_metadata", "key_pages_index", "value_sink_bytes", "value_local_bytes", "value_qbuffer_bytes",
+            "value_page_count", "value_pages_payload", "value_pages_metadata", "total_bytes", "kv_data_bytes",
+            "baseline_bytes", "compression_ratio", "kv_data_ratio"]
+    return [f"{k}: {_fmt(getattr(report, k))}" for k in keys]

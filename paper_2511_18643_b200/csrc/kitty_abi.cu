@@ -150,6 +150,22 @@ int kitty_dequant_value_pages(const uint8_t* slots, int64_t slot_stride, int32_t
                                                          scales_f32, zeros_f32, out, as_stream(stream)));
 }
 
+int kitty_quantize_lanes(const float* x, int32_t rows, int32_t cols, int32_t per_token, const int32_t* bits,
+                         uint8_t* codes, float* scales, float* zeros, void* stream) {
+    Range nvtx_range("kitty_quantize_lanes");
+    if (rows < 0 || cols < 0) return invalid("quantize_values needs a 2-D matrix");
+    return cuda_status(kitty::launch_quantize_lanes(x, rows, cols, per_token, bits, codes, scales, zeros,
+                                                    as_stream(stream)));
+}
+
+int kitty_dequantize_lanes(const uint8_t* codes, int32_t rows, int32_t cols, int32_t per_token, const float* scales,
+                           const float* zeros, float* out, void* stream) {
+    Range nvtx_range("kitty_dequantize_lanes");
+    if (rows < 0 || cols < 0) return invalid("dequantize_values needs a 2-D matrix");
+    return cuda_status(kitty::launch_dequantize_lanes(codes, rows, cols, per_token, scales, zeros, out,
+                                                      as_stream(stream)));
+}
+
 int kitty_fake_quantize(const float* x, int32_t rows, int32_t cols, int32_t per_token, const int32_t* bits,
                         float* out, void* stream) {
     Range nvtx_range("kitty_fake_quantize");

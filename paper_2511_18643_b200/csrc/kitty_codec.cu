@@ -777,6 +777,66 @@ __global__ void fake_quantize_kernel(const float* x, int rows, int cols, int per
     }
 }
 
+// _quantize_columns / quantize_values (quant.py:102-132) for every lane of x
+// (columns for per_channel, rows for per_token): codes (u8, like x) and the
+// lane's f32 scale / zero point.  bits[lane] in {2, 4}.
+__global__ void quantize_lanes_kernel(const float* x, int rows, int cols, int per_token, const int32_t* bits,
+                                      uint8_t* codes, float* scales, float* zeros) {
+    const int lanes = per_token ? rows : cols, len = per_token ? cols : rows;
+    const int64_t step = per_token ? 1 : cols;
+    for (int lane = blockIdx.x * blockDim.x + threadIdx.x; lane < lanes; lane += gridDim.x * blockDim.x) {
+        const float* src = per_token ? x + (int64_t)lane * cols : x + lane;
+        uint8_t* dst = per_token ? codes + (int64_t)lane * cols : codes + lane;
+        float mn = src[0], mx = mn;
+        for (int i = 1; i < len; ++i) {
+            mn = fminf(mn, src[i * step]);
+            mx = fmaxf(mx, src[i * step]);
+        }
+        if (mn == 0.f || mx == 0.f) {  // a zero min / max carries the sign of the lane's last zero
+            float z = 0.f;
+            for (int i = len - 1; i >= 0; --i) {
+                if (src[i * step] == 0.f) {
+                    z = src[i * step];
+                    break;
+                }
+            }
+            mn = mn == 0.f ? z : mn;
+            mx = mx == 0.f ? z : mx;
+        }
+        const LaneQuant q(mn, mx, static_cast<float>((1 << bits[lane]) - 1));
+        for (int i = 0; i < len; ++i) dst[i * step] = static_cast<uint8_t>(q.code(src[i * step]));
+        scales[lane] = q.scale;
+        zeros[lane] = mn;
+    }
+}
+
+// dequantize_values (quant.py:135-143): code * scale + zero, multiply then add.
+__global__ void dequantize_lanes_kernel(const uint8_t* codes, int rows, int cols, int per_token, const float* scales,
+                                        const float* zeros, float* out) {
+    const int64_t n = (int64_t)rows * cols;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int lane = per_token ? static_cast<int>(i / cols) : static_cast<int>(i % cols);
+        out[i] = __fadd_rn(__fmul_rn(static_cast<float>(codes[i]), scales[lane]), zeros[lane]);
+    }
+}
+
+cudaError_t launch_quantize_lanes(const float* x, int rows, int cols, int per_token, const int32_t* bits,
+                                  uint8_t* codes, float* scales, float* zeros, cudaStream_t st) {
+    const int lanes = per_token ? rows : cols;
+    if (lanes == 0 || rows == 0 || cols == 0) return cudaSuccess;
+    quantize_lanes_kernel<<<(lanes + 127) / 128, 128, 0, st>>>(x, rows, cols, per_token, bits, codes, scales, zeros);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_lanes(const uint8_t* codes, int rows, int cols, int per_token, const float* scales,
+                                    const float* zeros, float* out, cudaStream_t st) {
+    const int64_t n = (int64_t)rows * cols;
+    if (n == 0) return cudaSuccess;
+    const int blocks = static_cast<int>(n / 256 + 1 < 4096 ? n / 256 + 1 : 4096);
+    dequantize_lanes_kernel<<<blocks, 256, 0, st>>>(codes, rows, cols, per_token, scales, zeros, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fake_quantize(const float* x, int rows, int cols, int per_token, const int32_t* bits, float* out,
                                  cudaStream_t st) {
     const int lanes = per_token ? rows : cols;

@@ -32,6 +32,10 @@ cudaError_t launch_dequant_key_pages(const uint8_t* slots, int64_t stride, int P
 cudaError_t launch_dequant_value_pages(const uint8_t* slots, int64_t stride, int P, int g, int d,
                                        const float* sc32, const float* ze32, float* out,
                                        cudaStream_t st);
+cudaError_t launch_quantize_lanes(const float* x, int rows, int cols, int per_token, const int32_t* bits,
+                                  uint8_t* codes, float* scales, float* zeros, cudaStream_t st);
+cudaError_t launch_dequantize_lanes(const uint8_t* codes, int rows, int cols, int per_token, const float* scales,
+                                    const float* zeros, float* out, cudaStream_t st);
 cudaError_t launch_fake_quantize(const float* x, int rows, int cols, int per_token, const int32_t* bits, float* out,
                                  cudaStream_t st);
 cudaError_t launch_append(const KittyCacheDesc& c, const void* k_new, const void* v_new, cudaStream_t st);

@@ -67,12 +67,14 @@ struct ValueLayout {
 // clip(rint((x - mn) / safe), 0, qmax), all-zero codes when scale == 0.
 struct LaneQuant {
     float mn, scale, safe, inv, qmax;
+    bool exact;  // the reciprocal is not usable (scale < 2^-100 or > 2^100): always divide
     __device__ __forceinline__ LaneQuant(float mn_, float mx_, float qmax_) {
         mn = mn_;
         qmax = qmax_;
         scale = __fdiv_rn(__fsub_rn(mx_, mn_), qmax_);
         safe = scale > 0.f ? scale : 1.0f;
         inv = __frcp_rn(safe);
+        exact = !(safe >= 0x1p-100f && safe <= 0x1p100f);
     }
     // rint of the IEEE quotient (x - mn) / safe.  x * rcp(safe) is within
     // ~2^-23 relative (< 2e-6 absolute for quotients <= 15) of it, so its
@@ -83,7 +85,7 @@ struct LaneQuant {
         const float dlt = __fsub_rn(x, mn);
         const float qa = __fmul_rn(dlt, inv);
         float r = rintf(qa);
-        if (fabsf(__fsub_rn(__fsub_rn(qa, floorf(qa)), 0.5f)) < 1.0e-5f) r = rintf(__fdiv_rn(dlt, safe));
+        if (exact || fabsf(__fsub_rn(__fsub_rn(qa, floorf(qa)), 0.5f)) < 1.0e-5f) r = rintf(__fdiv_rn(dlt, safe));
         r = fminf(fmaxf(r, 0.f), qmax);
         return static_cast<uint32_t>(r);
     }

@@ -263,6 +263,60 @@ def select_boost(scores, boost_fraction: float, heuristic: str = "magnitude", se
     raise KittyError(f"unknown selection heuristic {heuristic!r}")
 
 
+QUANT_BITS = (2, 4)
+
+
+@dataclass(frozen=True)
+class QuantParams:
+    """quant.py:31-37: scale / zero-point pair of one quantization group."""
+
+    bits: int
+    scale: float
+    zero_point: float
+
+
+def quantize_values(xs, bits: int):
+    """quant.py:123-132 on the device (kitty_quantize_lanes): one group at 2 or
+    4 bits -> (codes uint8, QuantParams)."""
+    if bits not in QUANT_BITS:
+        raise KittyError(f"bits must be one of {QUANT_BITS}, got {bits}")
+    xs = np.asarray(xs, dtype=np.float32)
+    if xs.ndim != 1 or xs.size == 0:
+        raise KittyError("quantize_values needs a non-empty 1-D sequence")
+    if not np.isfinite(xs).all():
+        raise KittyError("quantize_values input must be finite")
+    lib = _lib.load_library()
+    dev = _device()
+    xt = torch.from_numpy(np.ascontiguousarray(xs)).to(dev)
+    bt = torch.tensor([bits], dtype=torch.int32, device=dev)
+    codes = torch.empty(xs.size, dtype=torch.uint8, device=dev)
+    sz = torch.empty(2, dtype=torch.float32, device=dev)
+    _lib.check(lib.kitty_quantize_lanes(xt.data_ptr(), xs.size, 1, 0, bt.data_ptr(), codes.data_ptr(), sz.data_ptr(),
+                                        sz[1:].data_ptr(), _stream()), "quantize_values")
+    scale, zero = sz.cpu().numpy()
+    return codes.cpu().numpy(), QuantParams(bits=bits, scale=float(scale), zero_point=float(zero))
+
+
+def dequantize_values(codes, params: QuantParams) -> np.ndarray:
+    """quant.py:135-143 on the device (kitty_dequantize_lanes): code * scale + zero."""
+    codes = np.asarray(codes)
+    qmax = 2**params.bits - 1
+    if codes.size and (codes.min() < 0 or codes.max() > qmax):
+        raise KittyError(f"code outside [0, {qmax}]")
+    shape = codes.shape
+    flat = np.ascontiguousarray(codes.reshape(-1), dtype=np.uint8)
+    if flat.size == 0:
+        return np.zeros(shape, np.float32)
+    lib = _lib.load_library()
+    dev = _device()
+    ct = torch.from_numpy(flat).to(dev)
+    sz = torch.tensor([params.scale, params.zero_point], dtype=torch.float32, device=dev)
+    out = torch.empty(flat.size, dtype=torch.float32, device=dev)
+    _lib.check(lib.kitty_dequantize_lanes(ct.data_ptr(), flat.size, 1, 0, sz.data_ptr(), sz[1:].data_ptr(),
+                                          out.data_ptr(), _stream()), "dequantize_values")
+    return out.cpu().numpy().reshape(shape)
+
+
 def fake_quantize_matrix(x, axis: str, bits_per_lane) -> np.ndarray:
     """quant.py:145-177 on the device (kitty_fake_quantize): quantize-then-
     dequantize every lane of ``x`` -- a column for ``per_channel``, a row for

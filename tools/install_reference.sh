@@ -8,4 +8,5 @@ rm -rf /tmp/kittykv_src && cp -r /root/reference/pkg /tmp/kittykv_src
 python -m pip install --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
     --target baseline/_ref --upgrade /tmp/kittykv_src
 rm -rf baseline/_ref_tests && mkdir -p baseline/_ref_tests && cp /root/reference/pkg/tests/test_pages.py \
-    /root/reference/pkg/tests/test_cache.py baseline/_ref_tests/
+    /root/reference/pkg/tests/test_cache.py /root/reference/pkg/tests/test_quant.py \
+    /root/reference/pkg/tests/test_analysis.py baseline/_ref_tests/
