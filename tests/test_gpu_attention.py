@@ -167,3 +167,25 @@ def test_length_bound_is_reported(cuda, d):
     cache.check()  # cleared
     cache.attend(q)
     cache.check()
+
+
+@pytest.mark.parametrize("vscale", [100.0, 3000.0])
+def test_large_value_magnitudes(cuda, vscale):
+    # f16 operands carry p * s (s = a value page's per-token scale): large
+    # values must not overflow them (the lazy softmax keeps p <= 4)
+    rng = np.random.default_rng(int(vscale))
+    b, h_kv, group, n = 1, 2, 4, 2000
+    cfg = cuda.KittyConfig(h_kv=h_kv, h_q=h_kv * group)
+    k = _keys(rng, (b, h_kv, n, 128))
+    v = _bf16(rng.normal(0, vscale, (b, h_kv, n, 128)))
+    cache = cuda.KittyBatchCache(cfg, b, n)
+    cache.prefill(torch.from_numpy(k), torch.from_numpy(v))
+    q = _bf16(rng.normal(0, 1, (b, h_kv * group, 128)))
+    out = cache.attend(torch.from_numpy(q).cuda(), out_dtype=torch.float32).cpu().numpy()
+    cache.check()
+    assert np.isfinite(out).all()
+    for h in range(h_kv):
+        kf, vf, _, _ = ko.bulk_unit_state(k[0, h], v[0, h], 32, 128, 128, 0.125, metadata16=True)
+        want = ko.attend_rows(kf, vf, q[0, h * group:(h + 1) * group])
+        got = out[0, h * group:(h + 1) * group]
+        assert np.max(np.abs(got - want)) <= 2e-3 * np.max(np.abs(want)) + 1e-2, h
