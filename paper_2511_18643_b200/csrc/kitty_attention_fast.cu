@@ -209,14 +209,67 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
 struct Consts {
     uint32_t m0, m1, m2, m3, magic;
     __device__ __forceinline__ Consts() {
-        m0 = 0x03000300u;  // code 0 of the byte, from its copy in bits 8-15: weight 256
-        m1 = 0x000C000Cu;  // code 1, bits 2-3: weight 4
-        m2 = 0x00300030u;  // code 2, bits 4-5: weight 16
-        m3 = 0x00C000C0u;  // code 3, bits 6-7: weight 64
+        m0 = 0x03000300u;  // bits 8-9 of each half: weight 256
+        m1 = 0x000C000Cu;  // bits 2-3: weight 4
+        m2 = 0x00300030u;  // bits 4-5: weight 16
+        m3 = 0x00C000C0u;  // bits 6-7: weight 64
         magic = kMagic;
         asm volatile("" : "+r"(m0), "+r"(m1), "+r"(m2), "+r"(m3), "+r"(magic));
     }
 };
+
+// ldmatrix.x4.trans of four 8 x 16-byte blocks of 32-byte code rows: lane
+// (gid, tig) gets, per block, rows 2 tig / 2 tig + 1 (the two f16 halves) at
+// bytes 2 gid, 2 gid + 1, i.e. 8 consecutive 2-bit codes of two rows in one
+// register -- the A-operand pairing the MMA wants, without a PRMT.
+__device__ __forceinline__ void ldsm_t4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+// One register of 8 codes per half -> the 8 f16x2 A operands of its codes:
+// codes 1-4 masked in place (weights 4, 16, 64, 256), code 0 after a 2-bit
+// left shift (4) and codes 5-7 after a 6-bit right shift (16, 64, 256); each
+// OR-ed with the exponent of 1024.  No code sits at weight 1: w >= 4 keeps
+// the 1024 offset's cancellation (removed per row after the MMA) far below
+// the fp16 operand rounding.
+__device__ __forceinline__ void conv8(const Consts& k, uint32_t r, uint32_t (&o)[8]) {
+    o[0] = and_or(r << 2, k.m1, k.magic);
+    o[1] = and_or(r, k.m1, k.magic);
+    o[2] = and_or(r, k.m2, k.magic);
+    o[3] = and_or(r, k.m3, k.magic);
+    o[4] = and_or(r, k.m0, k.magic);
+    const uint32_t y = r >> 6;
+    o[5] = and_or(y, k.m2, k.magic);
+    o[6] = and_or(y, k.m3, k.magic);
+    o[7] = and_or(y, k.m0, k.magic);
+}
+
+// weight class of tile m (the code position inside the lane's 8): 0: w 4,
+// 1: w 16, 2: w 64, 3: w 256
+__host__ __device__ constexpr int tile_c(int m) { return m < 2 ? 0 : (m < 5 ? m - 1 : m - 4); }
+__host__ __device__ constexpr float tile_w(int m) { return tile_c(m) == 0 ? 4.f : tile_c(m) == 1 ? 16.f : tile_c(m) == 2 ? 64.f : 256.f; }
+
+// acc[8][4] (+)= A x B for one k-step from the four ldmatrix registers:
+// r0 / r2 = rows (2 tig, 2 tig + 1) of the step at M-rows gid / gid + 8,
+// r1 / r3 = rows (2 tig + 8, 2 tig + 9); tile m = code m of each register.
+template <bool FIRST = false>
+__device__ __forceinline__ void mma_ldsm(const Consts& k, float (&acc)[8][4], uint32_t r0, uint32_t r1, uint32_t r2,
+                                         uint32_t r3, uint32_t b0, uint32_t b1) {
+    uint32_t a0[8], a1[8], a2[8], a3[8];
+    conv8(k, r0, a0);
+    conv8(k, r2, a1);
+    conv8(k, r1, a2);
+    conv8(k, r3, a3);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        if (FIRST)
+            mma16816_z(acc[m], a0[m], a1[m], a2[m], a3[m], b0, b1);
+        else
+            mma16816(acc[m], a0[m], a1[m], a2[m], a3[m], b0, b1);
+    }
+}
 
 // Byte b of two rows -> the fp16x2 A operands of its 4 codes: one PRMT puts
 // byte b of w0 in bytes 0 and 1 and byte b of w1 in bytes 2 and 3, then one
@@ -490,25 +543,27 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
     struct QkRegs {
         float acc[8][4], aux[4], aux2[4];
     };
+    // ldmatrix row address of this lane inside a 16-row block of 32-byte code
+    // rows: block mi = lane / 8 covers rows 8 (mi & 1) + [0, 8) at bytes 16 (mi >> 1)
+    const uint32_t ldsm_off = (8 * ((lane >> 3) & 1) + (lane & 7)) * 32 + 16 * (lane >> 4);
     auto qk_step = [&](int st, int ks, QkRegs& r) {
         const uint8_t* kp = kslots + st * kslot;
-        const uint32_t* kw = reinterpret_cast<const uint32_t*>(kp);
         // aux lanes (B columns 4-7) read their "scale" from the ones buffer
         const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
         const int c0 = 16 * ks + 2 * tig;
         const uint32_t b0 = hmul2(qa[ks][0], lds32(sbase + 2 * c0));
         const uint32_t b1 = hmul2(qa[ks][1], lds32(sbase + 2 * (c0 + 8)));
-        const uint32_t w0 = kw[8 * c0 + gid], w1 = kw[8 * (c0 + 1) + gid];
-        const uint32_t w2 = kw[8 * (c0 + 8) + gid], w3 = kw[8 * (c0 + 9) + gid];
+        uint32_t w0, w1, w2, w3;  // channel rows 16 ks + [0, 16), tokens 8 gid + [0, 8) / 64 + ...
+        ldsm_t4(smem_u32(kp) + 512 * ks + ldsm_off, w0, w1, w2, w3);
         // aux tile: only rows 0 (ones) and 8 (zero points) are read back
         const uint32_t z0 = lds32(kp + zero_off + 2 * c0);
         const uint32_t z1 = lds32(kp + zero_off + 2 * (c0 + 8));
         if (ks == 0) {
-            mma_codes<true>(kc, r.acc, w0, w1, w2, w3, b0, b1);
+            mma_ldsm<true>(kc, r.acc, w0, w1, w2, w3, b0, b1);
             mma16816_z(r.aux, kOnes, z0, kOnes, z1, b0, b1);
             if (kFull) mma16816_z(r.aux2, kOnes, z0, kOnes, z1, qa[ks][0], qa[ks][1]);
         } else {
-            mma_codes(kc, r.acc, w0, w1, w2, w3, b0, b1);
+            mma_ldsm(kc, r.acc, w0, w1, w2, w3, b0, b1);
             mma16816(r.aux, kOnes, z0, kOnes, z1, b0, b1);
             if (kFull) mma16816(r.aux2, kOnes, z0, kOnes, z1, qa[ks][0], qa[ks][1]);
         }
@@ -539,34 +594,32 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
                 const uint32_t m1 = (ok && j0 + 8 < d_boost ? 0xffffu : 0u) | (ok && j0 + 9 < d_boost ? 0xffff0000u : 0u);
                 const uint32_t b0 = hmul2(q01, s01) & m0;
                 const uint32_t b1 = hmul2(q89, s89) & m1;
-                const uint32_t* hw = reinterpret_cast<const uint32_t*>(kp + D * G / 4);
-                mma_codes(kc, acc, hw[8 * j0 + gid], hw[8 * (j0 + 1) + gid], hw[8 * (j0 + 8) + gid],
-                          hw[8 * (j0 + 9) + gid], b0, b1);
+                uint32_t h0, h1, h2, h3;  // high-bit rows 16 hk + [0, 16)
+                ldsm_t4(smem_u32(kp + D * G / 4) + 512 * hk + ldsm_off, h0, h1, h2, h3);
+                mma_ldsm(kc, acc, h0, h1, h2, h3, b0, b1);
                 mma16816(aux, kOnes, 0u, kOnes, 0u, b0, b1);
             }
         }
         // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha).
-        // Row weights: even tiles hold codes 0 / 1 of a byte (w 256 / 4), odd tiles 2 / 3 (w 16 / 64).
+        // Tile m holds code m of the lane's 8 (rows gid: token 8 gid + m, gid + 8:
+        // token 64 + 8 gid + m) at weight tile_w(m); bw[c] = the offset of class c.
         float bw[4][2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const float sumB = __shfl_sync(0xffffffffu, aux[j], kFull ? tig : (tig & 1));
             const float cst = kFull ? __shfl_sync(0xffffffffu, aux2[2 + j], tig)
                                     : __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
-            bw[0][j] = cst - 4.f * sumB;    // w 256
-            bw[1][j] = cst - 256.f * sumB;  // w 4
-            bw[2][j] = cst - 64.f * sumB;   // w 16
-            bw[3][j] = cst - 16.f * sumB;   // w 64
-            float x0 = acc[0][j], x1 = acc[0][2 + j], x2 = acc[1][j], x3 = acc[1][2 + j];
-#pragma unroll
-            for (int m = 2; m < 8; m += 2) {
-                x0 = fmaxf(x0, acc[m][j]);
-                x1 = fmaxf(x1, acc[m][2 + j]);
-                x2 = fmaxf(x2, acc[m + 1][j]);
-                x3 = fmaxf(x3, acc[m + 1][2 + j]);
-            }
-            float pm = fmaxf(fmaxf(fmaf(x0, 1.f / 256.f, bw[0][j]), fmaf(x1, 1.f / 4.f, bw[1][j])),
-                             fmaxf(fmaf(x2, 1.f / 16.f, bw[2][j]), fmaf(x3, 1.f / 64.f, bw[3][j])));
+            bw[0][j] = cst - 256.f * sumB;  // w 4
+            bw[1][j] = cst - 64.f * sumB;   // w 16
+            bw[2][j] = cst - 16.f * sumB;   // w 64
+            bw[3][j] = cst - 4.f * sumB;    // w 256
+            // raw maxima per weight class (same weight: monotone), then one FFMA each
+            const float x0 = fmaxf(fmaxf(acc[0][j], acc[0][2 + j]), fmaxf(acc[1][j], acc[1][2 + j]));
+            const float x1 = fmaxf(fmaxf(acc[2][j], acc[2][2 + j]), fmaxf(acc[5][j], acc[5][2 + j]));
+            const float x2 = fmaxf(fmaxf(acc[3][j], acc[3][2 + j]), fmaxf(acc[6][j], acc[6][2 + j]));
+            const float x3 = fmaxf(fmaxf(acc[4][j], acc[4][2 + j]), fmaxf(acc[7][j], acc[7][2 + j]));
+            float pm = fmaxf(fmaxf(fmaf(x0, 1.f / 4.f, bw[0][j]), fmaf(x1, 1.f / 16.f, bw[1][j])),
+                             fmaxf(fmaf(x2, 1.f / 64.f, bw[2][j]), fmaf(x3, 1.f / 256.f, bw[3][j])));
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 4));
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 8));
             pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 16));
@@ -579,24 +632,25 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) bw[c4][j] -= mnew[j];
         }
-        // probabilities (log2 domain), two tokens per f16x2 ex2, to P^T[st]:
-        // row = query, tokens 16 gid + 2m (+1) at word 8 gid + m
+        // probabilities (log2 domain) to P^T[st]: row = query, token t at word
+        // t / 2 (half t % 2); this lane's tokens 8 gid + m (words 4 gid ..) and
+        // 64 + 8 gid + m (words 32 + 4 gid ..), two 16-byte stores each
         if (kFull || tig < 2) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 if (2 * tig + j < GROUP) {
-                    uint32_t pw[8];
+                    uint32_t lo[4], hi[4];
 #pragma unroll
-                    for (int m = 0; m < 8; ++m) {
-                        const float wlo = (m & 1) ? 1.f / 16.f : 1.f / 256.f, whi = (m & 1) ? 1.f / 64.f : 1.f / 4.f;
-                        const int clo = (m & 1) ? 2 : 0, chi = (m & 1) ? 3 : 1;
-                        // two f32 ex2 + one pack: fewer instructions than ex2.f16x2 (3 on sm_100)
-                        pw[m] = pack_f16x2(ex2(fmaf(acc[m][j], wlo, bw[clo][j])), ex2(fmaf(acc[m][2 + j], whi, bw[chi][j])));
+                    for (int m = 0; m < 8; m += 2) {
+                        const float w0 = 1.f / tile_w(m), w1 = 1.f / tile_w(m + 1);
+                        const int c0 = tile_c(m), c1 = tile_c(m + 1);
+                        lo[m / 2] = pack_f16x2(ex2(fmaf(acc[m][j], w0, bw[c0][j])), ex2(fmaf(acc[m + 1][j], w1, bw[c1][j])));
+                        hi[m / 2] = pack_f16x2(ex2(fmaf(acc[m][2 + j], w0, bw[c0][j])),
+                                               ex2(fmaf(acc[m + 1][2 + j], w1, bw[c1][j])));
                     }
-                    // the row's 8 words are contiguous: two 16-byte stores
-                    uint4* row = reinterpret_cast<uint4*>(&sm.pt[st][(2 * tig + j) % PT_ROWS][8 * gid]);
-                    row[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-                    row[1] = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+                    uint32_t* row = &sm.pt[st][(2 * tig + j) % PT_ROWS][0];
+                    *reinterpret_cast<uint4*>(row + 4 * gid) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                    *reinterpret_cast<uint4*>(row + 32 + 4 * gid) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                 }
             }
         }
@@ -624,7 +678,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
     };
     auto pv_step = [&](int st, int ks, PvRegs& r) {
         const uint8_t* vp = vslots + st * vslot;
-        const uint32_t* vw = reinterpret_cast<const uint32_t*>(vp);
         const uint8_t* vscale = vp + G * D / 4;
         const uint8_t* vzero = vscale + 2 * G;
         const uint8_t* vsbase = main_col ? vscale : reinterpret_cast<const uint8_t*>(sm.ones);
@@ -634,11 +687,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
         const uint32_t pp1 = prow_ok ? ptr[8 * ks + 4] : 0u;  // tokens 16 ks + 8 + 2 tig (+1)
         const uint32_t b0 = hmul2(pp0, lds32(vsbase + 2 * t0));
         const uint32_t b1 = hmul2(pp1, lds32(vsbase + 2 * (t0 + 8)));
-        const uint32_t w0 = vw[8 * t0 + gid], w1 = vw[8 * (t0 + 1) + gid];
-        const uint32_t w2 = vw[8 * (t0 + 8) + gid], w3 = vw[8 * (t0 + 9) + gid];
+        uint32_t w0, w1, w2, w3;  // token rows 16 ks + [0, 16), channels 8 gid + [0, 8) / 64 + ...
+        ldsm_t4(smem_u32(vp) + 512 * ks + ldsm_off, w0, w1, w2, w3);
         const uint32_t z0 = lds32(vzero + 2 * t0);
         const uint32_t z1 = lds32(vzero + 2 * (t0 + 8));
-        mma_codes(kc, oacc, w0, w1, w2, w3, b0, b1);
+        mma_ldsm(kc, oacc, w0, w1, w2, w3, b0, b1);
         if (ks == 0)
             mma16816_z(r.vaux, kOnes, z0, kOnes, z1, b0, b1);
         else
@@ -662,10 +715,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
                                    : __shfl_sync(0xffffffffu, r.vaux[2 + j], 2 + (tig & 1));
             const float cf = fresh ? 0.f : corr[j];
             ol[j] = fmaf(ol[j], cf, lp);
-            ob[0][j] = fmaf(ob[0][j], cf, zz - 4.f * sBv);
-            ob[1][j] = fmaf(ob[1][j], cf, zz - 256.f * sBv);
-            ob[2][j] = fmaf(ob[2][j], cf, zz - 64.f * sBv);
-            ob[3][j] = fmaf(ob[3][j], cf, zz - 16.f * sBv);
+            ob[0][j] = fmaf(ob[0][j], cf, zz - 256.f * sBv);  // w 4
+            ob[1][j] = fmaf(ob[1][j], cf, zz - 64.f * sBv);   // w 16
+            ob[2][j] = fmaf(ob[2][j], cf, zz - 16.f * sBv);   // w 64
+            ob[3][j] = fmaf(ob[3][j], cf, zz - 4.f * sBv);    // w 256
         }
     };
     auto flush = [&](const Pg& d, const float (&mnew)[2]) {
@@ -675,11 +728,19 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
             for (int j = 0; j < 2; ++j) {
                 const int g = 2 * tig + j;
                 if (g < GROUP) {
+                    // tile m: row gid = channel 8 gid + m, row gid + 8 = channel 64 + 8 gid + m
+                    float lo[8], hi[8];
 #pragma unroll
-                    for (int m = 0; m < 8; ++m)
-                        *reinterpret_cast<float2*>(base + g * D + 16 * gid + 2 * m) =
-                            make_float2(fmaf(oacc[m][j], (m & 1) ? 1.f / 16.f : 1.f / 256.f, ob[(m & 1) ? 2 : 0][j]),
-                                        fmaf(oacc[m][2 + j], (m & 1) ? 1.f / 64.f : 1.f / 4.f, ob[(m & 1) ? 3 : 1][j]));
+                    for (int m = 0; m < 8; ++m) {
+                        lo[m] = fmaf(oacc[m][j], 1.f / tile_w(m), ob[tile_c(m)][j]);
+                        hi[m] = fmaf(oacc[m][2 + j], 1.f / tile_w(m), ob[tile_c(m)][j]);
+                    }
+                    float4* o4 = reinterpret_cast<float4*>(base + g * D + 8 * gid);
+                    o4[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                    o4[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
+                    float4* h4 = reinterpret_cast<float4*>(base + g * D + 64 + 8 * gid);
+                    h4[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                    h4[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
                     if (gid == 0) *reinterpret_cast<float2*>(base + GROUP * D + 2 * g) = make_float2(mnew[j], ol[j]);
                 }
             }
