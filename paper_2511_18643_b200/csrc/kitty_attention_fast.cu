@@ -15,9 +15,10 @@
 //    rings (cp.async.bulk + mbarrier; keys are issued one page ahead of
 //    values) and runs QK^T + online softmax of page k + 1 interleaved with
 //    P V of page k in one basic block;
-//  * 2-bit codes become fp16 MMA operands with one PRMT (pair two channel /
-//    token rows) plus one LOP3 per 2 codes: (x & mask) | 0x6400 = 1024 + w c;
-//    the 1024 offset and w are removed per row after the MMA;
+//  * 2-bit codes become fp16 MMA operands without per-element dequantisation:
+//    ldmatrix.x4.trans hands each lane 8 codes of two code rows per register,
+//    one LOP3 per code position makes (x & mask) | 0x6400 = 1024 + w c; the
+//    1024 offset and w are removed per tile after the MMA;
 //  * per-channel key scale folded into q (B = q alpha s, fp16), per-token
 //    value scale into p (B = p s); zero points and offset sums come out of one
 //    auxiliary MMA tile (row 0 = ones, row 8 = zeros) whose B columns 4-7
@@ -268,50 +269,6 @@ __device__ __forceinline__ void mma_ldsm(const Consts& k, float (&acc)[8][4], ui
             mma16816_z(acc[m], a0[m], a1[m], a2[m], a3[m], b0, b1);
         else
             mma16816(acc[m], a0[m], a1[m], a2[m], a3[m], b0, b1);
-    }
-}
-
-// Byte b of two rows -> the fp16x2 A operands of its 4 codes: one PRMT puts
-// byte b of w0 in bytes 0 and 1 and byte b of w1 in bytes 2 and 3, then one
-// LOP3 per code keeps that code's two bits inside the mantissa and ORs the
-// exponent of 1024: f16 = 1024 + w * code with w = 256 / 4 / 16 / 64 for
-// codes 0 / 1 / 2 / 3 (the weight and the 1024 are removed per row after the
-// MMA; w >= 4 keeps the offset cancellation far below fp16 operand rounding).
-template <int B>
-__device__ __forceinline__ void conv_byte(const Consts& k, uint32_t w0, uint32_t w1, uint32_t& c0,
-                                          uint32_t& c1, uint32_t& c2, uint32_t& c3) {
-    constexpr uint32_t sel = B | (B << 4) | ((4 + B) << 8) | ((4 + B) << 12);
-    const uint32_t x = prmt(w0, w1, sel);
-    c0 = and_or(x, k.m0, k.magic);
-    c1 = and_or(x, k.m1, k.magic);
-    c2 = and_or(x, k.m2, k.magic);
-    c3 = and_or(x, k.m3, k.magic);
-}
-
-// acc[8][4] += A(2-bit codes of rows r0..r3, word gid) x B for one k-step.
-// rows = (w0, w1) pair P0 and (w2, w3) pair P1.  Tile 2b + h holds codes
-// 2h / 2h + 1 of byte b (rows gid / gid + 8): weights 256, 4 (h = 0) and
-// 16, 64 (h = 1).
-template <bool FIRST = false>
-__device__ __forceinline__ void mma_codes(const Consts& k, float (&acc)[8][4], uint32_t w0, uint32_t w1,
-                                          uint32_t w2, uint32_t w3, uint32_t b0, uint32_t b1) {
-    // all 8 tiles' A fragments first (32 registers): distinct registers let the
-    // HMMAs issue back to back instead of waiting on operand-read WAR hazards
-    uint32_t a[8][4];
-    conv_byte<0>(k, w0, w1, a[0][0], a[0][1], a[1][0], a[1][1]);
-    conv_byte<0>(k, w2, w3, a[0][2], a[0][3], a[1][2], a[1][3]);
-    conv_byte<1>(k, w0, w1, a[2][0], a[2][1], a[3][0], a[3][1]);
-    conv_byte<1>(k, w2, w3, a[2][2], a[2][3], a[3][2], a[3][3]);
-    conv_byte<2>(k, w0, w1, a[4][0], a[4][1], a[5][0], a[5][1]);
-    conv_byte<2>(k, w2, w3, a[4][2], a[4][3], a[5][2], a[5][3]);
-    conv_byte<3>(k, w0, w1, a[6][0], a[6][1], a[7][0], a[7][1]);
-    conv_byte<3>(k, w2, w3, a[6][2], a[6][3], a[7][2], a[7][3]);
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-        if (FIRST)
-            mma16816_z(acc[m], a[m][0], a[m][1], a[m][2], a[m][3], b0, b1);
-        else
-            mma16816(acc[m], a[m][0], a[m][1], a[m][2], a[m][3], b0, b1);
     }
 }
 
