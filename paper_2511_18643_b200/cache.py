@@ -166,10 +166,16 @@ class KittyBatchCache:
         self.desc = d
         self._desc_ref = ctypes.byref(d)
 
+    def _check_movable(self):
+        if getattr(self, "captured", False):
+            raise KittyError("this cache is referenced by a captured CUDA graph: its buffers cannot be "
+                             "reallocated (size it for the whole decode before capturing)")
+
     def grow(self, max_tokens: int):
         """Longer sequences: widen the block tables (int32 per page; slots and
         rows stay where they are).  An auto-sized pool also gains the slots the
         new length needs -- the one path that copies page bytes."""
+        self._check_movable()
         old_mp = self.max_pages
         self.max_tokens = int(max_tokens)
         self.max_pages = self._pages_for(self.max_tokens)
@@ -185,6 +191,7 @@ class KittyBatchCache:
         self._ws = None
 
     def _grow_pool(self, slots: int):
+        self._check_movable()
         old = dict(kp=self.key_pool, vp=self.value_pool, kf=self.key_free, vf=self.value_free,
                    km=self.key_meta, vm=self.value_meta, n=self.pool_pages, free=list(self.free_pages))
         self._alloc_pool(slots)

@@ -111,6 +111,8 @@ class DecodeStep:
                 self._launch()
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g
+        for cache in self.layers:  # the graph holds their buffer addresses from now on
+            cache.captured = True
         return g
 
     def attention_only(self, layer: int):
