@@ -416,10 +416,13 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
         d.p = ip;
         d.pq = ip1 | (ip0 << 16);
         d.slot = islot;
-        d.ks = __shfl_sync(0xffffffffu, kreg, (ip - ip0) & 31);
-        d.vs = __shfl_sync(0xffffffffu, vreg, (ip - ip0) & 31);
         return d;
     };
+    // a page's key / value slots: shuffled from its item's block-table loads
+    // as late as possible (before the stream decodes another item), so the
+    // loads issued at the item's decode are not waited on
+    auto fill_ks = [&](Pg& d) { d.ks = __shfl_sync(0xffffffffu, kreg, (d.p - (d.pq >> 16)) & 31); };
+    auto fill_vs = [&](Pg& d) { d.vs = __shfl_sync(0xffffffffu, vreg, (d.p - (d.pq >> 16)) & 31); };
     // Page p of the warp's stream lands in key slot p & 1 and value slot p & 1
     // (use number p >> 1 of the slot: mbarrier phase (p >> 1) & 1).  QK runs
     // one page ahead of PV, so a key page is issued one page earlier than its
@@ -706,9 +709,15 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
 
     // ---- software pipeline: QK of page k + 1 beside PV of page k ----
     Pg d0 = next_page();
+    fill_ks(d0);
+    fill_vs(d0);
     if (d0.u >= 0) {
         Pg d1 = next_page();
+        fill_ks(d1);
+        fill_vs(d1);
         Pg d2 = next_page();
+        fill_ks(d2);
+        fill_vs(d2);
         issue_key(d0, 0);
         issue_val(d0, 0);
         issue_key(d1, 1);
@@ -732,6 +741,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
         for (; d1.u >= 0; ++k) {
             const int st = k & 1;
             const bool fresh0 = d0.p == (d0.pq >> 16), last0 = d0.p + 1 == (d0.pq & 0xffff);
+            fill_vs(d2);          // before the stream may move to another item
             Pg d3 = next_page();  // page k + 3: its key goes into key slot st ^ 1 after QK(k + 1)
             prefetch_q(d3, d2.u);
             float corr1[2], mnew1[2];
@@ -749,6 +759,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
             qk_tail(st ^ 1, qr, corr1, mnew1);
             if (last0) flush(d0, mnew0);
             __syncwarp();
+            fill_ks(d3);
             issue_val(d2, st);     // value slot st (page k) -> page k + 2
             issue_key(d3, st ^ 1);  // key slot st ^ 1 (page k + 1) -> page k + 3
             d0 = d1;
