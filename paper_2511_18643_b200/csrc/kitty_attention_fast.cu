@@ -102,6 +102,7 @@ struct Params {
     uint32_t units_mul, units_shift;  // fast division by units (quotient = (umulhi(n, mul) + n) >> shift)
     int* ctr;   // [0] next item, [1] finished CTAs
     float* part;
+    int fp_first;  // launch order: fp grid, page grid, merge (else page, fp, merge)
 };
 
 // ---- small PTX helpers --------------------------------------------------------
@@ -346,15 +347,20 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
     sm.ones[lane + 32] = kOnes;
     sm.inv[lane] = 0;
     // launched as a programmatic dependent of the preceding kernel (the append):
-    // the prologue above overlaps its tail; nothing of the cache is read before this
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    // the fp-token grid (our programmatic dependent) may be scheduled from now on
-    asm volatile("griddepcontrol.launch_dependents;");
+    // the prologue above overlaps its tail; nothing of the cache is read before this.
+    // fp-first order: the preceding kernel is the fp grid, whose CTAs all passed
+    // their own wait on the append before this grid could launch -- the cache is
+    // final, and the fp grid is waited for at the end (before the merge reads it)
+    if (!P.fp_first) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        // the fp-token grid (our programmatic dependent) may be scheduled from now on
+        asm volatile("griddepcontrol.launch_dependents;");
+    }
     // per-CTA copy of the unit lengths: an item's decode reads shared memory
     int* s_ulen = reinterpret_cast<int*>(smem_raw + wbytes * kWarps);
     const bool len_table = P.units <= kMaxTableUnits;
     if (len_table) {
-        for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = min(c.unit_len[i], P.max_tokens);
+        for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = min(__ldcg(c.unit_len + i), P.max_tokens);
     }
     __syncthreads();
 
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
                 const int ch = static_cast<int>(
                     (__umulhi(static_cast<uint32_t>(idx), P.units_mul) + static_cast<uint32_t>(idx)) >> P.units_shift);
                 iu = idx - ch * P.units;
-                const int n = len_table ? s_ulen[iu] : min(c.unit_len[iu], P.max_tokens);
+                const int n = len_table ? s_ulen[iu] : min(__ldcg(c.unit_len + iu), P.max_tokens);
                 const int past = n > c.cfg.s ? n - c.cfg.s : 0;
                 const int vp = (past - min(c.cfg.r, past)) / G;
                 const int lb = level_begin(sect, vp, P.lvl), le = level_begin(sect + 1, vp, P.lvl);
@@ -402,8 +408,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
                     islot = P.fmax + islot;
                     const int64_t row = (int64_t)iu * c.max_pages + ip0;
                     if (lane < ip1 - ip0) {
-                        kreg = c.key_block_table[row + lane];
-                        vreg = c.value_block_table[row + lane];
+                        kreg = __ldcg(c.key_block_table + row + lane);
+                        vreg = __ldcg(c.value_block_table + row + lane);
                     }
                 }
             }
@@ -782,6 +788,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
             flush(d0, mnew0);  // a stream's last page is its item's last
         }
     }
+    if (P.fp_first) asm volatile("griddepcontrol.wait;" ::: "memory");  // the fp grid is complete
     // the last warp out resets the work queue for the next launch (after its
     // outstanding ticket returned: using its value orders the atomics)
     if (lane == 0) {
@@ -795,19 +802,27 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
 }
 
 // The full-precision tokens: one 128-thread CTA per 32-token chunk
-// (kitty_fp.cuh), launched as a programmatic dependent of the page grid so its
-// CTAs fill the shared memory the page CTAs leave free and backfill SMs as
-// persistent page CTAs retire.
+// (kitty_fp.cuh).  Default order: launched first, as a programmatic dependent
+// of the append; the page grid follows as its dependent, so the persistent
+// page CTAs take over each SM as its fp CTAs drain and the elastic page queue
+// absorbs the staggered start (C2 -1.0, C3 -2.8 us per layer against the
+// page-first order, where the fp CTAs backfilled the page grid's tail).
 template <int GROUP>
 __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
     extern __shared__ __align__(128) uint8_t fsm[];
     const int it = blockIdx.x;
     const int fc = it / P.units, u = it - fc * P.units;
+    if (P.fp_first) {
+        // behind the append: wait for it, then let the page grid launch
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;");
+    } else {
+        asm volatile("griddepcontrol.launch_dependents;");  // the merge may pre-launch
+    }
     const fptok::Geom gm = fptok::geom(P.c, u, P.max_tokens);
-    asm volatile("griddepcontrol.launch_dependents;");  // the merge may pre-launch
     if (gm.n > 0 && fc * kFpChunk < gm.nfp) fptok::chunk_tc<GROUP>(P.c, P.q, P.part, P.nslot, part_stride(GROUP), fsm, u, fc, P.max_tokens);
     // launched as a programmatic dependent of the page grid: finish only after it
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!P.fp_first) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // K5: WARPS warps merge one (unit, query row): 2 when a unit has <= 32 partial
@@ -965,6 +980,12 @@ static const int g_pdl = [] {
     return e ? std::atoi(e) : 3;
 }();
 
+// launch order (A/B knob KITTY_FPFIRST): 1 = fp grid, page grid, merge
+static const int g_fp_first = [] {
+    const char* e = std::getenv("KITTY_FPFIRST");
+    return e ? std::atoi(e) : 1;
+}();
+
 template <int GROUP, int NKH>
 static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     auto kfn = page_kernel<GROUP, NKH>;
@@ -984,29 +1005,35 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
         at[i].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[i].val.programmaticStreamSerializationAllowed = (g_pdl >> i) & 1;
     }
-    {
+    auto page_grid = [&](cudaLaunchAttribute* a) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kWarps * 32);
         cfg.dynamicSmemBytes = sm;
         cfg.stream = st;
-        cfg.attrs = at + 0;
+        cfg.attrs = a;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kfn, prm);
-        if (e != cudaSuccess) return e;
-    }
-    {
+        return cudaLaunchKernelEx(&cfg, kfn, prm);
+    };
+    auto fp_grid = [&](cudaLaunchAttribute* a) {
         const int fsm = fptok::tc_scratch_bytes((int)prm.c.key_slot_bytes);
-        if ((e = set_kernel_smem((const void*)fp_tokens_kernel<GROUP>, fsm, true)) != cudaSuccess) return e;
+        cudaError_t e2 = set_kernel_smem((const void*)fp_tokens_kernel<GROUP>, fsm, true);
+        if (e2 != cudaSuccess) return e2;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(prm.units * prm.fmax);
         cfg.blockDim = dim3(128);
         cfg.dynamicSmemBytes = fsm;
         cfg.stream = st;
-        cfg.attrs = at + 1;
+        cfg.attrs = a;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, fp_tokens_kernel<GROUP>, prm);
-        if (e != cudaSuccess) return e;
+        return cudaLaunchKernelEx(&cfg, fp_tokens_kernel<GROUP>, prm);
+    };
+    if (prm.fp_first) {
+        if ((e = fp_grid(at + 0)) != cudaSuccess) return e;
+        if ((e = page_grid(at + 1)) != cudaSuccess) return e;
+    } else {
+        if ((e = page_grid(at + 0)) != cudaSuccess) return e;
+        if ((e = fp_grid(at + 1)) != cudaSuccess) return e;
     }
     {
         cudaLaunchConfig_t cfg = {};
@@ -1071,6 +1098,7 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     for (int i = 0; i < 4; ++i) prm.lvl[i] = p.lvl[i];
     prm.nslot = p.nslot;
     prm.units = p.units;
+    prm.fp_first = g_fp_first;
     prm.max_tokens = max_tokens;
     {
         // fast division by units: q = (umulhi(n, mul) + n) >> shift, n < 2^31
