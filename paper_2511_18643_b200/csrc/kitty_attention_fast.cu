@@ -980,10 +980,11 @@ static const int g_pdl = [] {
     return e ? std::atoi(e) : 3;
 }();
 
-// launch order (A/B knob KITTY_FPFIRST): 1 = fp grid, page grid, merge
+// launch order (A/B knob KITTY_FPFIRST, else per launch below): 1 = fp grid,
+// page grid, merge; 0 = page grid, fp grid, merge
 static const int g_fp_first = [] {
     const char* e = std::getenv("KITTY_FPFIRST");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : -1;
 }();
 
 template <int GROUP, int NKH>
@@ -1098,7 +1099,12 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
     for (int i = 0; i < 4; ++i) prm.lvl[i] = p.lvl[i];
     prm.nslot = p.nslot;
     prm.units = p.units;
-    prm.fp_first = g_fp_first;
+    // fp grid first when it needs more than one CTA per SM: beside the
+    // persistent page CTAs only one fp CTA fits an SM's shared memory, so a
+    // larger fp grid trickles through in many rounds (measured: first is
+    // C2 -1.0, C3 -2.8 us per layer); a grid of at most one CTA per SM runs
+    // in the page grid's shadow (C4: page-first 0.7 us faster)
+    prm.fp_first = g_fp_first >= 0 ? g_fp_first : ((long long)p.units * p.fmax > num_sms() ? 1 : 0);
     prm.max_tokens = max_tokens;
     {
         // fast division by units: q = (umulhi(n, mul) + n) >> shift, n < 2^31
