@@ -909,17 +909,18 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     const int maxp = past / G + 1;
     const long long pages = (long long)p.units * maxp;
     const long long streams = (long long)num_sms() * kCtasPerSm * kWarps;  // concurrent page streams (warps)
-    static int ppc_max = 8, cs1_div = 4, inited = 0;  // ppc_max <= 32: an item's pages fit the lanes
+    static int ppc_max = 8, cs1_div = 4, ppc_div = 2, inited = 0;  // ppc_max <= 32: an item's pages fit the lanes
     if (!inited) {
         inited = 1;
-        if (const char* e = getenv("KITTY_SCHED")) {  // experiments: "l1,l2,ppc_max,cs1_div"
-            sscanf(e, "%d,%d,%d,%d", &h_lvl[0], &h_lvl[1], &ppc_max, &cs1_div);
+        if (const char* e = getenv("KITTY_SCHED")) {  // experiments: "l1,l2,ppc_max,cs1_div[,ppc_div]"
+            sscanf(e, "%d,%d,%d,%d,%d", &h_lvl[0], &h_lvl[1], &ppc_max, &cs1_div, &ppc_div);
+            ppc_div = ppc_div < 1 ? 1 : ppc_div;
             ppc_max = ppc_max < 1 ? 1 : (ppc_max > 32 ? 32 : ppc_max);
             h_lvl[2] = h_lvl[0];  // a sweep sets one pair for every unit length
             h_lvl[3] = h_lvl[1];
         }
     }
-    int ppc = static_cast<int>(pages / (2 * streams));
+    int ppc = static_cast<int>(pages / (ppc_div * streams));
     ppc = ppc < 1 ? 1 : (ppc > ppc_max ? ppc_max : ppc);
     p.ppc = ppc;
     p.cmax = (maxp + ppc - 1) / ppc;
