@@ -788,7 +788,12 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
             flush(d0, mnew0);  // a stream's last page is its item's last
         }
     }
-    if (P.fp_first) asm volatile("griddepcontrol.wait;" ::: "memory");  // the fp grid is complete
+    if (P.fp_first) {
+        // this warp's stream is drained: the merge grid (our programmatic
+        // dependent; its CTAs wait for this grid) may take freed SM slots
+        asm volatile("griddepcontrol.launch_dependents;");
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // the fp grid is complete
+    }
     // the last warp out resets the work queue for the next launch (after its
     // outstanding ticket returned: using its value orders the atomics)
     if (lane == 0) {
@@ -973,12 +978,15 @@ size_t fast_attention_workspace_bytes(const KittyCacheDesc& c, int max_tokens) {
     return p.ctr_bytes + p.part_bytes;
 }
 
-// programmatic dependent launch per edge, a bit mask (A/B knob KITTY_PDL):
-// 1 = page grid behind the preceding kernel, 2 = fp grid behind the page grid,
-// 4 = merge grid behind the fp grid
+// programmatic dependent launch per edge, a bit mask (A/B knob KITTY_PDL,
+// else per launch): 1 = first attention grid behind the preceding kernel,
+// 2 = second behind the first, 4 = merge behind the second.  Page-first the
+// merge edge stays off (merge CTAs parked beside fp CTAs take SM slots the fp
+// grid still needs); fp-first it is on, and the page CTAs trigger it as their
+// streams drain.
 static const int g_pdl = [] {
     const char* e = std::getenv("KITTY_PDL");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : -1;
 }();
 
 // launch order (A/B knob KITTY_FPFIRST, else per launch below): 1 = fp grid,
@@ -1005,7 +1013,7 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     cudaLaunchAttribute at[3];
     for (int i = 0; i < 3; ++i) {
         at[i].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[i].val.programmaticStreamSerializationAllowed = (g_pdl >> i) & 1;
+        at[i].val.programmaticStreamSerializationAllowed = ((g_pdl >= 0 ? g_pdl : (prm.fp_first ? 7 : 3)) >> i) & 1;
     }
     auto page_grid = [&](cudaLaunchAttribute* a) {
         cudaLaunchConfig_t cfg = {};
