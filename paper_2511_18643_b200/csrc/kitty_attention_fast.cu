@@ -8,7 +8,8 @@
 // PAPER.md:425-446) instead of from cached f32 rows.
 //
 // One attention call = three launches chained by programmatic dependent
-// launch:
+// launch, the fp-token grid first when it needs more than one
+// CTA per SM (else the page grid first), the merge last:
 //  * page_kernel: the 2-bit pages.  Persistent CTAs (2 per SM x 4 warps);
 //    every warp is one page stream: it pulls work items (chunks of a unit's
 //    pages) from an atomic queue, stages key and value pages through 2-slot
@@ -26,7 +27,7 @@
 //  * mma.sync.m16n8k16 f16 x f16 -> f32, swap-AB: M = 16 tokens (QK) or 16
 //    channels (PV), N = the GQA group, K = 16 channels (QK) or tokens (PV);
 //  * softmax in the log2 domain with lazy rescaling (the running max moves
-//    only when a page exceeds it by 2^8);
+//    only when a page exceeds it by more than kLazy = 2, so P <= 4 in f16);
 //  * each work item leaves a partial record (acc, m, l) in the workspace;
 //  * fp_tokens_kernel: the sink / q-buffer / local tokens (kitty_fp.cuh);
 //  * combine_parts_kernel: LSE merge of a unit's partials (kitty_combine.cuh).
