@@ -84,6 +84,34 @@ template <int GROUP>
 __host__ __device__ inline int warp_smem_bytes(int kslot, int vslot) {
     return (warp_fixed_bytes<GROUP>() + 2 * kslot + 2 * vslot + 127) & ~127;
 }
+// warp-specialised page kernel: per (QK warp, PV warp) pair, the per-warp
+// fixed part plus the hand-off between the two (P^T stages, per-column
+// correction / running max of each page, the page's job, the value slot of
+// page k + 2 for the PV warp to fetch) and the stage barriers
+constexpr int kWsPairs = 4;  // pairs per CTA: 8 warps, 2 CTAs = 16 warps per SM
+template <int PT_ROWS>
+struct __align__(16) PairFixedT {
+    uint32_t pt[2][PT_ROWS][kPtWords];
+    uint32_t qtab[PT_ROWS][D / 2];
+    uint32_t ones[64];
+    float corr[2][8];
+    float mnew[2][8];
+    int job[2][4];  // u (< 0: end of stream), p, pq, slot
+    int vnext[2];   // value slot of page k + 2 (-1: none)
+    uint8_t inv[32];
+    unsigned long long kfull[2];
+    unsigned long long vfull[2];
+    unsigned long long pfull[2];
+    unsigned long long pempty[2];
+};
+template <int GROUP>
+__host__ __device__ constexpr int pair_fixed_bytes() {
+    return static_cast<int>((sizeof(PairFixedT<GROUP == 8 ? 8 : 4>) + 127) & ~size_t(127));
+}
+template <int GROUP>
+__host__ __device__ inline int pair_smem_bytes(int kslot, int vslot) {
+    return (pair_fixed_bytes<GROUP>() + 2 * kslot + 2 * vslot + 127) & ~127;
+}
 constexpr int kMaxTableUnits = 2048;  // units whose lengths a CTA caches in shared memory
 
 struct Params {
@@ -132,6 +160,18 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(phase)
+        : "memory");
+}
+// the same wait with a suspend-time hint: the warp sleeps in the barrier unit
+// until the phase completes (or the hint expires) instead of spinning, so a
+// waiting warp takes no issue slots from the warps that share its scheduler
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase), "r"(0x989680)
         : "memory");
 }
 
@@ -599,7 +639,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) bw[c4][j] -= mnew[j];
         }
-        // probabilities (log2 domain) to P^T[st]: row = query, token t at word
+        // exponents (log2 domain, x - max) to P^T[st]: row = query, token t at word
         // t / 2 (half t % 2); this lane's tokens 8 gid + m (words 4 gid ..) and
         // 64 + 8 gid + m (words 32 + 4 gid ..), two 16-byte stores each
         if (kFull || tig < 2) {
@@ -611,9 +651,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
                     for (int m = 0; m < 8; m += 2) {
                         const float w0 = 1.f / tile_w(m), w1 = 1.f / tile_w(m + 1);
                         const int c0 = tile_c(m), c1 = tile_c(m + 1);
-                        lo[m / 2] = pack_f16x2(ex2(fmaf(acc[m][j], w0, bw[c0][j])), ex2(fmaf(acc[m + 1][j], w1, bw[c1][j])));
-                        hi[m / 2] = pack_f16x2(ex2(fmaf(acc[m][2 + j], w0, bw[c0][j])),
-                                               ex2(fmaf(acc[m + 1][2 + j], w1, bw[c1][j])));
+                        // the exponent x (<= kLazy) as f16: P V takes ex2.f16x2 of it
+                        lo[m / 2] = pack_f16x2(fmaf(acc[m][j], w0, bw[c0][j]), fmaf(acc[m + 1][j], w1, bw[c1][j]));
+                        hi[m / 2] = pack_f16x2(fmaf(acc[m][2 + j], w0, bw[c0][j]), fmaf(acc[m + 1][2 + j], w1, bw[c1][j]));
                     }
                     uint32_t* row = &sm.pt[st][(2 * tig + j) % PT_ROWS][0];
                     *reinterpret_cast<uint4*>(row + 4 * gid) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
@@ -650,8 +690,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
         const uint8_t* vsbase = main_col ? vscale : reinterpret_cast<const uint8_t*>(sm.ones);
         const uint32_t* ptr = &sm.pt[st][prow_ok ? prow : 0][tig];
         const int t0 = 16 * ks + 2 * tig;
-        const uint32_t pp0 = prow_ok ? ptr[8 * ks] : 0u;      // tokens 16 ks + 2 tig (+1)
-        const uint32_t pp1 = prow_ok ? ptr[8 * ks + 4] : 0u;  // tokens 16 ks + 8 + 2 tig (+1)
+        // p = 2^x of the stored exponents (ex2.approx.f16x2: one MUFU per two
+        // tokens, and the f16 exponent costs |p error| < 2e-4 at p <= 2^kLazy)
+        const uint32_t pp0 = prow_ok ? ex2_h2(ptr[8 * ks]) : 0u;      // tokens 16 ks + 2 tig (+1)
+        const uint32_t pp1 = prow_ok ? ex2_h2(ptr[8 * ks + 4]) : 0u;  // tokens 16 ks + 8 + 2 tig (+1)
         const uint32_t b0 = hmul2(pp0, lds32(vsbase + 2 * t0));
         const uint32_t b1 = hmul2(pp1, lds32(vsbase + 2 * (t0 + 8)));
         uint32_t w0, w1, w2, w3;  // token rows 16 ks + [0, 16), channels 8 gid + [0, 8) / 64 + ...
@@ -801,6 +843,526 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P)
         asm volatile("" ::"r"(tk) : "memory");
         const int fin = atomicAdd(&P.ctr[1], 1);
         if (fin == static_cast<int>(gridDim.x) * kWarps - 1) {
+            P.ctr[0] = 0;
+            P.ctr[1] = 0;
+        }
+    }
+}
+
+// Warp-specialised variant (KITTY_WS): each page stream is served by a QK
+// warp and a PV warp, 16 warps per SM at <= 128 registers.
+template <int GROUP, int NKH>
+__global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(Params P) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    constexpr int PT_ROWS = GROUP == 8 ? 8 : 4;
+    using Fixed = PairFixedT<PT_ROWS>;
+    const KittyCacheDesc& c = P.c;
+    const int kslot = static_cast<int>(c.key_slot_bytes);
+    const int vslot = static_cast<int>(c.value_slot_bytes);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    // warps [0, kWsPairs): QK + softmax of their pair's page stream; warps
+    // [kWsPairs, 2 kWsPairs): P V of the same stream, one page behind
+    const int pair = warp & (kWsPairs - 1);
+    const bool qk_role = warp < kWsPairs;
+    const int wbytes = pair_smem_bytes<GROUP>(kslot, vslot);
+    uint8_t* const wbase = smem_raw + pair * wbytes;
+    Fixed& sm = *reinterpret_cast<Fixed*>(wbase);
+    uint8_t* const kslots = wbase + pair_fixed_bytes<GROUP>();
+    uint8_t* const vslots = kslots + 2 * kslot;
+    // group <= 4: B columns 0-3 are the queries, 4-7 auxiliary (unscaled q / p);
+    // group 8: all eight are queries and the auxiliary sums take a second MMA
+    constexpr bool kFull = GROUP == 8;
+    const bool main_col = kFull || gid < 4;
+    const int d_boost = c.cfg.d_boost;
+    const int scale_off = D * G / 4 + d_boost * G / 4 + D;  // KTYP key scales
+    const int zero_off = scale_off + 2 * D;
+    const int hkv = c.cfg.h_kv;
+
+    if (qk_role) {
+        if (lane == 0) {
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(&sm.kfull[i], 1);
+                mbar_init(&sm.vfull[i], 1);
+                mbar_init(&sm.pfull[i], 1);
+                mbar_init(&sm.pempty[i], 1);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_arrive(&sm.pempty[0]);  // both P^T stages start free
+            mbar_arrive(&sm.pempty[1]);
+        }
+        sm.ones[lane] = kOnes;
+        sm.ones[lane + 32] = kOnes;
+        sm.inv[lane] = 0;
+    }
+    // launched as a programmatic dependent of the preceding kernel (the append):
+    // the prologue above overlaps its tail; nothing of the cache is read before this.
+    // fp-first order: the preceding kernel is the fp grid, whose CTAs all passed
+    // their own wait on the append before this grid could launch -- the cache is
+    // final, and the fp grid is waited for at the end (before the merge reads it)
+    if (!P.fp_first) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        // the fp-token grid (our programmatic dependent) may be scheduled from now on
+        asm volatile("griddepcontrol.launch_dependents;");
+    }
+    // per-CTA copy of the unit lengths: an item's decode reads shared memory
+    int* s_ulen = reinterpret_cast<int*>(smem_raw + wbytes * kWsPairs);
+    const bool len_table = P.units <= kMaxTableUnits;
+    if (len_table) {
+        for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = min(__ldcg(c.unit_len + i), P.max_tokens);
+    }
+    __syncthreads();
+
+    // ---- the page stream: work items (atomic queue, one ticket ahead) -> pages ----
+    // An item's block-table entries are loaded by its lanes at once (one per
+    // page, cs <= 32), so a page costs one shuffle, not a dependent load.
+    int tk = 0;
+    if (qk_role && lane == 0) tk = atomicAdd(P.ctr, 1);
+    int iu = 0, ip = 0, ip0 = 0, ip1 = 0, islot = 0, kreg = 0, vreg = 0;
+    bool live = false, done = false;
+    const int nq0 = P.units * P.cmx[0], nq1 = P.units * P.cmx[1], nq2 = P.units * P.cmx[2];
+    auto next_page = [&]() -> Pg {
+        if (!done && !(live && ip + 1 < ip1)) {
+            live = false;
+            while (!live) {
+                const int it = __shfl_sync(0xffffffffu, tk, 0);
+                if (lane == 0) tk = atomicAdd(P.ctr, 1);
+                int sect, idx;
+                if (it < nq0) {
+                    sect = 0;
+                    idx = it;
+                } else if (it < nq0 + nq1) {
+                    sect = 1;
+                    idx = it - nq0;
+                } else if (it < nq0 + nq1 + nq2) {
+                    sect = 2;
+                    idx = it - nq0 - nq1;
+                } else {
+                    done = true;
+                    break;
+                }
+                const int ch = static_cast<int>(
+                    (__umulhi(static_cast<uint32_t>(idx), P.units_mul) + static_cast<uint32_t>(idx)) >> P.units_shift);
+                iu = idx - ch * P.units;
+                const int n = len_table ? s_ulen[iu] : min(__ldcg(c.unit_len + iu), P.max_tokens);
+                const int past = n > c.cfg.s ? n - c.cfg.s : 0;
+                const int vp = (past - min(c.cfg.r, past)) / G;
+                const int lb = level_begin(sect, vp, P.lvl), le = level_begin(sect + 1, vp, P.lvl);
+                ip0 = lb + ch * P.cs[sect];
+                ip1 = min(le, ip0 + P.cs[sect]);
+                live = ip0 < ip1;
+                if (live) {
+                    islot = ch;
+                    for (int l = 0; l < sect; ++l) islot += P.cmx[l];
+                    islot = P.fmax + islot;
+                    const int64_t row = (int64_t)iu * c.max_pages + ip0;
+                    if (lane < ip1 - ip0) {
+                        kreg = __ldcg(c.key_block_table + row + lane);
+                        vreg = __ldcg(c.value_block_table + row + lane);
+                    }
+                }
+            }
+            ip = ip0;
+        } else if (!done) {
+            ++ip;
+        }
+        Pg d;
+        d.u = done ? -1 : iu;
+        d.p = ip;
+        d.pq = ip1 | (ip0 << 16);
+        d.slot = islot;
+        return d;
+    };
+    // a page's key / value slots: shuffled from its item's block-table loads
+    // as late as possible (before the stream decodes another item), so the
+    // loads issued at the item's decode are not waited on
+    auto fill_ks = [&](Pg& d) { d.ks = __shfl_sync(0xffffffffu, kreg, (d.p - (d.pq >> 16)) & 31); };
+    auto fill_vs = [&](Pg& d) { d.vs = __shfl_sync(0xffffffffu, vreg, (d.p - (d.pq >> 16)) & 31); };
+    // Page p of the warp's stream lands in key slot p & 1 and value slot p & 1
+    // (use number p >> 1 of the slot: mbarrier phase (p >> 1) & 1).  QK runs
+    // one page ahead of PV, so a key page is issued one page earlier than its
+    // value page: each gets a full iteration of load time.
+    const uint64_t pol = l2_evict_first();
+    auto issue_key = [&](const Pg& d, int sl) {
+        if (lane == 0 && d.u >= 0) {
+            mbar_expect_tx(&sm.kfull[sl], kslot);
+            bulk_g2s(kslots + sl * kslot, c.key_pool + (int64_t)d.ks * kslot, kslot, &sm.kfull[sl], pol);
+        }
+    };
+    auto issue_val = [&](const Pg& d, int sl) {
+        if (lane == 0 && d.u >= 0) {
+            mbar_expect_tx(&sm.vfull[sl], vslot);
+            bulk_g2s(vslots + sl * vslot, c.value_pool + (int64_t)d.vs * vslot, vslot, &sm.vfull[sl], pol);
+        }
+    };
+    // a new unit's q rows (group x 256 B, L2-resident) are pulled into L1 two
+    // pages before its first QK reads them
+    auto prefetch_q = [&](const Pg& d, int prev_u) {
+        if (d.u >= 0 && d.u != prev_u && lane < GROUP * 2) {
+            const int b = d.u / hkv, h = d.u - b * hkv;
+            const uint16_t* qg = P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP) * D + lane * 64;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(qg));
+        }
+    };
+
+    const Consts kc;
+    uint32_t pe_phase = 0;  // parity of the P^T stage's release the QK tail waits for
+    // ---- QK side state: q fragments of its unit, running max of its item ----
+    int cur_unit = -1;
+    uint32_t qa[8][2];
+    float om[2] = {-INFINITY, -INFINITY};
+    const int qcol = kFull ? gid : (gid & 3);
+    // ---- PV side state: output accumulators, row sums, zero / offset constants ----
+    float oacc[8][4] = {};
+    float ol[2] = {0.f, 0.f};
+    float ob[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    const int prow = kFull ? gid : (gid & 3);
+    const bool prow_ok = prow < GROUP;
+    const bool real0 = kFull || (tig < 2 && 2 * tig < GROUP), real1 = kFull || (tig < 2 && 2 * tig + 1 < GROUP);
+
+    // QK of page d (stage st): waits for the stage, computes the page's logits
+    // and probabilities into P^T[st], its correction factors and running max
+    auto qk_prologue = [&](const Pg& d, int st, uint32_t phase) {
+        if (d.u != cur_unit) {
+            cur_unit = d.u;
+            const int b = d.u / hkv, h = d.u - b * hkv;
+            const uint16_t* qg = P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + (qcol < GROUP ? qcol : 0)) * D;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int dd = 16 * ks + 2 * tig + 8 * hh;
+                    const uint32_t w = qcol < GROUP ? __ldg(reinterpret_cast<const unsigned int*>(qg + dd)) : 0u;
+                    qa[ks][hh] = pack_f16x2(__uint_as_float(w << 16) * kAlpha, __uint_as_float(w & 0xffff0000u) * kAlpha);
+                    // 4 q alpha per channel for the boosted rows (x4 is exact in f16)
+                    if (NKH > 0 && main_col && qcol < GROUP)
+                        sm.qtab[qcol][dd / 2] = pack_f16x2(__uint_as_float(w << 16) * (4.f * kAlpha),
+                                                           __uint_as_float(w & 0xffff0000u) * (4.f * kAlpha));
+                }
+            }
+        }
+        if (d.p == (d.pq >> 16)) om[0] = om[1] = -INFINITY;  // an item's first page
+        mbar_wait_sleep(&sm.kfull[st], phase);
+        if (NKH > 0) {  // boosted rows -> channels (inverse of boost_idx)
+            const uint8_t* kp = kslots + st * kslot;
+            const uint32_t bw = lds32(kp + D * G / 4 + d_boost * G / 4 + 4 * lane);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t bi = (bw >> (8 * k)) & 0xffu;
+                if (bi < 32u) sm.inv[bi] = static_cast<uint8_t>(4 * lane + k);
+            }
+        }
+        __syncwarp();
+    };
+    // QK of a page, in three parts so that the caller can interleave its
+    // k-steps with the P V k-steps of the previous page (one basic block)
+    struct QkRegs {
+        float acc[8][4], aux[4], aux2[4];
+    };
+    // ldmatrix row address of this lane inside a 16-row block of 32-byte code
+    // rows: block mi = lane / 8 covers rows 8 (mi & 1) + [0, 8) at bytes 16 (mi >> 1)
+    const uint32_t ldsm_off = (8 * ((lane >> 3) & 1) + (lane & 7)) * 32 + 16 * (lane >> 4);
+    auto qk_step = [&](int st, int ks, QkRegs& r) {
+        const uint8_t* kp = kslots + st * kslot;
+        // aux lanes (B columns 4-7) read their "scale" from the ones buffer
+        const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
+        const int c0 = 16 * ks + 2 * tig;
+        const uint32_t b0 = hmul2(qa[ks][0], lds32(sbase + 2 * c0));
+        const uint32_t b1 = hmul2(qa[ks][1], lds32(sbase + 2 * (c0 + 8)));
+        uint32_t w0, w1, w2, w3;  // channel rows 16 ks + [0, 16), tokens 8 gid + [0, 8) / 64 + ...
+        ldsm_t4(smem_u32(kp) + 512 * ks + ldsm_off, w0, w1, w2, w3);
+        // aux tile: only rows 0 (ones) and 8 (zero points) are read back
+        const uint32_t z0 = lds32(kp + zero_off + 2 * c0);
+        const uint32_t z1 = lds32(kp + zero_off + 2 * (c0 + 8));
+        if (ks == 0) {
+            mma_ldsm<true>(kc, r.acc, w0, w1, w2, w3, b0, b1);
+            mma16816_z(r.aux, kOnes, z0, kOnes, z1, b0, b1);
+            if (kFull) mma16816_z(r.aux2, kOnes, z0, kOnes, z1, qa[ks][0], qa[ks][1]);
+        } else {
+            mma_ldsm(kc, r.acc, w0, w1, w2, w3, b0, b1);
+            mma16816(r.aux, kOnes, z0, kOnes, z1, b0, b1);
+            if (kFull) mma16816(r.aux2, kOnes, z0, kOnes, z1, qa[ks][0], qa[ks][1]);
+        }
+    };
+    auto qk_tail = [&](int st, QkRegs& r, float (&corr)[2], float (&mnew)[2]) {
+        const uint8_t* kp = kslots + st * kslot;
+        float (&acc)[8][4] = r.acc;
+        float (&aux)[4] = r.aux;
+        float (&aux2)[4] = r.aux2;
+        if (NKH > 0) {
+            // boosted row j (its high bits, weight 4) -> channel inv[j]: B = 4 q alpha s
+            const uint16_t* qt = reinterpret_cast<const uint16_t*>(sm.qtab[qcol < GROUP ? qcol : 0]);
+            const uint16_t* sc = reinterpret_cast<const uint16_t*>(kp + scale_off);  // even offset at d = g = 128
+#pragma unroll
+            for (int hk = 0; hk < NKH; ++hk) {
+                const int j0 = 16 * hk + 2 * tig;
+                const uint32_t ch01 = *reinterpret_cast<const uint16_t*>(sm.inv + j0);
+                const uint32_t ch89 = *reinterpret_cast<const uint16_t*>(sm.inv + j0 + 8);
+                const uint32_t c0 = ch01 & 0xffu, c1 = ch01 >> 8, c8 = ch89 & 0xffu, c9 = ch89 >> 8;
+                const uint32_t q01 = static_cast<uint32_t>(qt[c0]) | (static_cast<uint32_t>(qt[c1]) << 16);
+                const uint32_t s01 = static_cast<uint32_t>(sc[c0]) | (static_cast<uint32_t>(sc[c1]) << 16);
+                const uint32_t q89 = static_cast<uint32_t>(qt[c8]) | (static_cast<uint32_t>(qt[c9]) << 16);
+                const uint32_t s89 = static_cast<uint32_t>(sc[c8]) | (static_cast<uint32_t>(sc[c9]) << 16);
+                // rows past d_boost (d_boost 8: rows 8-15 of the tile; an odd
+                // d_boost: the second half of a pair) are not high-bit rows
+                const bool ok = main_col && qcol < GROUP;
+                const uint32_t m0 = (ok && j0 < d_boost ? 0xffffu : 0u) | (ok && j0 + 1 < d_boost ? 0xffff0000u : 0u);
+                const uint32_t m1 = (ok && j0 + 8 < d_boost ? 0xffffu : 0u) | (ok && j0 + 9 < d_boost ? 0xffff0000u : 0u);
+                const uint32_t b0 = hmul2(q01, s01) & m0;
+                const uint32_t b1 = hmul2(q89, s89) & m1;
+                uint32_t h0, h1, h2, h3;  // high-bit rows 16 hk + [0, 16)
+                ldsm_t4(smem_u32(kp + D * G / 4) + 512 * hk + ldsm_off, h0, h1, h2, h3);
+                mma_ldsm(kc, acc, h0, h1, h2, h3, b0, b1);
+                mma16816(aux, kOnes, 0u, kOnes, 0u, b0, b1);
+            }
+        }
+        // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha).
+        // Tile m holds code m of the lane's 8 (rows gid: token 8 gid + m, gid + 8:
+        // token 64 + 8 gid + m) at weight tile_w(m); bw[c] = the offset of class c.
+        float bw[4][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float sumB = __shfl_sync(0xffffffffu, aux[j], kFull ? tig : (tig & 1));
+            const float cst = kFull ? __shfl_sync(0xffffffffu, aux2[2 + j], tig)
+                                    : __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
+            bw[0][j] = cst - 256.f * sumB;  // w 4
+            bw[1][j] = cst - 64.f * sumB;   // w 16
+            bw[2][j] = cst - 16.f * sumB;   // w 64
+            bw[3][j] = cst - 4.f * sumB;    // w 256
+            // raw maxima per weight class (same weight: monotone), then one FFMA each
+            const float x0 = fmaxf(fmaxf(acc[0][j], acc[0][2 + j]), fmaxf(acc[1][j], acc[1][2 + j]));
+            const float x1 = fmaxf(fmaxf(acc[2][j], acc[2][2 + j]), fmaxf(acc[5][j], acc[5][2 + j]));
+            const float x2 = fmaxf(fmaxf(acc[3][j], acc[3][2 + j]), fmaxf(acc[6][j], acc[6][2 + j]));
+            const float x3 = fmaxf(fmaxf(acc[4][j], acc[4][2 + j]), fmaxf(acc[7][j], acc[7][2 + j]));
+            float pm = fmaxf(fmaxf(fmaf(x0, 1.f / 4.f, bw[0][j]), fmaf(x1, 1.f / 16.f, bw[1][j])),
+                             fmaxf(fmaf(x2, 1.f / 64.f, bw[2][j]), fmaf(x3, 1.f / 256.f, bw[3][j])));
+            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 4));
+            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 8));
+            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 16));
+            // lazy rescaling: the reference max moves only when a page's max
+            // exceeds it by more than kLazy (log2 domain), so P stays <= 2^kLazy
+            // (f16-safe) and the output rescale below almost never runs
+            mnew[j] = pm > om[j] + kLazy ? pm : om[j];
+            corr[j] = ex2(om[j] - mnew[j]);  // 0 on an item's first page (om = -inf), else 1 unless moved
+            om[j] = mnew[j];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) bw[c4][j] -= mnew[j];
+        }
+        // P^T[st] is free once the PV warp is done with page k - 2
+        mbar_wait_sleep(&sm.pempty[st], pe_phase);
+        // probabilities (log2 domain) to P^T[st]: row = query, token t at word
+        // t / 2 (half t % 2); this lane's tokens 8 gid + m (words 4 gid ..) and
+        // 64 + 8 gid + m (words 32 + 4 gid ..), two 16-byte stores each
+        if (kFull || tig < 2) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (2 * tig + j < GROUP) {
+                    uint32_t lo[4], hi[4];
+#pragma unroll
+                    for (int m = 0; m < 8; m += 2) {
+                        const float w0 = 1.f / tile_w(m), w1 = 1.f / tile_w(m + 1);
+                        const int c0 = tile_c(m), c1 = tile_c(m + 1);
+                        // the exponent x (<= kLazy) as f16: the PV warp takes ex2.f16x2 of it
+                        lo[m / 2] = pack_f16x2(fmaf(acc[m][j], w0, bw[c0][j]), fmaf(acc[m + 1][j], w1, bw[c1][j]));
+                        hi[m / 2] = pack_f16x2(fmaf(acc[m][2 + j], w0, bw[c0][j]), fmaf(acc[m + 1][2 + j], w1, bw[c1][j]));
+                    }
+                    uint32_t* row = &sm.pt[st][(2 * tig + j) % PT_ROWS][0];
+                    *reinterpret_cast<uint4*>(row + 4 * gid) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                    *reinterpret_cast<uint4*>(row + 32 + 4 * gid) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                }
+            }
+        }
+    };
+    // P V of page d (stage st) with P^T[st]; fresh = its item's first page
+    // P V of a page (stage st) with P^T[st]; fresh = its item's first page
+    struct PvRegs {
+        float vaux[4], vaux2[4];
+    };
+    auto pv_head = [&](bool fresh, const float (&corr)[2], int st, uint32_t phase) {
+        mbar_wait_sleep(&sm.vfull[st], phase);
+        // an item's first page zeroes the running output (factor 0); later
+        // pages rescale it only when a real column's max moved (warp vote;
+        // rare under lazy rescaling).  One in-place multiply path: no copies.
+        const float c0 = fresh ? 0.f : corr[0], c1 = fresh ? 0.f : corr[1];
+        if (__any_sync(0xffffffffu, fresh || (real0 && c0 != 1.f) || (real1 && c1 != 1.f))) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                oacc[m][0] *= c0;
+                oacc[m][2] *= c0;
+                oacc[m][1] *= c1;
+                oacc[m][3] *= c1;
+            }
+        }
+    };
+    auto pv_step = [&](int st, int ks, PvRegs& r) {
+        const uint8_t* vp = vslots + st * vslot;
+        const uint8_t* vscale = vp + G * D / 4;
+        const uint8_t* vzero = vscale + 2 * G;
+        const uint8_t* vsbase = main_col ? vscale : reinterpret_cast<const uint8_t*>(sm.ones);
+        const uint32_t* ptr = &sm.pt[st][prow_ok ? prow : 0][tig];
+        const int t0 = 16 * ks + 2 * tig;
+        // p = 2^x of the exponents the QK warp stored (f16x2; |error| < 2e-4 for p <= 4)
+        const uint32_t pp0 = prow_ok ? ex2_h2(ptr[8 * ks]) : 0u;      // tokens 16 ks + 2 tig (+1)
+        const uint32_t pp1 = prow_ok ? ex2_h2(ptr[8 * ks + 4]) : 0u;  // tokens 16 ks + 8 + 2 tig (+1)
+        const uint32_t b0 = hmul2(pp0, lds32(vsbase + 2 * t0));
+        const uint32_t b1 = hmul2(pp1, lds32(vsbase + 2 * (t0 + 8)));
+        uint32_t w0, w1, w2, w3;  // token rows 16 ks + [0, 16), channels 8 gid + [0, 8) / 64 + ...
+        ldsm_t4(smem_u32(vp) + 512 * ks + ldsm_off, w0, w1, w2, w3);
+        const uint32_t z0 = lds32(vzero + 2 * t0);
+        const uint32_t z1 = lds32(vzero + 2 * (t0 + 8));
+        mma_ldsm(kc, oacc, w0, w1, w2, w3, b0, b1);
+        if (ks == 0)
+            mma16816_z(r.vaux, kOnes, z0, kOnes, z1, b0, b1);
+        else
+            mma16816(r.vaux, kOnes, z0, kOnes, z1, b0, b1);
+        if (kFull) {  // the unscaled p: sum p and sum p z
+            if (ks == 0)
+                mma16816_z(r.vaux2, kOnes, z0, kOnes, z1, pp0, pp1);
+            else
+                mma16816(r.vaux2, kOnes, z0, kOnes, z1, pp0, pp1);
+        }
+    };
+    auto pv_tail = [&](bool fresh, const float (&corr)[2], PvRegs& r) {
+        // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z).
+        // Row constants (zero points, the 1024 offset) accumulate per column in
+        // ob[weight class] and are added at the flush.
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float sBv = __shfl_sync(0xffffffffu, r.vaux[j], kFull ? tig : (tig & 1));
+            const float lp = kFull ? __shfl_sync(0xffffffffu, r.vaux2[j], tig) : __shfl_sync(0xffffffffu, r.vaux[j], 2 + (tig & 1));
+            const float zz = kFull ? __shfl_sync(0xffffffffu, r.vaux2[2 + j], tig)
+                                   : __shfl_sync(0xffffffffu, r.vaux[2 + j], 2 + (tig & 1));
+            const float cf = fresh ? 0.f : corr[j];
+            ol[j] = fmaf(ol[j], cf, lp);
+            ob[0][j] = fmaf(ob[0][j], cf, zz - 256.f * sBv);  // w 4
+            ob[1][j] = fmaf(ob[1][j], cf, zz - 64.f * sBv);   // w 16
+            ob[2][j] = fmaf(ob[2][j], cf, zz - 16.f * sBv);   // w 64
+            ob[3][j] = fmaf(ob[3][j], cf, zz - 4.f * sBv);    // w 256
+        }
+    };
+    auto flush = [&](const Pg& d, const float (&mnew)[2]) {
+        float* base = P.part + ((int64_t)d.u * P.nslot + d.slot) * part_stride(GROUP);
+        if (kFull || tig < 2) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int g = 2 * tig + j;
+                if (g < GROUP) {
+                    // tile m: row gid = channel 8 gid + m, row gid + 8 = channel 64 + 8 gid + m
+                    float lo[8], hi[8];
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) {
+                        lo[m] = fmaf(oacc[m][j], 1.f / tile_w(m), ob[tile_c(m)][j]);
+                        hi[m] = fmaf(oacc[m][2 + j], 1.f / tile_w(m), ob[tile_c(m)][j]);
+                    }
+                    float4* o4 = reinterpret_cast<float4*>(base + g * D + 8 * gid);
+                    o4[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                    o4[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
+                    float4* h4 = reinterpret_cast<float4*>(base + g * D + 64 + 8 * gid);
+                    h4[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                    h4[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+                    if (gid == 0) *reinterpret_cast<float2*>(base + GROUP * D + 2 * g) = make_float2(mnew[j], ol[j]);
+                }
+            }
+        }
+    };
+
+    // ---- the pair's pipeline: QK warp on page k while the PV warp runs page
+    // k - 1.  Stage st = k & 1 holds page k's key slot, value slot, P^T and job;
+    // pfull[st]: the QK warp published page k (P^T, corrections, job);
+    // pempty[st]: the PV warp is done with it (P^T, job, value slot) ----
+    if (qk_role) {
+        Pg d0 = next_page();
+        fill_ks(d0);
+        fill_vs(d0);
+        Pg d1 = next_page();
+        fill_ks(d1);
+        fill_vs(d1);
+        issue_key(d0, 0);
+        issue_val(d0, 0);
+        issue_key(d1, 1);
+        issue_val(d1, 1);
+        prefetch_q(d1, d0.u);
+        uint32_t k = 0;
+#pragma unroll 1
+        for (; d0.u >= 0; ++k) {
+            const int st = k & 1;
+            const uint32_t ph = (k >> 1) & 1;
+            float corr[2], mnew[2];
+            qk_prologue(d0, st, ph);
+            pe_phase = ph;
+            QkRegs qr;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) qk_step(st, ks, qr);
+            qk_tail(st, qr, corr, mnew);
+            Pg d2 = next_page();  // page k + 2: key slot st, value slot st
+            fill_ks(d2);
+            fill_vs(d2);
+            prefetch_q(d2, d1.u);
+            if (gid == 0) {
+                sm.corr[st][2 * tig] = corr[0];
+                sm.corr[st][2 * tig + 1] = corr[1];
+                sm.mnew[st][2 * tig] = mnew[0];
+                sm.mnew[st][2 * tig + 1] = mnew[1];
+            }
+            if (lane == 0) {
+                sm.job[st][0] = d0.u;
+                sm.job[st][1] = d0.p;
+                sm.job[st][2] = d0.pq;
+                sm.job[st][3] = d0.slot;
+                sm.vnext[st] = d2.u >= 0 ? d2.vs : -1;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.pfull[st]);
+            issue_key(d2, st);  // QK(k) is done with key slot st
+            d0 = d1;
+            d1 = d2;
+        }
+        // end of the stream: an empty job once the PV warp released the stage
+        const int st = k & 1;
+        mbar_wait_sleep(&sm.pempty[st], (k >> 1) & 1);
+        if (lane == 0) sm.job[st][0] = -1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.pfull[st]);
+    } else {
+        uint32_t k = 0;
+#pragma unroll 1
+        for (;; ++k) {
+            const int st = k & 1;
+            const uint32_t ph = (k >> 1) & 1;
+            mbar_wait_sleep(&sm.pfull[st], ph);
+            Pg d;
+            d.u = sm.job[st][0];
+            if (d.u < 0) break;
+            d.p = sm.job[st][1];
+            d.pq = sm.job[st][2];
+            d.slot = sm.job[st][3];
+            const int vs2 = sm.vnext[st];
+            const float corr[2] = {sm.corr[st][2 * tig], sm.corr[st][2 * tig + 1]};
+            const float mnew[2] = {sm.mnew[st][2 * tig], sm.mnew[st][2 * tig + 1]};
+            const bool fresh = d.p == (d.pq >> 16), last = d.p + 1 == (d.pq & 0xffff);
+            PvRegs pr;
+            pv_head(fresh, corr, st, ph);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) pv_step(st, ks, pr);
+            pv_tail(fresh, corr, pr);
+            if (last) flush(d, mnew);
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&sm.pempty[st]);
+                if (vs2 >= 0) {  // value slot st -> page k + 2
+                    mbar_expect_tx(&sm.vfull[st], vslot);
+                    bulk_g2s(vslots + st * vslot, c.value_pool + (int64_t)vs2 * vslot, vslot, &sm.vfull[st], pol);
+                }
+            }
+        }
+    }
+    // the last warp out resets the work queue for the next launch (after its
+    // outstanding ticket returned: using its value orders the atomics)
+    if (qk_role && lane == 0) {
+        asm volatile("" ::"r"(tk) : "memory");
+        const int fin = atomicAdd(&P.ctr[1], 1);
+        if (fin == static_cast<int>(gridDim.x) * kWsPairs - 1) {
             P.ctr[0] = 0;
             P.ctr[1] = 0;
         }
@@ -997,13 +1559,27 @@ static const int g_fp_first = [] {
     return e ? std::atoi(e) : -1;
 }();
 
+// page kernel variant (A/B knob KITTY_WS, else per group): 1 = warp-specialised
+// QK / PV pairs (16 warps / SM at <= 128 registers), 0 = one warp per page
+// stream interleaving both (8 warps / SM).  Measured: group 8 (C5) 487.1 vs
+// 490.3 us per layer with pairs; group 4 (C2) 105.5 vs 105.2, C4 38.3 vs 37.7.
+static const int g_ws_env = [] {
+    const char* e = std::getenv("KITTY_WS");
+    return e ? std::atoi(e) : -1;
+}();
+
 template <int GROUP, int NKH>
 static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
-    auto kfn = page_kernel<GROUP, NKH>;
-    const size_t sm = (size_t)warp_smem_bytes<GROUP>((int)prm.c.key_slot_bytes, (int)prm.c.value_slot_bytes) * kWarps +
+    const bool g_ws = g_ws_env >= 0 ? g_ws_env != 0 : GROUP == 8;
+    auto kfn = g_ws ? page_ws_kernel<GROUP, NKH> : page_kernel<GROUP, NKH>;
+    const int ks_b = (int)prm.c.key_slot_bytes, vs_b = (int)prm.c.value_slot_bytes;
+    const size_t sm = (size_t)(g_ws ? pair_smem_bytes<GROUP>(ks_b, vs_b) * kWsPairs : warp_smem_bytes<GROUP>(ks_b, vs_b) * kWarps) +
                       (prm.units <= kMaxTableUnits ? 4 * prm.units : 0);
     cudaError_t e = set_kernel_smem((const void*)kfn,
-                                    warp_smem_bytes<GROUP>(kKeySlotMax, kValueSlot) * kWarps + 4 * kMaxTableUnits, true);
+                                    (g_ws ? pair_smem_bytes<GROUP>(kKeySlotMax, kValueSlot) * kWsPairs
+                                          : warp_smem_bytes<GROUP>(kKeySlotMax, kValueSlot) * kWarps) +
+                                        4 * kMaxTableUnits,
+                                    true);
     if (e != cudaSuccess) return e;
     // persistent grid: kCtasPerSm CTAs per SM must be co-resident (their shared
     // memory plus the 1 KB per-CTA reservation fit the SM), else fewer per SM
@@ -1019,7 +1595,7 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     auto page_grid = [&](cudaLaunchAttribute* a) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(kWarps * 32);
+        cfg.blockDim = dim3(g_ws ? 2 * kWsPairs * 32 : kWarps * 32);
         cfg.dynamicSmemBytes = sm;
         cfg.stream = st;
         cfg.attrs = a;
