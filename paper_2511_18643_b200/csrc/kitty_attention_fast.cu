@@ -1394,10 +1394,8 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
 }
 
 // K5: WARPS warps merge one (unit, query row): 2 when a unit has <= 32 partial
-// slots (short contexts: many small CTAs, one wave); 4 when 8-warp CTAs would
-// need more than one wave and a unit has <= 128 slots; 16 above 128 slots
-// (long contexts); else 8
-// (long contexts); else 8.  CSPLIT CTAs share a row (channel slices) when the
+// slots (short contexts: many small CTAs, one wave), 4 up to 128 slots, 16
+// above (long contexts).  CSPLIT CTAs share a row (channel slices) when the
 // rows alone would not fill the GPU (a few long units: C4).
 template <int GROUP, int WARPS, int CSPLIT = 1>
 __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
