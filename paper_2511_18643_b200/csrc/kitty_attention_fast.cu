@@ -33,6 +33,7 @@
 //  * combine_parts_kernel: LSE merge of a unit's partials (kitty_combine.cuh).
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kitty_attention.cuh"
 #include "kitty_combine.cuh"
@@ -352,524 +353,29 @@ struct Pg {
     int u, p, pq, slot, ks, vs;
 };
 
-template <int GROUP, int NKH>
-__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) page_kernel(Params P) {
+// WS = false: one warp per page stream, QK of page k + 1 interleaved with P V
+// of page k (8 warps / SM).  WS = true (KITTY_WS; the default at group 8):
+// each stream is served by a QK + softmax warp and a PV warp one page behind
+// it, handing pages over through mbarriers (16 warps / SM at <= 128 registers).
+template <int GROUP, int NKH, bool WS>
+__global__ void __launch_bounds__(WS ? 2 * kWsPairs * 32 : kWarps * 32, kCtasPerSm) page_kernel(Params P) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     constexpr int PT_ROWS = GROUP == 8 ? 8 : 4;
-    using Fixed = WarpFixedT<PT_ROWS>;
+    using Fixed = std::conditional_t<WS, PairFixedT<PT_ROWS>, WarpFixedT<PT_ROWS>>;
     const KittyCacheDesc& c = P.c;
     const int kslot = static_cast<int>(c.key_slot_bytes);
     const int vslot = static_cast<int>(c.value_slot_bytes);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    const int wbytes = warp_smem_bytes<GROUP>(kslot, vslot);
-    uint8_t* const wbase = smem_raw + warp * wbytes;
-    Fixed& sm = *reinterpret_cast<Fixed*>(wbase);
-    uint8_t* const kslots = wbase + warp_fixed_bytes<GROUP>();
-    uint8_t* const vslots = kslots + 2 * kslot;
-    // group <= 4: B columns 0-3 are the queries, 4-7 auxiliary (unscaled q / p);
-    // group 8: all eight are queries and the auxiliary sums take a second MMA
-    constexpr bool kFull = GROUP == 8;
-    const bool main_col = kFull || gid < 4;
-    const int d_boost = c.cfg.d_boost;
-    const int scale_off = D * G / 4 + d_boost * G / 4 + D;  // KTYP key scales
-    const int zero_off = scale_off + 2 * D;
-    const int hkv = c.cfg.h_kv;
-
-    if (lane == 0) {
-        mbar_init(&sm.kfull[0], 1);
-        mbar_init(&sm.kfull[1], 1);
-        mbar_init(&sm.vfull[0], 1);
-        mbar_init(&sm.vfull[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    sm.ones[lane] = kOnes;
-    sm.ones[lane + 32] = kOnes;
-    sm.inv[lane] = 0;
-    // launched as a programmatic dependent of the preceding kernel (the append):
-    // the prologue above overlaps its tail; nothing of the cache is read before this.
-    // fp-first order: the preceding kernel is the fp grid, whose CTAs all passed
-    // their own wait on the append before this grid could launch -- the cache is
-    // final, and the fp grid is waited for at the end (before the merge reads it)
-    if (!P.fp_first) {
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        // the fp-token grid (our programmatic dependent) may be scheduled from now on
-        asm volatile("griddepcontrol.launch_dependents;");
-    }
-    // per-CTA copy of the unit lengths: an item's decode reads shared memory
-    int* s_ulen = reinterpret_cast<int*>(smem_raw + wbytes * kWarps);
-    const bool len_table = P.units <= kMaxTableUnits;
-    if (len_table) {
-        for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = min(__ldcg(c.unit_len + i), P.max_tokens);
-    }
-    __syncthreads();
-
-    // ---- the page stream: work items (atomic queue, one ticket ahead) -> pages ----
-    // An item's block-table entries are loaded by its lanes at once (one per
-    // page, cs <= 32), so a page costs one shuffle, not a dependent load.
-    int tk = 0;
-    if (lane == 0) tk = atomicAdd(P.ctr, 1);
-    int iu = 0, ip = 0, ip0 = 0, ip1 = 0, islot = 0, kreg = 0, vreg = 0;
-    bool live = false, done = false;
-    const int nq0 = P.units * P.cmx[0], nq1 = P.units * P.cmx[1], nq2 = P.units * P.cmx[2];
-    auto next_page = [&]() -> Pg {
-        if (!done && !(live && ip + 1 < ip1)) {
-            live = false;
-            while (!live) {
-                const int it = __shfl_sync(0xffffffffu, tk, 0);
-                if (lane == 0) tk = atomicAdd(P.ctr, 1);
-                int sect, idx;
-                if (it < nq0) {
-                    sect = 0;
-                    idx = it;
-                } else if (it < nq0 + nq1) {
-                    sect = 1;
-                    idx = it - nq0;
-                } else if (it < nq0 + nq1 + nq2) {
-                    sect = 2;
-                    idx = it - nq0 - nq1;
-                } else {
-                    done = true;
-                    break;
-                }
-                const int ch = static_cast<int>(
-                    (__umulhi(static_cast<uint32_t>(idx), P.units_mul) + static_cast<uint32_t>(idx)) >> P.units_shift);
-                iu = idx - ch * P.units;
-                const int n = len_table ? s_ulen[iu] : min(__ldcg(c.unit_len + iu), P.max_tokens);
-                const int past = n > c.cfg.s ? n - c.cfg.s : 0;
-                const int vp = (past - min(c.cfg.r, past)) / G;
-                const int lb = level_begin(sect, vp, P.lvl), le = level_begin(sect + 1, vp, P.lvl);
-                ip0 = lb + ch * P.cs[sect];
-                ip1 = min(le, ip0 + P.cs[sect]);
-                live = ip0 < ip1;
-                if (live) {
-                    islot = ch;
-                    for (int l = 0; l < sect; ++l) islot += P.cmx[l];
-                    islot = P.fmax + islot;
-                    const int64_t row = (int64_t)iu * c.max_pages + ip0;
-                    if (lane < ip1 - ip0) {
-                        kreg = __ldcg(c.key_block_table + row + lane);
-                        vreg = __ldcg(c.value_block_table + row + lane);
-                    }
-                }
-            }
-            ip = ip0;
-        } else if (!done) {
-            ++ip;
-        }
-        Pg d;
-        d.u = done ? -1 : iu;
-        d.p = ip;
-        d.pq = ip1 | (ip0 << 16);
-        d.slot = islot;
-        return d;
-    };
-    // a page's key / value slots: shuffled from its item's block-table loads
-    // as late as possible (before the stream decodes another item), so the
-    // loads issued at the item's decode are not waited on
-    auto fill_ks = [&](Pg& d) { d.ks = __shfl_sync(0xffffffffu, kreg, (d.p - (d.pq >> 16)) & 31); };
-    auto fill_vs = [&](Pg& d) { d.vs = __shfl_sync(0xffffffffu, vreg, (d.p - (d.pq >> 16)) & 31); };
-    // Page p of the warp's stream lands in key slot p & 1 and value slot p & 1
-    // (use number p >> 1 of the slot: mbarrier phase (p >> 1) & 1).  QK runs
-    // one page ahead of PV, so a key page is issued one page earlier than its
-    // value page: each gets a full iteration of load time.
-    const uint64_t pol = l2_evict_first();
-    auto issue_key = [&](const Pg& d, int sl) {
-        if (lane == 0 && d.u >= 0) {
-            mbar_expect_tx(&sm.kfull[sl], kslot);
-            bulk_g2s(kslots + sl * kslot, c.key_pool + (int64_t)d.ks * kslot, kslot, &sm.kfull[sl], pol);
-        }
-    };
-    auto issue_val = [&](const Pg& d, int sl) {
-        if (lane == 0 && d.u >= 0) {
-            mbar_expect_tx(&sm.vfull[sl], vslot);
-            bulk_g2s(vslots + sl * vslot, c.value_pool + (int64_t)d.vs * vslot, vslot, &sm.vfull[sl], pol);
-        }
-    };
-    // a new unit's q rows (group x 256 B, L2-resident) are pulled into L1 two
-    // pages before its first QK reads them
-    auto prefetch_q = [&](const Pg& d, int prev_u) {
-        if (d.u >= 0 && d.u != prev_u && lane < GROUP * 2) {
-            const int b = d.u / hkv, h = d.u - b * hkv;
-            const uint16_t* qg = P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP) * D + lane * 64;
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(qg));
-        }
-    };
-
-    const Consts kc;
-    // ---- QK side state: q fragments of its unit, running max of its item ----
-    int cur_unit = -1;
-    uint32_t qa[8][2];
-    float om[2] = {-INFINITY, -INFINITY};
-    const int qcol = kFull ? gid : (gid & 3);
-    // ---- PV side state: output accumulators, row sums, zero / offset constants ----
-    float oacc[8][4] = {};
-    float ol[2] = {0.f, 0.f};
-    float ob[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-    const int prow = kFull ? gid : (gid & 3);
-    const bool prow_ok = prow < GROUP;
-    const bool real0 = kFull || (tig < 2 && 2 * tig < GROUP), real1 = kFull || (tig < 2 && 2 * tig + 1 < GROUP);
-
-    // QK of page d (stage st): waits for the stage, computes the page's logits
-    // and probabilities into P^T[st], its correction factors and running max
-    auto qk_prologue = [&](const Pg& d, int st, uint32_t phase) {
-        if (d.u != cur_unit) {
-            cur_unit = d.u;
-            const int b = d.u / hkv, h = d.u - b * hkv;
-            const uint16_t* qg = P.q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + (qcol < GROUP ? qcol : 0)) * D;
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const int dd = 16 * ks + 2 * tig + 8 * hh;
-                    const uint32_t w = qcol < GROUP ? __ldg(reinterpret_cast<const unsigned int*>(qg + dd)) : 0u;
-                    qa[ks][hh] = pack_f16x2(__uint_as_float(w << 16) * kAlpha, __uint_as_float(w & 0xffff0000u) * kAlpha);
-                    // 4 q alpha per channel for the boosted rows (x4 is exact in f16)
-                    if (NKH > 0 && main_col && qcol < GROUP)
-                        sm.qtab[qcol][dd / 2] = pack_f16x2(__uint_as_float(w << 16) * (4.f * kAlpha),
-                                                           __uint_as_float(w & 0xffff0000u) * (4.f * kAlpha));
-                }
-            }
-        }
-        if (d.p == (d.pq >> 16)) om[0] = om[1] = -INFINITY;  // an item's first page
-        mbar_wait(&sm.kfull[st], phase);
-        if (NKH > 0) {  // boosted rows -> channels (inverse of boost_idx)
-            const uint8_t* kp = kslots + st * kslot;
-            const uint32_t bw = lds32(kp + D * G / 4 + d_boost * G / 4 + 4 * lane);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t bi = (bw >> (8 * k)) & 0xffu;
-                if (bi < 32u) sm.inv[bi] = static_cast<uint8_t>(4 * lane + k);
-            }
-        }
-        __syncwarp();
-    };
-    // QK of a page, in three parts so that the caller can interleave its
-    // k-steps with the P V k-steps of the previous page (one basic block)
-    struct QkRegs {
-        float acc[8][4], aux[4], aux2[4];
-    };
-    // ldmatrix row address of this lane inside a 16-row block of 32-byte code
-    // rows: block mi = lane / 8 covers rows 8 (mi & 1) + [0, 8) at bytes 16 (mi >> 1)
-    const uint32_t ldsm_off = (8 * ((lane >> 3) & 1) + (lane & 7)) * 32 + 16 * (lane >> 4);
-    auto qk_step = [&](int st, int ks, QkRegs& r) {
-        const uint8_t* kp = kslots + st * kslot;
-        // aux lanes (B columns 4-7) read their "scale" from the ones buffer
-        const uint8_t* sbase = main_col ? kp + scale_off : reinterpret_cast<const uint8_t*>(sm.ones);
-        const int c0 = 16 * ks + 2 * tig;
-        const uint32_t b0 = hmul2(qa[ks][0], lds32(sbase + 2 * c0));
-        const uint32_t b1 = hmul2(qa[ks][1], lds32(sbase + 2 * (c0 + 8)));
-        uint32_t w0, w1, w2, w3;  // channel rows 16 ks + [0, 16), tokens 8 gid + [0, 8) / 64 + ...
-        ldsm_t4(smem_u32(kp) + 512 * ks + ldsm_off, w0, w1, w2, w3);
-        // aux tile: only rows 0 (ones) and 8 (zero points) are read back
-        const uint32_t z0 = lds32(kp + zero_off + 2 * c0);
-        const uint32_t z1 = lds32(kp + zero_off + 2 * (c0 + 8));
-        if (ks == 0) {
-            mma_ldsm<true>(kc, r.acc, w0, w1, w2, w3, b0, b1);
-            mma16816_z(r.aux, kOnes, z0, kOnes, z1, b0, b1);
-            if (kFull) mma16816_z(r.aux2, kOnes, z0, kOnes, z1, qa[ks][0], qa[ks][1]);
-        } else {
-            mma_ldsm(kc, r.acc, w0, w1, w2, w3, b0, b1);
-            mma16816(r.aux, kOnes, z0, kOnes, z1, b0, b1);
-            if (kFull) mma16816(r.aux2, kOnes, z0, kOnes, z1, qa[ks][0], qa[ks][1]);
-        }
-    };
-    auto qk_tail = [&](int st, QkRegs& r, float (&corr)[2], float (&mnew)[2]) {
-        const uint8_t* kp = kslots + st * kslot;
-        float (&acc)[8][4] = r.acc;
-        float (&aux)[4] = r.aux;
-        float (&aux2)[4] = r.aux2;
-        if (NKH > 0) {
-            // boosted row j (its high bits, weight 4) -> channel inv[j]: B = 4 q alpha s
-            const uint16_t* qt = reinterpret_cast<const uint16_t*>(sm.qtab[qcol < GROUP ? qcol : 0]);
-            const uint16_t* sc = reinterpret_cast<const uint16_t*>(kp + scale_off);  // even offset at d = g = 128
-#pragma unroll
-            for (int hk = 0; hk < NKH; ++hk) {
-                const int j0 = 16 * hk + 2 * tig;
-                const uint32_t ch01 = *reinterpret_cast<const uint16_t*>(sm.inv + j0);
-                const uint32_t ch89 = *reinterpret_cast<const uint16_t*>(sm.inv + j0 + 8);
-                const uint32_t c0 = ch01 & 0xffu, c1 = ch01 >> 8, c8 = ch89 & 0xffu, c9 = ch89 >> 8;
-                const uint32_t q01 = static_cast<uint32_t>(qt[c0]) | (static_cast<uint32_t>(qt[c1]) << 16);
-                const uint32_t s01 = static_cast<uint32_t>(sc[c0]) | (static_cast<uint32_t>(sc[c1]) << 16);
-                const uint32_t q89 = static_cast<uint32_t>(qt[c8]) | (static_cast<uint32_t>(qt[c9]) << 16);
-                const uint32_t s89 = static_cast<uint32_t>(sc[c8]) | (static_cast<uint32_t>(sc[c9]) << 16);
-                // rows past d_boost (d_boost 8: rows 8-15 of the tile; an odd
-                // d_boost: the second half of a pair) are not high-bit rows
-                const bool ok = main_col && qcol < GROUP;
-                const uint32_t m0 = (ok && j0 < d_boost ? 0xffffu : 0u) | (ok && j0 + 1 < d_boost ? 0xffff0000u : 0u);
-                const uint32_t m1 = (ok && j0 + 8 < d_boost ? 0xffffu : 0u) | (ok && j0 + 9 < d_boost ? 0xffff0000u : 0u);
-                const uint32_t b0 = hmul2(q01, s01) & m0;
-                const uint32_t b1 = hmul2(q89, s89) & m1;
-                uint32_t h0, h1, h2, h3;  // high-bit rows 16 hk + [0, 16)
-                ldsm_t4(smem_u32(kp + D * G / 4) + 512 * hk + ldsm_off, h0, h1, h2, h3);
-                mma_ldsm(kc, acc, h0, h1, h2, h3, b0, b1);
-                mma16816(aux, kOnes, 0u, kOnes, 0u, b0, b1);
-            }
-        }
-        // aux row 0 (lanes 0-3): sum of B per column; row 8, columns 4-7: sum(z * q * alpha).
-        // Tile m holds code m of the lane's 8 (rows gid: token 8 gid + m, gid + 8:
-        // token 64 + 8 gid + m) at weight tile_w(m); bw[c] = the offset of class c.
-        float bw[4][2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const float sumB = __shfl_sync(0xffffffffu, aux[j], kFull ? tig : (tig & 1));
-            const float cst = kFull ? __shfl_sync(0xffffffffu, aux2[2 + j], tig)
-                                    : __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
-            bw[0][j] = cst - 256.f * sumB;  // w 4
-            bw[1][j] = cst - 64.f * sumB;   // w 16
-            bw[2][j] = cst - 16.f * sumB;   // w 64
-            bw[3][j] = cst - 4.f * sumB;    // w 256
-            // raw maxima per weight class (same weight: monotone), then one FFMA each
-            const float x0 = fmaxf(fmaxf(acc[0][j], acc[0][2 + j]), fmaxf(acc[1][j], acc[1][2 + j]));
-            const float x1 = fmaxf(fmaxf(acc[2][j], acc[2][2 + j]), fmaxf(acc[5][j], acc[5][2 + j]));
-            const float x2 = fmaxf(fmaxf(acc[3][j], acc[3][2 + j]), fmaxf(acc[6][j], acc[6][2 + j]));
-            const float x3 = fmaxf(fmaxf(acc[4][j], acc[4][2 + j]), fmaxf(acc[7][j], acc[7][2 + j]));
-            float pm = fmaxf(fmaxf(fmaf(x0, 1.f / 4.f, bw[0][j]), fmaf(x1, 1.f / 16.f, bw[1][j])),
-                             fmaxf(fmaf(x2, 1.f / 64.f, bw[2][j]), fmaf(x3, 1.f / 256.f, bw[3][j])));
-            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 4));
-            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 8));
-            pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 16));
-            // lazy rescaling: the reference max moves only when a page's max
-            // exceeds it by more than kLazy (log2 domain), so P stays <= 2^kLazy
-            // (f16-safe) and the output rescale below almost never runs
-            mnew[j] = pm > om[j] + kLazy ? pm : om[j];
-            corr[j] = ex2(om[j] - mnew[j]);  // 0 on an item's first page (om = -inf), else 1 unless moved
-            om[j] = mnew[j];
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) bw[c4][j] -= mnew[j];
-        }
-        // exponents (log2 domain, x - max) to P^T[st]: row = query, token t at word
-        // t / 2 (half t % 2); this lane's tokens 8 gid + m (words 4 gid ..) and
-        // 64 + 8 gid + m (words 32 + 4 gid ..), two 16-byte stores each
-        if (kFull || tig < 2) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                if (2 * tig + j < GROUP) {
-                    uint32_t lo[4], hi[4];
-#pragma unroll
-                    for (int m = 0; m < 8; m += 2) {
-                        const float w0 = 1.f / tile_w(m), w1 = 1.f / tile_w(m + 1);
-                        const int c0 = tile_c(m), c1 = tile_c(m + 1);
-                        // the exponent x (<= kLazy) as f16: P V takes ex2.f16x2 of it
-                        lo[m / 2] = pack_f16x2(fmaf(acc[m][j], w0, bw[c0][j]), fmaf(acc[m + 1][j], w1, bw[c1][j]));
-                        hi[m / 2] = pack_f16x2(fmaf(acc[m][2 + j], w0, bw[c0][j]), fmaf(acc[m + 1][2 + j], w1, bw[c1][j]));
-                    }
-                    uint32_t* row = &sm.pt[st][(2 * tig + j) % PT_ROWS][0];
-                    *reinterpret_cast<uint4*>(row + 4 * gid) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-                    *reinterpret_cast<uint4*>(row + 32 + 4 * gid) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                }
-            }
-        }
-    };
-    // P V of page d (stage st) with P^T[st]; fresh = its item's first page
-    // P V of a page (stage st) with P^T[st]; fresh = its item's first page
-    struct PvRegs {
-        float vaux[4], vaux2[4];
-    };
-    auto pv_head = [&](bool fresh, const float (&corr)[2], int st, uint32_t phase) {
-        mbar_wait(&sm.vfull[st], phase);
-        // an item's first page zeroes the running output (factor 0); later
-        // pages rescale it only when a real column's max moved (warp vote;
-        // rare under lazy rescaling).  One in-place multiply path: no copies.
-        const float c0 = fresh ? 0.f : corr[0], c1 = fresh ? 0.f : corr[1];
-        if (__any_sync(0xffffffffu, fresh || (real0 && c0 != 1.f) || (real1 && c1 != 1.f))) {
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                oacc[m][0] *= c0;
-                oacc[m][2] *= c0;
-                oacc[m][1] *= c1;
-                oacc[m][3] *= c1;
-            }
-        }
-    };
-    auto pv_step = [&](int st, int ks, PvRegs& r) {
-        const uint8_t* vp = vslots + st * vslot;
-        const uint8_t* vscale = vp + G * D / 4;
-        const uint8_t* vzero = vscale + 2 * G;
-        const uint8_t* vsbase = main_col ? vscale : reinterpret_cast<const uint8_t*>(sm.ones);
-        const uint32_t* ptr = &sm.pt[st][prow_ok ? prow : 0][tig];
-        const int t0 = 16 * ks + 2 * tig;
-        // p = 2^x of the stored exponents (ex2.approx.f16x2: one MUFU per two
-        // tokens, and the f16 exponent costs |p error| < 2e-4 at p <= 2^kLazy)
-        const uint32_t pp0 = prow_ok ? ex2_h2(ptr[8 * ks]) : 0u;      // tokens 16 ks + 2 tig (+1)
-        const uint32_t pp1 = prow_ok ? ex2_h2(ptr[8 * ks + 4]) : 0u;  // tokens 16 ks + 8 + 2 tig (+1)
-        const uint32_t b0 = hmul2(pp0, lds32(vsbase + 2 * t0));
-        const uint32_t b1 = hmul2(pp1, lds32(vsbase + 2 * (t0 + 8)));
-        uint32_t w0, w1, w2, w3;  // token rows 16 ks + [0, 16), channels 8 gid + [0, 8) / 64 + ...
-        ldsm_t4(smem_u32(vp) + 512 * ks + ldsm_off, w0, w1, w2, w3);
-        const uint32_t z0 = lds32(vzero + 2 * t0);
-        const uint32_t z1 = lds32(vzero + 2 * (t0 + 8));
-        mma_ldsm(kc, oacc, w0, w1, w2, w3, b0, b1);
-        if (ks == 0)
-            mma16816_z(r.vaux, kOnes, z0, kOnes, z1, b0, b1);
-        else
-            mma16816(r.vaux, kOnes, z0, kOnes, z1, b0, b1);
-        if (kFull) {  // the unscaled p: sum p and sum p z
-            if (ks == 0)
-                mma16816_z(r.vaux2, kOnes, z0, kOnes, z1, pp0, pp1);
-            else
-                mma16816(r.vaux2, kOnes, z0, kOnes, z1, pp0, pp1);
-        }
-    };
-    auto pv_tail = [&](bool fresh, const float (&corr)[2], PvRegs& r) {
-        // vaux lanes 0-1: sum(p s) per column; lanes 2-3: sum(p) and sum(p z).
-        // Row constants (zero points, the 1024 offset) accumulate per column in
-        // ob[weight class] and are added at the flush.
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const float sBv = __shfl_sync(0xffffffffu, r.vaux[j], kFull ? tig : (tig & 1));
-            const float lp = kFull ? __shfl_sync(0xffffffffu, r.vaux2[j], tig) : __shfl_sync(0xffffffffu, r.vaux[j], 2 + (tig & 1));
-            const float zz = kFull ? __shfl_sync(0xffffffffu, r.vaux2[2 + j], tig)
-                                   : __shfl_sync(0xffffffffu, r.vaux[2 + j], 2 + (tig & 1));
-            const float cf = fresh ? 0.f : corr[j];
-            ol[j] = fmaf(ol[j], cf, lp);
-            ob[0][j] = fmaf(ob[0][j], cf, zz - 256.f * sBv);  // w 4
-            ob[1][j] = fmaf(ob[1][j], cf, zz - 64.f * sBv);   // w 16
-            ob[2][j] = fmaf(ob[2][j], cf, zz - 16.f * sBv);   // w 64
-            ob[3][j] = fmaf(ob[3][j], cf, zz - 4.f * sBv);    // w 256
-        }
-    };
-    auto flush = [&](const Pg& d, const float (&mnew)[2]) {
-        float* base = P.part + ((int64_t)d.u * P.nslot + d.slot) * part_stride(GROUP);
-        if (kFull || tig < 2) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int g = 2 * tig + j;
-                if (g < GROUP) {
-                    // tile m: row gid = channel 8 gid + m, row gid + 8 = channel 64 + 8 gid + m
-                    float lo[8], hi[8];
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) {
-                        lo[m] = fmaf(oacc[m][j], 1.f / tile_w(m), ob[tile_c(m)][j]);
-                        hi[m] = fmaf(oacc[m][2 + j], 1.f / tile_w(m), ob[tile_c(m)][j]);
-                    }
-                    float4* o4 = reinterpret_cast<float4*>(base + g * D + 8 * gid);
-                    o4[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
-                    o4[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
-                    float4* h4 = reinterpret_cast<float4*>(base + g * D + 64 + 8 * gid);
-                    h4[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                    h4[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
-                    if (gid == 0) *reinterpret_cast<float2*>(base + GROUP * D + 2 * g) = make_float2(mnew[j], ol[j]);
-                }
-            }
-        }
-    };
-
-    // ---- software pipeline: QK of page k + 1 beside PV of page k ----
-    Pg d0 = next_page();
-    fill_ks(d0);
-    fill_vs(d0);
-    if (d0.u >= 0) {
-        Pg d1 = next_page();
-        fill_ks(d1);
-        fill_vs(d1);
-        Pg d2 = next_page();
-        fill_ks(d2);
-        fill_vs(d2);
-        issue_key(d0, 0);
-        issue_val(d0, 0);
-        issue_key(d1, 1);
-        issue_val(d1, 1);
-        prefetch_q(d1, d0.u);
-        prefetch_q(d2, d1.u);
-        float corr0[2], mnew0[2];
-        {
-            qk_prologue(d0, 0, 0);
-            QkRegs qr;
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) qk_step(0, ks, qr);
-            qk_tail(0, qr, corr0, mnew0);
-        }
-        __syncwarp();
-        issue_key(d2, 0);  // key slot 0 is free once QK(0) is done
-        // steady state: one path (QK of page k + 1 beside PV of page k), so the
-        // output accumulators keep their registers across the back edge
-        uint32_t k = 0;
-#pragma unroll 1
-        for (; d1.u >= 0; ++k) {
-            const int st = k & 1;
-            const bool fresh0 = d0.p == (d0.pq >> 16), last0 = d0.p + 1 == (d0.pq & 0xffff);
-            fill_vs(d2);          // before the stream may move to another item
-            Pg d3 = next_page();  // page k + 3: its key goes into key slot st ^ 1 after QK(k + 1)
-            prefetch_q(d3, d2.u);
-            float corr1[2], mnew1[2];
-            PvRegs pr;
-            qk_prologue(d1, st ^ 1, ((k + 1) >> 1) & 1);
-            pv_head(fresh0, corr0, st, (k >> 1) & 1);
-            QkRegs qr;
-            // the two pages' k-steps alternate: independent chains for the scheduler
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                pv_step(st, ks, pr);
-                qk_step(st ^ 1, ks, qr);
-            }
-            pv_tail(fresh0, corr0, pr);
-            qk_tail(st ^ 1, qr, corr1, mnew1);
-            if (last0) flush(d0, mnew0);
-            __syncwarp();
-            fill_ks(d3);
-            issue_val(d2, st);     // value slot st (page k) -> page k + 2
-            issue_key(d3, st ^ 1);  // key slot st ^ 1 (page k + 1) -> page k + 3
-            d0 = d1;
-            d1 = d2;
-            d2 = d3;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                corr0[j] = corr1[j];
-                mnew0[j] = mnew1[j];
-            }
-        }
-        {  // the stream's last page: P V only
-            const int st = k & 1;
-            const bool fresh0 = d0.p == (d0.pq >> 16);
-            PvRegs pr;
-            pv_head(fresh0, corr0, st, (k >> 1) & 1);
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) pv_step(st, ks, pr);
-            pv_tail(fresh0, corr0, pr);
-            flush(d0, mnew0);  // a stream's last page is its item's last
-        }
-    }
-    if (P.fp_first) {
-        // this warp's stream is drained: the merge grid (our programmatic
-        // dependent; its CTAs wait for this grid) may take freed SM slots
-        asm volatile("griddepcontrol.launch_dependents;");
-        asm volatile("griddepcontrol.wait;" ::: "memory");  // the fp grid is complete
-    }
-    // the last warp out resets the work queue for the next launch (after its
-    // outstanding ticket returned: using its value orders the atomics)
-    if (lane == 0) {
-        asm volatile("" ::"r"(tk) : "memory");
-        const int fin = atomicAdd(&P.ctr[1], 1);
-        if (fin == static_cast<int>(gridDim.x) * kWarps - 1) {
-            P.ctr[0] = 0;
-            P.ctr[1] = 0;
-        }
-    }
-}
-
-// Warp-specialised variant (KITTY_WS): each page stream is served by a QK
-// warp and a PV warp, 16 warps per SM at <= 128 registers.
-template <int GROUP, int NKH>
-__global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(Params P) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    constexpr int PT_ROWS = GROUP == 8 ? 8 : 4;
-    using Fixed = PairFixedT<PT_ROWS>;
-    const KittyCacheDesc& c = P.c;
-    const int kslot = static_cast<int>(c.key_slot_bytes);
-    const int vslot = static_cast<int>(c.value_slot_bytes);
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int gid = lane >> 2, tig = lane & 3;
-    // warps [0, kWsPairs): QK + softmax of their pair's page stream; warps
-    // [kWsPairs, 2 kWsPairs): P V of the same stream, one page behind
-    const int pair = warp & (kWsPairs - 1);
-    const bool qk_role = warp < kWsPairs;
-    const int wbytes = pair_smem_bytes<GROUP>(kslot, vslot);
+    // WS: warps [0, kWsPairs) run QK + softmax of their pair's page stream,
+    // warps [kWsPairs, 2 kWsPairs) P V of the same stream, one page behind
+    const int pair = WS ? (warp & (kWsPairs - 1)) : warp;  // the page stream within the CTA
+    const bool qk_role = !WS || warp < kWsPairs;
+    const int wbytes = WS ? pair_smem_bytes<GROUP>(kslot, vslot) : warp_smem_bytes<GROUP>(kslot, vslot);
     uint8_t* const wbase = smem_raw + pair * wbytes;
     Fixed& sm = *reinterpret_cast<Fixed*>(wbase);
-    uint8_t* const kslots = wbase + pair_fixed_bytes<GROUP>();
+    uint8_t* const kslots = wbase + (WS ? pair_fixed_bytes<GROUP>() : warp_fixed_bytes<GROUP>());
     uint8_t* const vslots = kslots + 2 * kslot;
     // group <= 4: B columns 0-3 are the queries, 4-7 auxiliary (unscaled q / p);
     // group 8: all eight are queries and the auxiliary sums take a second MMA
@@ -885,12 +391,16 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
             for (int i = 0; i < 2; ++i) {
                 mbar_init(&sm.kfull[i], 1);
                 mbar_init(&sm.vfull[i], 1);
-                mbar_init(&sm.pfull[i], 1);
-                mbar_init(&sm.pempty[i], 1);
+                if constexpr (WS) {
+                    mbar_init(&sm.pfull[i], 1);
+                    mbar_init(&sm.pempty[i], 1);
+                }
             }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            mbar_arrive(&sm.pempty[0]);  // both P^T stages start free
-            mbar_arrive(&sm.pempty[1]);
+            if constexpr (WS) {
+                mbar_arrive(&sm.pempty[0]);  // both P^T stages start free
+                mbar_arrive(&sm.pempty[1]);
+            }
         }
         sm.ones[lane] = kOnes;
         sm.ones[lane + 32] = kOnes;
@@ -907,7 +417,7 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
         asm volatile("griddepcontrol.launch_dependents;");
     }
     // per-CTA copy of the unit lengths: an item's decode reads shared memory
-    int* s_ulen = reinterpret_cast<int*>(smem_raw + wbytes * kWsPairs);
+    int* s_ulen = reinterpret_cast<int*>(smem_raw + wbytes * (WS ? kWsPairs : kWarps));
     const bool len_table = P.units <= kMaxTableUnits;
     if (len_table) {
         for (int i = threadIdx.x; i < P.units; i += blockDim.x) s_ulen[i] = min(__ldcg(c.unit_len + i), P.max_tokens);
@@ -1007,7 +517,15 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
     };
 
     const Consts kc;
-    uint32_t pe_phase = 0;  // parity of the P^T stage's release the QK tail waits for
+    uint32_t pe_phase = 0;  // WS: parity of the P^T stage release the QK tail waits for
+    // a stage barrier wait: spinning (one warp per stream: its own data), or
+    // with a suspend hint (WS: a warp waiting on its partner)
+    auto bar_wait = [&](unsigned long long* bar, uint32_t ph) {
+        if constexpr (WS)
+            mbar_wait_sleep(bar, ph);
+        else
+            mbar_wait(bar, ph);
+    };
     // ---- QK side state: q fragments of its unit, running max of its item ----
     int cur_unit = -1;
     uint32_t qa[8][2];
@@ -1043,7 +561,7 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
             }
         }
         if (d.p == (d.pq >> 16)) om[0] = om[1] = -INFINITY;  // an item's first page
-        mbar_wait_sleep(&sm.kfull[st], phase);
+        bar_wait(&sm.kfull[st], phase);
         if (NKH > 0) {  // boosted rows -> channels (inverse of boost_idx)
             const uint8_t* kp = kslots + st * kslot;
             const uint32_t bw = lds32(kp + D * G / 4 + d_boost * G / 4 + 4 * lane);
@@ -1149,9 +667,9 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) bw[c4][j] -= mnew[j];
         }
-        // P^T[st] is free once the PV warp is done with page k - 2
-        mbar_wait_sleep(&sm.pempty[st], pe_phase);
-        // probabilities (log2 domain) to P^T[st]: row = query, token t at word
+        // WS: P^T[st] is free once the PV warp is done with page k - 2
+        if constexpr (WS) mbar_wait_sleep(&sm.pempty[st], pe_phase);
+        // exponents (log2 domain, x - max) to P^T[st]: row = query, token t at word
         // t / 2 (half t % 2); this lane's tokens 8 gid + m (words 4 gid ..) and
         // 64 + 8 gid + m (words 32 + 4 gid ..), two 16-byte stores each
         if (kFull || tig < 2) {
@@ -1163,7 +681,7 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
                     for (int m = 0; m < 8; m += 2) {
                         const float w0 = 1.f / tile_w(m), w1 = 1.f / tile_w(m + 1);
                         const int c0 = tile_c(m), c1 = tile_c(m + 1);
-                        // the exponent x (<= kLazy) as f16: the PV warp takes ex2.f16x2 of it
+                        // the exponent x (<= kLazy) as f16: P V takes ex2.f16x2 of it
                         lo[m / 2] = pack_f16x2(fmaf(acc[m][j], w0, bw[c0][j]), fmaf(acc[m + 1][j], w1, bw[c1][j]));
                         hi[m / 2] = pack_f16x2(fmaf(acc[m][2 + j], w0, bw[c0][j]), fmaf(acc[m + 1][2 + j], w1, bw[c1][j]));
                     }
@@ -1180,7 +698,7 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
         float vaux[4], vaux2[4];
     };
     auto pv_head = [&](bool fresh, const float (&corr)[2], int st, uint32_t phase) {
-        mbar_wait_sleep(&sm.vfull[st], phase);
+        bar_wait(&sm.vfull[st], phase);
         // an item's first page zeroes the running output (factor 0); later
         // pages rescale it only when a real column's max moved (warp vote;
         // rare under lazy rescaling).  One in-place multiply path: no copies.
@@ -1202,7 +720,8 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
         const uint8_t* vsbase = main_col ? vscale : reinterpret_cast<const uint8_t*>(sm.ones);
         const uint32_t* ptr = &sm.pt[st][prow_ok ? prow : 0][tig];
         const int t0 = 16 * ks + 2 * tig;
-        // p = 2^x of the exponents the QK warp stored (f16x2; |error| < 2e-4 for p <= 4)
+        // p = 2^x of the stored exponents (ex2.approx.f16x2: one MUFU per two
+        // tokens, and the f16 exponent costs |p error| < 2e-4 at p <= 2^kLazy)
         const uint32_t pp0 = prow_ok ? ex2_h2(ptr[8 * ks]) : 0u;      // tokens 16 ks + 2 tig (+1)
         const uint32_t pp1 = prow_ok ? ex2_h2(ptr[8 * ks + 4]) : 0u;  // tokens 16 ks + 8 + 2 tig (+1)
         const uint32_t b0 = hmul2(pp0, lds32(vsbase + 2 * t0));
@@ -1267,92 +786,176 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
         }
     };
 
-    // ---- the pair's pipeline: QK warp on page k while the PV warp runs page
-    // k - 1.  Stage st = k & 1 holds page k's key slot, value slot, P^T and job;
-    // pfull[st]: the QK warp published page k (P^T, corrections, job);
-    // pempty[st]: the PV warp is done with it (P^T, job, value slot) ----
-    if (qk_role) {
+    if constexpr (!WS) {
+        // ---- software pipeline: QK of page k + 1 beside PV of page k ----
         Pg d0 = next_page();
         fill_ks(d0);
         fill_vs(d0);
-        Pg d1 = next_page();
-        fill_ks(d1);
-        fill_vs(d1);
-        issue_key(d0, 0);
-        issue_val(d0, 0);
-        issue_key(d1, 1);
-        issue_val(d1, 1);
-        prefetch_q(d1, d0.u);
-        uint32_t k = 0;
-#pragma unroll 1
-        for (; d0.u >= 0; ++k) {
-            const int st = k & 1;
-            const uint32_t ph = (k >> 1) & 1;
-            float corr[2], mnew[2];
-            qk_prologue(d0, st, ph);
-            pe_phase = ph;
-            QkRegs qr;
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) qk_step(st, ks, qr);
-            qk_tail(st, qr, corr, mnew);
-            Pg d2 = next_page();  // page k + 2: key slot st, value slot st
+        if (d0.u >= 0) {
+            Pg d1 = next_page();
+            fill_ks(d1);
+            fill_vs(d1);
+            Pg d2 = next_page();
             fill_ks(d2);
             fill_vs(d2);
+            issue_key(d0, 0);
+            issue_val(d0, 0);
+            issue_key(d1, 1);
+            issue_val(d1, 1);
+            prefetch_q(d1, d0.u);
             prefetch_q(d2, d1.u);
-            if (gid == 0) {
-                sm.corr[st][2 * tig] = corr[0];
-                sm.corr[st][2 * tig + 1] = corr[1];
-                sm.mnew[st][2 * tig] = mnew[0];
-                sm.mnew[st][2 * tig + 1] = mnew[1];
+            float corr0[2], mnew0[2];
+            {
+                qk_prologue(d0, 0, 0);
+                QkRegs qr;
+    #pragma unroll
+                for (int ks = 0; ks < 8; ++ks) qk_step(0, ks, qr);
+                qk_tail(0, qr, corr0, mnew0);
             }
-            if (lane == 0) {
-                sm.job[st][0] = d0.u;
-                sm.job[st][1] = d0.p;
-                sm.job[st][2] = d0.pq;
-                sm.job[st][3] = d0.slot;
-                sm.vnext[st] = d2.u >= 0 ? d2.vs : -1;
+            __syncwarp();
+            issue_key(d2, 0);  // key slot 0 is free once QK(0) is done
+            // steady state: one path (QK of page k + 1 beside PV of page k), so the
+            // output accumulators keep their registers across the back edge
+            uint32_t k = 0;
+    #pragma unroll 1
+            for (; d1.u >= 0; ++k) {
+                const int st = k & 1;
+                const bool fresh0 = d0.p == (d0.pq >> 16), last0 = d0.p + 1 == (d0.pq & 0xffff);
+                fill_vs(d2);          // before the stream may move to another item
+                Pg d3 = next_page();  // page k + 3: its key goes into key slot st ^ 1 after QK(k + 1)
+                prefetch_q(d3, d2.u);
+                float corr1[2], mnew1[2];
+                PvRegs pr;
+                qk_prologue(d1, st ^ 1, ((k + 1) >> 1) & 1);
+                pv_head(fresh0, corr0, st, (k >> 1) & 1);
+                QkRegs qr;
+                // the two pages' k-steps alternate: independent chains for the scheduler
+    #pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    pv_step(st, ks, pr);
+                    qk_step(st ^ 1, ks, qr);
+                }
+                pv_tail(fresh0, corr0, pr);
+                qk_tail(st ^ 1, qr, corr1, mnew1);
+                if (last0) flush(d0, mnew0);
+                __syncwarp();
+                fill_ks(d3);
+                issue_val(d2, st);     // value slot st (page k) -> page k + 2
+                issue_key(d3, st ^ 1);  // key slot st ^ 1 (page k + 1) -> page k + 3
+                d0 = d1;
+                d1 = d2;
+                d2 = d3;
+    #pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    corr0[j] = corr1[j];
+                    mnew0[j] = mnew1[j];
+                }
             }
+            {  // the stream's last page: P V only
+                const int st = k & 1;
+                const bool fresh0 = d0.p == (d0.pq >> 16);
+                PvRegs pr;
+                pv_head(fresh0, corr0, st, (k >> 1) & 1);
+    #pragma unroll
+                for (int ks = 0; ks < 8; ++ks) pv_step(st, ks, pr);
+                pv_tail(fresh0, corr0, pr);
+                flush(d0, mnew0);  // a stream's last page is its item's last
+            }
+        }
+        if (P.fp_first) {
+            // this warp's stream is drained: the merge grid (our programmatic
+            // dependent; its CTAs wait for this grid) may take freed SM slots
+            asm volatile("griddepcontrol.launch_dependents;");
+            asm volatile("griddepcontrol.wait;" ::: "memory");  // the fp grid is complete
+        }
+    } else {
+        // ---- the pair's pipeline: QK warp on page k while the PV warp runs page
+        // k - 1.  Stage st = k & 1 holds page k's key slot, value slot, P^T and job;
+        // pfull[st]: the QK warp published page k (P^T, corrections, job);
+        // pempty[st]: the PV warp is done with it (P^T, job, value slot) ----
+        if (qk_role) {
+            Pg d0 = next_page();
+            fill_ks(d0);
+            fill_vs(d0);
+            Pg d1 = next_page();
+            fill_ks(d1);
+            fill_vs(d1);
+            issue_key(d0, 0);
+            issue_val(d0, 0);
+            issue_key(d1, 1);
+            issue_val(d1, 1);
+            prefetch_q(d1, d0.u);
+            uint32_t k = 0;
+    #pragma unroll 1
+            for (; d0.u >= 0; ++k) {
+                const int st = k & 1;
+                const uint32_t ph = (k >> 1) & 1;
+                float corr[2], mnew[2];
+                qk_prologue(d0, st, ph);
+                pe_phase = ph;
+                QkRegs qr;
+    #pragma unroll
+                for (int ks = 0; ks < 8; ++ks) qk_step(st, ks, qr);
+                qk_tail(st, qr, corr, mnew);
+                Pg d2 = next_page();  // page k + 2: key slot st, value slot st
+                fill_ks(d2);
+                fill_vs(d2);
+                prefetch_q(d2, d1.u);
+                if (gid == 0) {
+                    sm.corr[st][2 * tig] = corr[0];
+                    sm.corr[st][2 * tig + 1] = corr[1];
+                    sm.mnew[st][2 * tig] = mnew[0];
+                    sm.mnew[st][2 * tig + 1] = mnew[1];
+                }
+                if (lane == 0) {
+                    sm.job[st][0] = d0.u;
+                    sm.job[st][1] = d0.p;
+                    sm.job[st][2] = d0.pq;
+                    sm.job[st][3] = d0.slot;
+                    sm.vnext[st] = d2.u >= 0 ? d2.vs : -1;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.pfull[st]);
+                issue_key(d2, st);  // QK(k) is done with key slot st
+                d0 = d1;
+                d1 = d2;
+            }
+            // end of the stream: an empty job once the PV warp released the stage
+            const int st = k & 1;
+            mbar_wait_sleep(&sm.pempty[st], (k >> 1) & 1);
+            if (lane == 0) sm.job[st][0] = -1;
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.pfull[st]);
-            issue_key(d2, st);  // QK(k) is done with key slot st
-            d0 = d1;
-            d1 = d2;
-        }
-        // end of the stream: an empty job once the PV warp released the stage
-        const int st = k & 1;
-        mbar_wait_sleep(&sm.pempty[st], (k >> 1) & 1);
-        if (lane == 0) sm.job[st][0] = -1;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.pfull[st]);
-    } else {
-        uint32_t k = 0;
-#pragma unroll 1
-        for (;; ++k) {
-            const int st = k & 1;
-            const uint32_t ph = (k >> 1) & 1;
-            mbar_wait_sleep(&sm.pfull[st], ph);
-            Pg d;
-            d.u = sm.job[st][0];
-            if (d.u < 0) break;
-            d.p = sm.job[st][1];
-            d.pq = sm.job[st][2];
-            d.slot = sm.job[st][3];
-            const int vs2 = sm.vnext[st];
-            const float corr[2] = {sm.corr[st][2 * tig], sm.corr[st][2 * tig + 1]};
-            const float mnew[2] = {sm.mnew[st][2 * tig], sm.mnew[st][2 * tig + 1]};
-            const bool fresh = d.p == (d.pq >> 16), last = d.p + 1 == (d.pq & 0xffff);
-            PvRegs pr;
-            pv_head(fresh, corr, st, ph);
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) pv_step(st, ks, pr);
-            pv_tail(fresh, corr, pr);
-            if (last) flush(d, mnew);
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&sm.pempty[st]);
-                if (vs2 >= 0) {  // value slot st -> page k + 2
-                    mbar_expect_tx(&sm.vfull[st], vslot);
-                    bulk_g2s(vslots + st * vslot, c.value_pool + (int64_t)vs2 * vslot, vslot, &sm.vfull[st], pol);
+        } else {
+            uint32_t k = 0;
+    #pragma unroll 1
+            for (;; ++k) {
+                const int st = k & 1;
+                const uint32_t ph = (k >> 1) & 1;
+                mbar_wait_sleep(&sm.pfull[st], ph);
+                Pg d;
+                d.u = sm.job[st][0];
+                if (d.u < 0) break;
+                d.p = sm.job[st][1];
+                d.pq = sm.job[st][2];
+                d.slot = sm.job[st][3];
+                const int vs2 = sm.vnext[st];
+                const float corr[2] = {sm.corr[st][2 * tig], sm.corr[st][2 * tig + 1]};
+                const float mnew[2] = {sm.mnew[st][2 * tig], sm.mnew[st][2 * tig + 1]};
+                const bool fresh = d.p == (d.pq >> 16), last = d.p + 1 == (d.pq & 0xffff);
+                PvRegs pr;
+                pv_head(fresh, corr, st, ph);
+    #pragma unroll
+                for (int ks = 0; ks < 8; ++ks) pv_step(st, ks, pr);
+                pv_tail(fresh, corr, pr);
+                if (last) flush(d, mnew);
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm.pempty[st]);
+                    if (vs2 >= 0) {  // value slot st -> page k + 2
+                        mbar_expect_tx(&sm.vfull[st], vslot);
+                        bulk_g2s(vslots + st * vslot, c.value_pool + (int64_t)vs2 * vslot, vslot, &sm.vfull[st], pol);
+                    }
                 }
             }
         }
@@ -1362,7 +965,7 @@ __global__ void __launch_bounds__(2 * kWsPairs * 32, kCtasPerSm) page_ws_kernel(
     if (qk_role && lane == 0) {
         asm volatile("" ::"r"(tk) : "memory");
         const int fin = atomicAdd(&P.ctr[1], 1);
-        if (fin == static_cast<int>(gridDim.x) * kWsPairs - 1) {
+        if (fin == static_cast<int>(gridDim.x) * (WS ? kWsPairs : kWarps) - 1) {
             P.ctr[0] = 0;
             P.ctr[1] = 0;
         }
@@ -1569,7 +1172,7 @@ static const int g_ws_env = [] {
 template <int GROUP, int NKH>
 static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
     const bool g_ws = g_ws_env >= 0 ? g_ws_env != 0 : GROUP == 8;
-    auto kfn = g_ws ? page_ws_kernel<GROUP, NKH> : page_kernel<GROUP, NKH>;
+    auto kfn = g_ws ? page_kernel<GROUP, NKH, true> : page_kernel<GROUP, NKH, false>;
     const int ks_b = (int)prm.c.key_slot_bytes, vs_b = (int)prm.c.value_slot_bytes;
     const size_t sm = (size_t)(g_ws ? pair_smem_bytes<GROUP>(ks_b, vs_b) * kWsPairs : warp_smem_bytes<GROUP>(ks_b, vs_b) * kWarps) +
                       (prm.units <= kMaxTableUnits ? 4 * prm.units : 0);
