@@ -1045,8 +1045,16 @@ __global__ void __launch_bounds__(WARPS * 32) combine_parts_kernel(Params P) {
     };
     const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
     const int64_t row = (int64_t)b * c.cfg.h_q + (int64_t)h * GROUP + g;
-    lse_merge_row<GROUP, decltype(slot_of), WARPS, CSPLIT>(P.part + (int64_t)u * P.nslot * kStride, kStride, nparts,
-                                                          slot_of, g, P.out, P.out_dtype, row, slice);
+    // 33-128 slots (4-warp CTAs): one pass, (m, l) loaded with the rows (C5
+    // 488.0 -> 478.0 us per layer, C2 equal); the 2-warp CTAs of short units
+    // (C3: 124.9 vs 123.7) and long contexts (C4: 37.7 vs 37.1) keep the max
+    // pass first
+    if constexpr (WARPS == 4)
+        lse_merge_row_1p<GROUP, decltype(slot_of), WARPS, CSPLIT>(P.part + (int64_t)u * P.nslot * kStride, kStride,
+                                                                 nparts, slot_of, g, P.out, P.out_dtype, row, slice);
+    else
+        lse_merge_row<GROUP, decltype(slot_of), WARPS, CSPLIT>(P.part + (int64_t)u * P.nslot * kStride, kStride, nparts,
+                                                              slot_of, g, P.out, P.out_dtype, row, slice);
 }
 
 }  // namespace fastattn

@@ -2,10 +2,14 @@
 //
 // A unit's work items each leave a partial record (acc[group][d] = sum p v
 // relative to the item's own running max m, then (m, l) per query row, m in
-// the log2 domain).  One CTA of kMergeWarps warps merges one (unit, query row):
-// the weights 2^(m - max) are computed first (thread = part), every warp sums
-// a strided subset of the accumulator rows, and warp 0 adds the warp sums and
-// writes out = acc / l -- the softmax normalisation of cache.py:243-248.
+// the log2 domain).  One CTA merges one (unit, query row) (or a channel slice
+// of it) into out = acc / l -- the softmax normalisation of cache.py:243-248:
+//  * lse_merge_row (long rows, hundreds of parts): the weights 2^(m - max)
+//    first (thread = part), then every warp sums a strided subset of the
+//    accumulator rows and warp 0 adds the warp sums;
+//  * lse_merge_row_1p (<= 128 parts): every lane group keeps a running
+//    (max, sum, acc) over its parts, loading (m, l) with the rows in one
+//    round trip, and the groups are combined by log-sum-exp at the end.
 #pragma once
 
 #include "kitty_common.cuh"
@@ -133,6 +137,97 @@ __device__ __forceinline__ void lse_merge_row(const float* pb, int stride, int n
         o.z += x.z;
         o.w += x.w;
         lt += s_lsum[w];
+    }
+    const float inv = 1.f / lt;
+    const int64_t ob = row * D + c0 + 4 * lane;
+    if (out_dtype == KITTY_F32) {
+        *reinterpret_cast<float4*>(static_cast<float*>(out) + ob) = make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
+    } else {
+        uint2 v;
+        v.x = f32_to_bf16_bits(o.x * inv) | (f32_to_bf16_bits(o.y * inv) << 16);
+        v.y = f32_to_bf16_bits(o.z * inv) | (f32_to_bf16_bits(o.w * inv) << 16);
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(out) + ob) = v;
+    }
+}
+
+// One-pass variant: every lane group keeps a running (max, sum, acc) over its
+// parts, loading each part's (m, l) together with its accumulator slice (one
+// round trip per F parts instead of a max pass and a row pass), then the
+// groups' partial states are combined by log-sum-exp in shared memory.
+template <int GROUP, class SlotFn, int WARPS, int CSPLIT = 1>
+__device__ __forceinline__ void lse_merge_row_1p(const float* pb, int stride, int nparts, SlotFn slot_of, int g,
+                                                 void* out, int out_dtype, int64_t row, int slice = 0) {
+    constexpr int D = 128;
+    constexpr int F = 8;                 // parts in flight per lane group
+    constexpr int LPP = 32 / CSPLIT;     // lanes per part slice
+    constexpr int NG = WARPS * CSPLIT;   // lane groups in the CTA
+    __shared__ float s_m[NG], s_l[NG];
+    __shared__ float4 s_acc[NG][LPP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane / LPP, cl = lane - sub * LPP;
+    const int grp = warp * CSPLIT + sub;
+    const int c0 = slice * (D / CSPLIT);
+    const float* rowp = pb + g * D + c0 + 4 * cl;
+    float m_run = -INFINITY, l_run = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i0 = grp; i0 < nparts; i0 += F * NG) {
+        float2 ml[F];
+        float4 a[F];
+#pragma unroll
+        for (int j = 0; j < F; ++j) {
+            const int i = i0 + j * NG;
+            if (i < nparts) {
+                const float* rec = pb + (int64_t)slot_of(i) * stride;
+                ml[j] = __ldcg(reinterpret_cast<const float2*>(rec + GROUP * D + 2 * g));
+                a[j] = __ldcg(reinterpret_cast<const float4*>(rowp + (rec - pb)));
+            } else {
+                ml[j] = make_float2(-INFINITY, 0.f);
+                a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        float mx = m_run;
+#pragma unroll
+        for (int j = 0; j < F; ++j) mx = fmaxf(mx, ml[j].x);
+        if (mx != -INFINITY) {
+            const float sc = m_run == -INFINITY ? 0.f : merge_ex2(m_run - mx);
+            acc.x *= sc;
+            acc.y *= sc;
+            acc.z *= sc;
+            acc.w *= sc;
+            l_run *= sc;
+#pragma unroll
+            for (int j = 0; j < F; ++j) {
+                const float w = ml[j].x == -INFINITY ? 0.f : merge_ex2(ml[j].x - mx);
+                l_run = fmaf(w, ml[j].y, l_run);
+                acc.x = fmaf(w, a[j].x, acc.x);
+                acc.y = fmaf(w, a[j].y, acc.y);
+                acc.z = fmaf(w, a[j].z, acc.z);
+                acc.w = fmaf(w, a[j].w, acc.w);
+            }
+            m_run = mx;
+        }
+    }
+    if (cl == 0) {
+        s_m[grp] = m_run;
+        s_l[grp] = l_run;
+    }
+    s_acc[grp][cl] = acc;
+    __syncthreads();
+    if (warp != 0 || lane >= LPP) return;
+    float M = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < NG; ++q) M = fmaxf(M, s_m[q]);
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    float lt = 0.f;
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {
+        const float w = s_m[q] == -INFINITY ? 0.f : merge_ex2(s_m[q] - M);
+        const float4 x = s_acc[q][lane];
+        o.x = fmaf(w, x.x, o.x);
+        o.y = fmaf(w, x.y, o.y);
+        o.z = fmaf(w, x.z, o.z);
+        o.w = fmaf(w, x.w, o.w);
+        lt = fmaf(w, s_l[q], lt);
     }
     const float inv = 1.f / lt;
     const int64_t ob = row * D + c0 + 4 * lane;
