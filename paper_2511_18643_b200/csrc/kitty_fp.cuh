@@ -53,7 +53,18 @@ constexpr int kRowH = D + 8;  // f16 per staged row (272 B: conflict-free ldmatr
 // value tiles and the page barrier -- ~22 KB at d_boost 16, so two chunk CTAs
 // fit beside the page kernel's two CTAs on an SM.
 __host__ __device__ inline int tc_kbuf_bytes(int kslot) { return (kslot + 127) & ~127; }
-__host__ __device__ inline int tc_scratch_bytes(int kslot) { return tc_kbuf_bytes(kslot) + 2 * kChunk * kRowH * 2 + 64; }
+constexpr int kTileBytes = kChunk * kRowH * 2;  // one f16 row tile
+// Union layout (un): when no chunk mixes staged and paged keys (S and R
+// multiples of 32 at G = 128: every chunk is all-sink / all-q-buffer, or lies
+// in one key page), the key page and the key tile share their bytes, and the
+// boost inverse map sits after the value tile -- 17.6 instead of 22.8 KB, so
+// more chunk CTAs are resident per SM.
+__host__ __device__ inline int tc_front_bytes(int kslot, bool un) {
+    return un ? (tc_kbuf_bytes(kslot) > kTileBytes ? tc_kbuf_bytes(kslot) : kTileBytes) : tc_kbuf_bytes(kslot) + kTileBytes;
+}
+__host__ __device__ inline int tc_scratch_bytes(int kslot, bool un = false) {
+    return tc_front_bytes(kslot, un) + kTileBytes + (un ? 128 : 0) + 64;
+}
 
 __device__ __forceinline__ uint32_t f2h2(float lo, float hi) {
     uint32_t r;
@@ -212,16 +223,17 @@ __device__ __forceinline__ void qk_from_codes(const uint8_t* kbuf, int d_boost, 
 
 template <int GROUP>
 __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part, int nslot, int stride,
-                         uint8_t* scratch, int u, int fc, int max_tokens) {
+                         uint8_t* scratch, int u, int fc, int max_tokens, bool un) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const int S = c.cfg.s, W = c.cfg.r + c.cfg.g, d_boost = c.cfg.d_boost;
     const int kslot = static_cast<int>(c.key_slot_bytes);
     const int scale_off = D * G / 4 + d_boost * G / 4 + D, zero_off = scale_off + 2 * D;
     uint8_t* kbuf = scratch;
-    uint16_t* kt = reinterpret_cast<uint16_t*>(scratch + tc_kbuf_bytes(kslot));  // [32][kRowH] f16 keys
-    uint16_t* vt = kt + kChunk * kRowH;                                          // [32][kRowH] f16 values
-    uint64_t* bar = reinterpret_cast<uint64_t*>(vt + kChunk * kRowH);
+    uint16_t* kt = reinterpret_cast<uint16_t*>(scratch + (un ? 0 : tc_kbuf_bytes(kslot)));  // [32][kRowH] f16 keys
+    uint16_t* vt = reinterpret_cast<uint16_t*>(scratch + tc_front_bytes(kslot, un));       // [32][kRowH] f16 values
+    uint8_t* inv_buf = un ? reinterpret_cast<uint8_t*>(vt + kChunk * kRowH) : reinterpret_cast<uint8_t*>(kt);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(vt + kChunk * kRowH) + (un ? 128 : 0));
     // after the dequantisation (a __syncthreads) the key page is dead: logits
     // and P^T live in its bytes (4.5 KB <= the slot)
     float* lgs = reinterpret_cast<float*>(kbuf);                   // [4][32][8] partial logits
@@ -294,7 +306,7 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
         const int pbase = vbase - S + c0 - s_len;
         const int off0 = pbase - pg_lo * G;
         if (pg_lo == pg_hi && c0 >= s_len && pbase + cnt - 1 < gm.kp * G && (off0 & 15) == 0 && off0 + kChunk <= G) {
-            uint8_t* inv = reinterpret_cast<uint8_t*>(kt);  // the key tile is not needed
+            uint8_t* inv = inv_buf;  // the key tile is not needed (or shares the page's bytes)
             if (tid == 0) page_wait(bar, 0);
             __syncthreads();
             if (tid < D) {
@@ -379,6 +391,7 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
             hmma(acc, a0, a1, a2, a3, b0, b1);
         }
         // acc: rows (tokens) 16 mrow + gid / + 8, columns 2 tig, 2 tig + 1
+        if (un) __syncthreads();  // the logits overwrite the key tile every warp was reading
         float* lg = lgs + khalf * kChunk * 8;
         *reinterpret_cast<float2*>(lg + (16 * mrow + gid) * 8 + 2 * tig) = make_float2(acc[0], acc[1]);
         *reinterpret_cast<float2*>(lg + (16 * mrow + 8 + gid) * 8 + 2 * tig) = make_float2(acc[2], acc[3]);
