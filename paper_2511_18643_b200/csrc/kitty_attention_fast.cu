@@ -1088,10 +1088,11 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     const int maxp = past / G + 1;
     const long long pages = (long long)p.units * maxp;
     const long long streams = (long long)num_sms() * kCtasPerSm * kWarps;  // concurrent page streams (warps)
-    static int ppc_max = 8, cs1_div = 4, ppc_div = 2, inited = 0;  // ppc_max <= 32: an item's pages fit the lanes
+    static int ppc_max = 8, cs1_div = 4, ppc_div = 2, inited = 0, swept = 0;  // ppc_max <= 32: an item's pages fit the lanes
     if (!inited) {
         inited = 1;
         if (const char* e = getenv("KITTY_SCHED")) {  // experiments: "l1,l2,ppc_max,cs1_div[,ppc_div]"
+            swept = 1;
             sscanf(e, "%d,%d,%d,%d,%d", &h_lvl[0], &h_lvl[1], &ppc_max, &cs1_div, &ppc_div);
             ppc_div = ppc_div < 1 ? 1 : ppc_div;
             ppc_max = ppc_max < 1 ? 1 : (ppc_max > 32 ? 32 : ppc_max);
@@ -1100,11 +1101,18 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
         }
     }
     int ppc = static_cast<int>(pages / (ppc_div * streams));
-    ppc = ppc < 1 ? 1 : (ppc > ppc_max ? ppc_max : ppc);
+    // Many pages per stream (C5: ~55): items up to 32 pages, level 1 in
+    // quarters of 8, levels from 940 / 985 per mille -- a third fewer partial
+    // records per unit, whose write + merge traffic (150 MB per C5 layer at the
+    // defaults, beyond L2) dominated the tail (C5 481.5 -> 442.6 us per layer;
+    // C2 / C3, ~14 pages per stream, keep the defaults: swept, tools/gpu_sched_sweep.sh)
+    const bool big = !swept && ppc >= 24;
+    const int pmax = big ? 32 : ppc_max, c1div = big ? 8 : cs1_div;
+    ppc = ppc < 1 ? 1 : (ppc > pmax ? pmax : ppc);
     p.ppc = ppc;
     p.cmax = (maxp + ppc - 1) / ppc;
     p.cs[0] = ppc;
-    p.cs[1] = ppc / cs1_div > 1 ? ppc / cs1_div : 1;
+    p.cs[1] = ppc / c1div > 1 ? ppc / c1div : 1;
     p.cs[2] = 1;
     // Level 0 in whole rounds: its items (ppc pages each, for units at the
     // longest length) are pulled round by round by the page streams; when
@@ -1113,7 +1121,7 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
     // of a stream's work -- as everyone else runs out, so level 0 shrinks to
     // the whole rounds (C4; with 3+ rounds, C3 / C5, the cut costs more than
     // the tail it removes).
-    for (int i = 0; i < 4; ++i) p.lvl[i] = h_lvl[i];
+    for (int i = 0; i < 4; ++i) p.lvl[i] = big ? (i % 2 == 0 ? 940 : 985) : h_lvl[i];
     {
         const int past_m = max_tokens > c.cfg.s ? max_tokens - c.cfg.s : 0;
         const int vpm = (past_m - min(c.cfg.r, past_m)) / G;
