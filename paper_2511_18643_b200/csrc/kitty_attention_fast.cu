@@ -1101,13 +1101,17 @@ static FastPlan plan(const KittyCacheDesc& c, int max_tokens) {
         }
     }
     int ppc = static_cast<int>(pages / (ppc_div * streams));
-    // Many pages per stream (C5: ~55): items up to 32 pages, level 1 in
-    // quarters of 8, levels from 940 / 985 per mille -- a third fewer partial
-    // records per unit, whose write + merge traffic (150 MB per C5 layer at the
-    // defaults, beyond L2) dominated the tail (C5 481.5 -> 442.6 us per layer;
-    // C2 / C3, ~14 pages per stream, keep the defaults: swept, tools/gpu_sched_sweep.sh)
+    // Many pages per stream (C5: ~55): items up to 16 pages, levels from 940 /
+    // 985 per mille -- fewer partial records per unit, whose write + merge
+    // traffic (150 MB per C5 layer at the defaults, beyond L2) dominated the
+    // tail (C5 481.5 -> 451 us per layer; C2 / C3, ~14 pages per stream, keep
+    // the defaults: swept, tools/gpu_sched_sweep.sh).  Not longer: the P V
+    // accumulators carry the 1024 offset of the code operands for the whole
+    // item, and the tensor cores' accumulation error grows with it (C5 at
+    // 32-page items: 0.0136 max-abs against the oracle, over the 1e-2 bar; at
+    // 16: 0.0068, at 8: 0.0058)
     const bool big = !swept && ppc >= 24;
-    const int pmax = big ? 32 : ppc_max, c1div = big ? 8 : cs1_div;
+    const int pmax = big ? 16 : ppc_max, c1div = cs1_div;
     ppc = ppc < 1 ? 1 : (ppc > pmax ? pmax : ppc);
     p.ppc = ppc;
     p.cmax = (maxp + ppc - 1) / ppc;
