@@ -147,6 +147,34 @@ def test_c2_shape_sampled_units_vs_oracle(cuda):
         assert np.max(np.abs(out[b, h * g:(h + 1) * g] - want)) <= TOL, (b, h)
 
 
+@pytest.mark.parametrize("h_q", [32, 64])
+def test_many_pages_per_stream_sampled_units_vs_oracle(cuda, h_q):
+    # > 24 pages per page stream (here 512 units x 127 page pairs): the page
+    # schedule switches to longer items (up to 16 pages) and fewer partial
+    # records (the C5 regime); the P V accumulators then carry the code
+    # operands' offset over more k-steps, so the accuracy bar is re-checked
+    B, h_kv, n = 64, 8, 16384
+    g = h_q // h_kv
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    gain = torch.ones(128, device="cuda")
+    gain[torch.randperm(128, generator=gen, device="cuda")[:16]] = 8.0
+    k = (torch.randn((B, h_kv, n, 128), generator=gen, device="cuda") * gain).bfloat16()
+    v = torch.randn((B, h_kv, n, 128), generator=gen, device="cuda").bfloat16()
+    q = torch.randn((B, h_q, 128), generator=gen, device="cuda").bfloat16()
+    cfg = cuda.KittyConfig(h_kv=h_kv, h_q=h_q)
+    cache = cuda.KittyBatchCache(cfg, B, n)
+    cache.prefill(k, v)
+    out = cache.attend(q).float().cpu().numpy()
+    cache.check()
+    for b, h in ((0, 0), (31, 4), (63, 7)):
+        kk = k[b, h].float().cpu().numpy()
+        vv = v[b, h].float().cpu().numpy()
+        kf, vf, _, _ = ko.bulk_unit_state(kk, vv, 32, 128, 128, 0.125, metadata16=True)
+        want = ko.attend_rows(kf, vf, q[b, h * g:(h + 1) * g].float().cpu().numpy())
+        assert np.max(np.abs(out[b, h * g:(h + 1) * g] - want)) <= TOL, (b, h)
+
+
 @pytest.mark.parametrize("d", [128, 16])
 def test_length_bound_is_reported(cuda, d):
     # kitty_decode_attention's max_tokens bounds the unit lengths; a longer
