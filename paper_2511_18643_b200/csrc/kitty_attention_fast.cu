@@ -134,6 +134,7 @@ struct Params {
     float* part;
     int fp_first;  // launch order: fp grid, page grid, merge (else page, fp, merge)
     int fp_union;  // fp chunk scratch: key page and key tile share bytes (kitty_fp.cuh)
+    int fp_warp;   // fp chunks one per warp (fp_warp_kernel) instead of one per CTA
 };
 
 // ---- small PTX helpers --------------------------------------------------------
@@ -998,6 +999,32 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
     if (!P.fp_first) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// The full-precision tokens in the aligned geometries (S a multiple of 32:
+// no chunk mixes staged and paged keys): one warp per 32-token chunk
+// (fptok::chunk_warp), kFpWarps chunks per CTA, no CTA-wide barrier.
+constexpr int kFpWarps = 2;
+__host__ __device__ inline int fpw_warp_bytes(int kslot) { return (fptok::cw_warp_bytes(kslot) + 127) & ~127; }
+template <int GROUP>
+__global__ void __launch_bounds__(kFpWarps * 32) fp_warp_kernel(Params P) {
+    extern __shared__ __align__(128) uint8_t fsm[];
+    const int warp = threadIdx.x >> 5;
+    const int it = blockIdx.x * kFpWarps + warp;
+    const int fc = it / P.units, u = it - fc * P.units;
+    if (P.fp_first) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;");
+    } else {
+        asm volatile("griddepcontrol.launch_dependents;");
+    }
+    if (fc < P.fmax) {
+        const fptok::Geom gm = fptok::geom(P.c, u, P.max_tokens);
+        if (gm.n > 0 && fc * kFpChunk < gm.nfp)
+            fptok::chunk_warp<GROUP>(P.c, P.q, P.part, P.nslot, part_stride(GROUP),
+                                     fsm + warp * fpw_warp_bytes((int)P.c.key_slot_bytes), u, fc, P.max_tokens);
+    }
+    if (!P.fp_first) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // K5: WARPS warps merge one (unit, query row): 2 when a unit has <= 32 partial
 // slots (short contexts: many small CTAs, one wave), 4 up to 128 slots, 16
 // above (long contexts).  CSPLIT CTAs share a row (channel slices) when the
@@ -1226,6 +1253,19 @@ static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
         return cudaLaunchKernelEx(&cfg, kfn, prm);
     };
     auto fp_grid = [&](cudaLaunchAttribute* a) {
+        if (prm.fp_warp) {
+            const int wsm = kFpWarps * fpw_warp_bytes((int)prm.c.key_slot_bytes);
+            cudaError_t e2 = set_kernel_smem((const void*)fp_warp_kernel<GROUP>, wsm, true);
+            if (e2 != cudaSuccess) return e2;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((prm.units * prm.fmax + kFpWarps - 1) / kFpWarps);
+            cfg.blockDim = dim3(kFpWarps * 32);
+            cfg.dynamicSmemBytes = wsm;
+            cfg.stream = st;
+            cfg.attrs = a;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, fp_warp_kernel<GROUP>, prm);
+        }
         const int fsm = fptok::tc_scratch_bytes((int)prm.c.key_slot_bytes, prm.fp_union != 0);
         cudaError_t e2 = set_kernel_smem((const void*)fp_tokens_kernel<GROUP>, fsm, true);
         if (e2 != cudaSuccess) return e2;
@@ -1320,6 +1360,8 @@ cudaError_t launch_fast_attention(const KittyCacheDesc& c, const uint16_t* q, vo
         // per step with the union layout, group 8 (C5) +0.4 % (kept apart)
         const bool aligned = c.cfg.s % kFpChunk == 0 && c.cfg.r % kFpChunk == 0;
         prm.fp_union = un_env >= 0 ? (un_env != 0 && aligned) : (aligned && p.group <= 4);
+        static const int fw_env = getenv("KITTY_FPWARP") ? atoi(getenv("KITTY_FPWARP")) : -1;
+        prm.fp_warp = fw_env >= 0 ? (fw_env != 0 && c.cfg.s % kFpChunk == 0) : (c.cfg.s % kFpChunk == 0);
     }
     prm.fp_first = g_fp_first >= 0 ? g_fp_first : ((long long)p.units * p.fmax > num_sms() ? 1 : 0);
     prm.max_tokens = max_tokens;

@@ -460,5 +460,285 @@ __device__ void chunk_tc(const KittyCacheDesc& c, const uint16_t* q, float* part
     }
 }
 
+// ---- one warp per 32-token chunk (the aligned geometries: no chunk mixes
+// staged and paged keys, i.e. S a multiple of 32) ----------------------------
+// Every lane fetches its token's bf16 K row (sink / key q-buffer chunks) and
+// V row straight into a padded shared tile with its own 1-D bulk copies (no
+// register staging, no conversion); QK runs as a bf16 MMA (q and K exact,
+// the 1 / sqrt(d) log2(e) scale applied to the fp32 logits), or from the 2-bit
+// codes for a chunk inside one key page (qk_codes_warp); the softmax keeps p
+// as a bf16 hi + lo pair so that P V runs as two bf16 MMAs at ~16-bit
+// precision.  No CTA-wide barrier: a chunk is one warp's work.
+__host__ __device__ inline int cw_front_bytes(int kslot) {
+    const int a = tc_kbuf_bytes(kslot) + 128;  // key page + boost inverse map
+    return ((a > kTileBytes ? a : kTileBytes) + 127) & ~127;
+}
+__host__ __device__ inline int cw_warp_bytes(int kslot) {
+    // front (key page | key tile), value tile, logits [32][8] f32, P^T hi / lo [8][40] bf16, barrier
+    return cw_front_bytes(kslot) + kTileBytes + kChunk * 8 * 4 + 2 * 8 * 40 * 2 + 64;
+}
+
+__device__ __forceinline__ void hmma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                          uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+
+// Logits of a chunk inside one key page from its 2-bit codes, all 128
+// channels by one warp (qk_from_codes' arithmetic: f16 1024 + w c operands,
+// B = q alpha s, offsets and zero points from the auxiliary MMA, boosted rows
+// as extra k-steps); lane gid's tokens are off0 + 4 gid + j.  Full logits to
+// lg[token][8].
+template <int GROUP>
+__device__ __forceinline__ void qk_codes_warp(const uint8_t* kbuf, int d_boost, int off0, const uint16_t* qbase,
+                                              const uint8_t* inv, float* lg) {
+    constexpr bool kFull = GROUP == 8;
+    const int lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const bool main_col = kFull || gid < 4;
+    const int qcol = kFull ? gid : (gid & 3);
+    const bool qok = qcol < GROUP;
+    const int scale_off = D * G / 4 + d_boost * G / 4 + D, zero_off = scale_off + 2 * D;
+    const uint32_t* kw = reinterpret_cast<const uint32_t*>(kbuf);
+    const int wi = (off0 >> 4) + (gid >> 2);
+    const uint32_t B = gid & 3;
+    const uint32_t sel = B | (B << 4) | ((4 + B) << 8) | ((4 + B) << 12);
+    const uint32_t m0 = 0x03000300u, m1 = 0x000C000Cu, m2 = 0x00300030u, m3 = 0x00C000C0u, magic = 0x64006400u;
+    const uint32_t ones = 0x3C003C00u;
+    const uint16_t* qg = qbase + (qok ? qcol : 0) * D;
+    float acc[2][4] = {}, aux[4] = {}, aux2[4] = {};
+    auto kstep = [&](const uint32_t* rows, int r0, uint32_t b0, uint32_t b1) {
+        const uint32_t w0 = rows[8 * r0 + wi], w1 = rows[8 * (r0 + 1) + wi];
+        const uint32_t w2 = rows[8 * (r0 + 8) + wi], w3 = rows[8 * (r0 + 9) + wi];
+        const uint32_t x = fprmt(w0, w1, sel), y = fprmt(w2, w3, sel);
+        hmma(acc[0], fand_or(x, m0, magic), fand_or(x, m1, magic), fand_or(y, m0, magic), fand_or(y, m1, magic), b0, b1);
+        hmma(acc[1], fand_or(x, m2, magic), fand_or(x, m3, magic), fand_or(y, m2, magic), fand_or(y, m3, magic), b0, b1);
+    };
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+        const int c0 = 16 * ks + 2 * tig;
+        uint32_t qa0 = 0u, qa1 = 0u;
+        if (qok) {
+            const uint32_t u0 = __ldg(reinterpret_cast<const uint32_t*>(qg + c0));
+            const uint32_t u1 = __ldg(reinterpret_cast<const uint32_t*>(qg + c0 + 8));
+            qa0 = f2h2(__uint_as_float(u0 << 16) * kAlpha, __uint_as_float(u0 & 0xffff0000u) * kAlpha);
+            qa1 = f2h2(__uint_as_float(u1 << 16) * kAlpha, __uint_as_float(u1 & 0xffff0000u) * kAlpha);
+        }
+        const uint32_t s0 = main_col ? *reinterpret_cast<const uint32_t*>(kbuf + scale_off + 2 * c0) : ones;
+        const uint32_t s1 = main_col ? *reinterpret_cast<const uint32_t*>(kbuf + scale_off + 2 * (c0 + 8)) : ones;
+        const uint32_t b0 = fhmul2(qa0, s0), b1 = fhmul2(qa1, s1);
+        const uint32_t z0 = *reinterpret_cast<const uint32_t*>(kbuf + zero_off + 2 * c0);
+        const uint32_t z1 = *reinterpret_cast<const uint32_t*>(kbuf + zero_off + 2 * (c0 + 8));
+        kstep(kw, c0, b0, b1);
+        hmma(aux, ones, z0, ones, z1, b0, b1);
+        if (kFull) hmma(aux2, ones, z0, ones, z1, qa0, qa1);
+    }
+    for (int hk = 0; 16 * hk < d_boost; ++hk) {  // boosted rows [16 hk, 16 hk + 16)
+        const int j0 = 16 * hk + 2 * tig;
+        auto qs = [&](int j) -> uint32_t {
+            if (j >= d_boost || !main_col || !qok) return 0u;
+            const int ch = inv[j];
+            const float qv = __uint_as_float(static_cast<uint32_t>(qg[ch]) << 16) * (4.f * kAlpha);
+            const uint16_t sv = *reinterpret_cast<const uint16_t*>(kbuf + scale_off + 2 * ch);
+            return __half_as_ushort(__hmul(__float2half_rn(qv), __ushort_as_half(sv)));
+        };
+        const uint32_t b0 = qs(j0) | (qs(j0 + 1) << 16), b1 = qs(j0 + 8) | (qs(j0 + 9) << 16);
+        kstep(kw + (D * G / 4) / 4, j0, b0, b1);
+        hmma(aux, ones, 0u, ones, 0u, b0, b1);
+    }
+    float sumB[2], cst[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        sumB[j] = __shfl_sync(0xffffffffu, aux[j], kFull ? tig : (tig & 1));
+        cst[j] = kFull ? __shfl_sync(0xffffffffu, aux2[2 + j], tig) : __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int g = 2 * tig + j;
+        if (g < GROUP && (kFull || tig < 2)) {
+            lg[(4 * gid + 0) * 8 + g] = fmaf(acc[0][j], 1.f / 256.f, cst[j] - 4.f * sumB[j]);
+            lg[(4 * gid + 1) * 8 + g] = fmaf(acc[0][2 + j], 1.f / 4.f, cst[j] - 256.f * sumB[j]);
+            lg[(4 * gid + 2) * 8 + g] = fmaf(acc[1][j], 1.f / 16.f, cst[j] - 64.f * sumB[j]);
+            lg[(4 * gid + 3) * 8 + g] = fmaf(acc[1][2 + j], 1.f / 64.f, cst[j] - 16.f * sumB[j]);
+        }
+    }
+}
+
+template <int GROUP>
+__device__ void chunk_warp(const KittyCacheDesc& c, const uint16_t* q, float* part, int nslot, int stride,
+                           uint8_t* scratch, int u, int fc, int max_tokens) {
+    const int lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int S = c.cfg.s, W = c.cfg.r + c.cfg.g, d_boost = c.cfg.d_boost;
+    const int kslot = static_cast<int>(c.key_slot_bytes);
+    uint8_t* kbuf = scratch;
+    uint16_t* kt = reinterpret_cast<uint16_t*>(scratch);  // [32][kRowH] bf16 keys (shares the page's bytes)
+    uint8_t* inv = scratch + tc_kbuf_bytes(kslot);
+    uint16_t* vt = reinterpret_cast<uint16_t*>(scratch + cw_front_bytes(kslot));  // [32][kRowH] bf16 values
+    float* lg = reinterpret_cast<float*>(vt + kChunk * kRowH);                     // [32][8] logits
+    uint16_t* pth = reinterpret_cast<uint16_t*>(lg + kChunk * 8);                  // [8][40] bf16 p hi
+    uint16_t* ptl = pth + 8 * 40;                                                  // [8][40] bf16 p lo
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ptl + 8 * 40);
+    const uint32_t bar_s = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    const Geom gm = geom(c, u, max_tokens);
+    const int s_len = min(gm.n, S);
+    const int c0 = fc * kChunk;
+    const int cnt = min(kChunk, gm.nfp - c0);
+    const int vbase = S + gm.vp * G;
+    const int b = u / c.cfg.h_kv, h = u - b * c.cfg.h_kv;
+    const uint16_t* qbase = q + ((int64_t)b * c.cfg.h_q + (int64_t)h * GROUP) * D;
+    // this chunk: all sink / key q-buffer tokens, or all inside key page pg
+    const int pbase = vbase - S + c0 - s_len;  // cache position of chunk token 0 (when c0 >= s_len)
+    const bool coded = c0 >= s_len && pbase < gm.kp * G;
+    const int pg = coded ? pbase / G : 0, off0 = pbase - pg * G;
+    // ---- every load in flight at once: the page (lane 0), each lane's rows ----
+    const bool valid = lane < cnt;
+    const int tt = valid ? (c0 + lane < s_len ? c0 + lane : vbase + (c0 + lane - s_len)) : 0;
+    const int pct = tt - S;
+    const uint32_t bytes = (coded ? kslot : 0) + cnt * (coded ? 256 : 512);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(bytes) : "memory");
+        if (coded)
+            bulk_row(kbuf, c.key_pool + (int64_t)c.key_block_table[(int64_t)u * c.max_pages + pg] * kslot, kslot, bar);
+    }
+    __syncwarp();
+    if (valid) {
+        const uint16_t* ksink = static_cast<const uint16_t*>(c.k_sink);
+        const uint16_t* vsink = static_cast<const uint16_t*>(c.v_sink);
+        const uint16_t* vrow = tt < S ? vsink + ((int64_t)u * S + tt) * D : static_cast<const uint16_t*>(c.v_ring) + ((int64_t)u * W + (pct % W)) * D;
+        bulk_row(vt + lane * kRowH, vrow, 256, bar);
+        if (!coded) {
+            const uint16_t* krow = tt < S ? ksink + ((int64_t)u * S + tt) * D : static_cast<const uint16_t*>(c.k_qbuf) + ((int64_t)u * G + (pct % G)) * D;
+            bulk_row(kt + lane * kRowH, krow, 256, bar);
+        }
+    } else {  // rows past the chunk's tokens: zero values (their p is 0, but 0 x NaN is not)
+        uint4* vz = reinterpret_cast<uint4*>(vt + lane * kRowH);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) vz[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (!coded) {
+            uint4* kz = reinterpret_cast<uint4*>(kt + lane * kRowH);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) kz[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
+    }
+    // B fragments of q (bf16 pairs, exact), while the rows are in flight
+    uint32_t qb[8][2];
+    if (!coded) {
+        const uint16_t* qg = qbase + (gid < GROUP ? gid : 0) * D;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int ch = 16 * ks + 2 * tig;
+            qb[ks][0] = gid < GROUP ? __ldg(reinterpret_cast<const uint32_t*>(qg + ch)) : 0u;
+            qb[ks][1] = gid < GROUP ? __ldg(reinterpret_cast<const uint32_t*>(qg + ch + 8)) : 0u;
+        }
+    }
+    page_wait(bar, 0);
+    __syncwarp();
+    // ---- logits lg[token][query] (log2 domain) ----
+    if (coded) {
+        {
+            const uint32_t bw = *reinterpret_cast<const uint32_t*>(kbuf + D * G / 4 + d_boost * G / 4 + 4 * lane);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t bi = (bw >> (8 * k)) & 0xffu;
+                if (bi < 32u) inv[bi] = static_cast<uint8_t>(4 * lane + k);
+            }
+        }
+        __syncwarp();
+        qk_codes_warp<GROUP>(kbuf, d_boost, off0, qbase, inv, lg);
+    } else {
+        const uint32_t kt_s = static_cast<uint32_t>(__cvta_generic_to_shared(kt));
+        const int i4 = lane >> 3, r8 = lane & 7;
+        float acc[2][4] = {};
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                uint32_t a0, a1, a2, a3;
+                const int row = 16 * mt + r8 + 8 * (i4 & 1), cc = 16 * ks + 8 * (i4 >> 1);
+                ldsm_x4(kt_s + 2 * (row * kRowH + cc), a0, a1, a2, a3);
+                hmma_bf16(acc[mt], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+            }
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            *reinterpret_cast<float2*>(lg + (16 * mt + gid) * 8 + 2 * tig) = make_float2(acc[mt][0] * kAlpha, acc[mt][1] * kAlpha);
+            *reinterpret_cast<float2*>(lg + (16 * mt + 8 + gid) * 8 + 2 * tig) = make_float2(acc[mt][2] * kAlpha, acc[mt][3] * kAlpha);
+        }
+    }
+    __syncwarp();
+    // ---- softmax over the chunk's tokens (lane = token), one query at a time ----
+    float* base = part + ((int64_t)u * nslot + fc) * stride;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        if (g < GROUP) {
+            const float x = valid ? lg[lane * 8 + g] : -INFINITY;
+            float mc = x;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+            const float p = valid ? ex2f(x - mc) : 0.f;
+            float sm = p;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            const __nv_bfloat16 ph = __float2bfloat16_rn(p);
+            const __nv_bfloat16 pl = __float2bfloat16_rn(p - __bfloat162float(ph));
+            pth[g * 40 + lane] = __bfloat16_as_ushort(ph);
+            ptl[g * 40 + lane] = __bfloat16_as_ushort(pl);
+            if (lane == 0) {
+                base[GROUP * D + 2 * g] = mc;
+                base[GROUP * D + 2 * g + 1] = sm;
+            }
+        } else {
+            pth[g * 40 + lane] = 0;
+            ptl[g * 40 + lane] = 0;
+        }
+    }
+    __syncwarp();
+    // ---- P V: out^T [channel][query], A = V^T (ldmatrix.trans), B = p hi / lo ----
+    {
+        const uint32_t vt_s = static_cast<uint32_t>(__cvta_generic_to_shared(vt));
+        const int i4 = lane >> 3, r8 = lane & 7;
+        float acc[8][4] = {};
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(pth + gid * 40 + 16 * ks + 2 * tig);
+            const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(pth + gid * 40 + 16 * ks + 8 + 2 * tig);
+            const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(ptl + gid * 40 + 16 * ks + 2 * tig);
+            const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(ptl + gid * 40 + 16 * ks + 8 + 2 * tig);
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                const int tok = 16 * ks + r8 + 8 * (i4 >> 1), chn = 16 * mt + 8 * (i4 & 1);
+                ldsm_x4_t(vt_s + 2 * (tok * kRowH + chn), a0, a1, a2, a3);
+                hmma_bf16(acc[mt], a0, a1, a2, a3, bh0, bh1);
+                hmma_bf16(acc[mt], a0, a1, a2, a3, bl0, bl1);
+            }
+        }
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            const int ch = 16 * mt + gid;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int g = 2 * tig + j;
+                if (g < GROUP) {
+                    base[g * D + ch] = acc[mt][j];
+                    base[g * D + ch + 8] = acc[mt][2 + j];
+                }
+            }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar_s) : "memory");
+}
+
 }  // namespace fptok
 }  // namespace kitty
