@@ -1002,7 +1002,7 @@ __global__ void __launch_bounds__(128) fp_tokens_kernel(Params P) {
 // The full-precision tokens in the aligned geometries (S a multiple of 32:
 // no chunk mixes staged and paged keys): one warp per 32-token chunk
 // (fptok::chunk_warp), kFpWarps chunks per CTA, no CTA-wide barrier.
-constexpr int kFpWarps = 2;
+constexpr int kFpWarps = 1;  // one chunk per CTA (2: C3 -1.8 %, 4: -3.7 %)
 __host__ __device__ inline int fpw_warp_bytes(int kslot) { return (fptok::cw_warp_bytes(kslot) + 127) & ~127; }
 template <int GROUP>
 __global__ void __launch_bounds__(kFpWarps * 32) fp_warp_kernel(Params P) {

@@ -2,7 +2,9 @@
 (kitty_attention_fast.cu reads them once per process, so each runs in a
 subprocess): the launch order (fp grid first / page grid first), the
 warp-specialised page kernel at every GQA group (the default only at group 8),
-and programmatic dependent launch off.  Every variant must give the same
+programmatic dependent launch off, and the CTA-per-chunk full-precision
+kernel (with and without the shared page / key-tile layout) where the
+warp-per-chunk one is the default.  Every variant must give the same
 answer as the oracle within the attention bar (max-abs 1e-2), on a ragged
 batch with a short and a long (> 128 partial slots) unit."""
 
@@ -51,7 +53,8 @@ print("WORST", worst)
 
 
 @pytest.mark.parametrize("env", [{"KITTY_FPFIRST": "1"}, {"KITTY_FPFIRST": "0"}, {"KITTY_WS": "1"},
-                                 {"KITTY_WS": "0"}, {"KITTY_PDL": "0"}, {"KITTY_WS": "1", "KITTY_FPFIRST": "0"}],
+                                 {"KITTY_WS": "0"}, {"KITTY_PDL": "0"}, {"KITTY_WS": "1", "KITTY_FPFIRST": "0"},
+                                 {"KITTY_FPWARP": "0"}, {"KITTY_FPWARP": "0", "KITTY_FPUNION": "0"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_launch_variant_matches_oracle(cuda, env):
     full = dict(os.environ, **env)
