@@ -474,8 +474,9 @@ __host__ __device__ inline int cw_front_bytes(int kslot) {
     return ((a > kTileBytes ? a : kTileBytes) + 127) & ~127;
 }
 __host__ __device__ inline int cw_warp_bytes(int kslot) {
-    // front (key page | key tile), value tile, logits [32][8] f32, P^T hi / lo [8][40] bf16, barrier
-    return cw_front_bytes(kslot) + kTileBytes + kChunk * 8 * 4 + 2 * 8 * 40 * 2 + 64;
+    // front (key page | key tile; then the logits [32][8] f32 and P^T hi / lo
+    // [8][40] bf16 in its first 2.3 KB once QK has read it), value tile, barrier
+    return cw_front_bytes(kslot) + kTileBytes + 64;
 }
 
 __device__ __forceinline__ void hmma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -559,6 +560,7 @@ __device__ __forceinline__ void qk_codes_warp(const uint8_t* kbuf, int d_boost, 
         sumB[j] = __shfl_sync(0xffffffffu, aux[j], kFull ? tig : (tig & 1));
         cst[j] = kFull ? __shfl_sync(0xffffffffu, aux2[2 + j], tig) : __shfl_sync(0xffffffffu, aux[2 + j], 2 + (tig & 1));
     }
+    __syncwarp();  // every lane is done reading the page (the logits may take its bytes)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int g = 2 * tig + j;
@@ -582,10 +584,10 @@ __device__ void chunk_warp(const KittyCacheDesc& c, const uint16_t* q, float* pa
     uint16_t* kt = reinterpret_cast<uint16_t*>(scratch);  // [32][kRowH] bf16 keys (shares the page's bytes)
     uint8_t* inv = scratch + tc_kbuf_bytes(kslot);
     uint16_t* vt = reinterpret_cast<uint16_t*>(scratch + cw_front_bytes(kslot));  // [32][kRowH] bf16 values
-    float* lg = reinterpret_cast<float*>(vt + kChunk * kRowH);                     // [32][8] logits
-    uint16_t* pth = reinterpret_cast<uint16_t*>(lg + kChunk * 8);                  // [8][40] bf16 p hi
-    uint16_t* ptl = pth + 8 * 40;                                                  // [8][40] bf16 p lo
-    uint64_t* bar = reinterpret_cast<uint64_t*>(ptl + 8 * 40);
+    float* lg = reinterpret_cast<float*>(scratch);                 // [32][8] logits (after QK: over the keys)
+    uint16_t* pth = reinterpret_cast<uint16_t*>(lg + kChunk * 8);  // [8][40] bf16 p hi
+    uint16_t* ptl = pth + 8 * 40;                                  // [8][40] bf16 p lo
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(vt + kChunk * kRowH));
     const uint32_t bar_s = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
     const Geom gm = geom(c, u, max_tokens);
     const int s_len = min(gm.n, S);
@@ -654,7 +656,7 @@ __device__ void chunk_warp(const KittyCacheDesc& c, const uint16_t* q, float* pa
             }
         }
         __syncwarp();
-        qk_codes_warp<GROUP>(kbuf, d_boost, off0, qbase, inv, lg);
+        qk_codes_warp<GROUP>(kbuf, d_boost, off0, qbase, inv, lg);  // lg is written after every read of the page
     } else {
         const uint32_t kt_s = static_cast<uint32_t>(__cvta_generic_to_shared(kt));
         const int i4 = lane >> 3, r8 = lane & 7;
@@ -669,6 +671,7 @@ __device__ void chunk_warp(const KittyCacheDesc& c, const uint16_t* q, float* pa
                 hmma_bf16(acc[mt], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
             }
         }
+        __syncwarp();  // every lane's key-tile reads are done: the logits take those bytes
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
             *reinterpret_cast<float2*>(lg + (16 * mt + gid) * 8 + 2 * tig) = make_float2(acc[mt][0] * kAlpha, acc[mt][1] * kAlpha);
