@@ -1209,10 +1209,11 @@ static const int g_fp_first = [] {
     return e ? std::atoi(e) : -1;
 }();
 
-// page kernel variant (A/B knob KITTY_WS, else per group): 1 = warp-specialised
-// QK / PV pairs (16 warps / SM at <= 128 registers), 0 = one warp per page
-// stream interleaving both (8 warps / SM).  Measured: group 8 (C5) 487.1 vs
-// 490.3 us per layer with pairs; group 4 (C2) 105.5 vs 105.2, C4 38.3 vs 37.7.
+// page kernel variant (A/B knob KITTY_WS): 1 = warp-specialised QK / PV pairs
+// (16 warps / SM at <= 128 registers), 0 (default) = one warp per page stream
+// interleaving both (8 warps / SM).  Pairs won at group 8 (C5 490.3 vs 487.9
+// us per layer) until the fp-token and merge work shrank; with the final
+// kernels one warp per stream is ahead there too (C5 3 746 vs 3 698 tok/s).
 static const int g_ws_env = [] {
     const char* e = std::getenv("KITTY_WS");
     return e ? std::atoi(e) : -1;
@@ -1220,7 +1221,7 @@ static const int g_ws_env = [] {
 
 template <int GROUP, int NKH>
 static cudaError_t launch_t(const Params& prm, int grid, cudaStream_t st) {
-    const bool g_ws = g_ws_env >= 0 ? g_ws_env != 0 : GROUP == 8;
+    const bool g_ws = g_ws_env > 0;
     auto kfn = g_ws ? page_kernel<GROUP, NKH, true> : page_kernel<GROUP, NKH, false>;
     const int ks_b = (int)prm.c.key_slot_bytes, vs_b = (int)prm.c.value_slot_bytes;
     const size_t sm = (size_t)(g_ws ? pair_smem_bytes<GROUP>(ks_b, vs_b) * kWsPairs : warp_smem_bytes<GROUP>(ks_b, vs_b) * kWarps) +
