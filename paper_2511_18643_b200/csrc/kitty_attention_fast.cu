@@ -185,6 +185,16 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_last4(float* p, float a, float b, float c, float d, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d),
+                 "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar,
                                          uint64_t pol) {
     asm volatile(
@@ -496,6 +506,7 @@ __global__ void __launch_bounds__(WS ? 2 * kWsPairs * 32 : kWarps * 32, kCtasPer
     // one page ahead of PV, so a key page is issued one page earlier than its
     // value page: each gets a full iteration of load time.
     const uint64_t pol = l2_evict_first();
+    const uint64_t pol_last = l2_evict_last();
     auto issue_key = [&](const Pg& d, int sl) {
         if (lane == 0 && d.u >= 0) {
             mbar_expect_tx(&sm.kfull[sl], kslot);
@@ -776,12 +787,13 @@ __global__ void __launch_bounds__(WS ? 2 * kWsPairs * 32 : kWarps * 32, kCtasPer
                         lo[m] = fmaf(oacc[m][j], 1.f / tile_w(m), ob[tile_c(m)][j]);
                         hi[m] = fmaf(oacc[m][2 + j], 1.f / tile_w(m), ob[tile_c(m)][j]);
                     }
-                    float4* o4 = reinterpret_cast<float4*>(base + g * D + 8 * gid);
-                    o4[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
-                    o4[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
-                    float4* h4 = reinterpret_cast<float4*>(base + g * D + 64 + 8 * gid);
-                    h4[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                    h4[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+                    // the record is re-read by the merge right after: keep it in L2
+                    float* o4 = base + g * D + 8 * gid;
+                    st_last4(o4, lo[0], lo[1], lo[2], lo[3], pol_last);
+                    st_last4(o4 + 4, lo[4], lo[5], lo[6], lo[7], pol_last);
+                    float* h4 = base + g * D + 64 + 8 * gid;
+                    st_last4(h4, hi[0], hi[1], hi[2], hi[3], pol_last);
+                    st_last4(h4 + 4, hi[4], hi[5], hi[6], hi[7], pol_last);
                     if (gid == 0) *reinterpret_cast<float2*>(base + GROUP * D + 2 * g) = make_float2(mnew[j], ol[j]);
                 }
             }
